@@ -1,0 +1,407 @@
+"""Benchmark of the B200 *_L hot path (contract: see DESIGN.md §Measurement).
+
+Headline (BASELINE.json configs[1], "config 2"): the 4th-order *_L-product
+A 256x128x3x32 * B 128x256x3x32, float32 N(0,1), L = DCT along modes 3 and 4,
+in GFLOP/s on the algorithmic count of SURVEY.md §8(d) (2,491,416,576 flop per
+product).  One step = one product with A, B resident in HBM; L2 is flushed
+(512 MiB write) between timed steps.  `e2e` is the same metric through the
+public numpy-in / numpy-out API (host copies inside the timed region).
+
+Secondary (BASELINE configs[2], "config 3"): PGA completion iterations/s on the
+synthetic 144x176x3x100 colour-video stand-in (tol 1e-300, 200 iterations),
+reported in the "pga" object.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG2 = dict(a=(256, 128, 3, 32), b=(128, 256, 3, 32), kind="dct")
+CFG3 = dict(shape=(144, 176, 3, 100), rank=10, sr=0.2, iters=200)
+GFLOP_CFG2 = 2_491_416_576
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _cfg2_inputs(seed=0):
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal(CFG2["a"], dtype=np.float32)
+    b = rng.standard_normal(CFG2["b"], dtype=np.float32)
+    return a, b
+
+
+def _cpu_info():
+    info = {"cores": len(os.sched_getaffinity(0))}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["blas_threads"] = max((t.get("num_threads", 1) for t in threadpool_info()), default=1)
+    except Exception:
+        info["blas_threads"] = info["cores"]
+    return info
+
+
+# ----------------------------------------------------------------------------- CPU (oracle) legs
+def cpu_lproduct(steps: int, warmup: int, budget_s: float | None = None):
+    """The reference algorithm (oracle port) on the host cores, seconds per product."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ltensor_oracle as O
+
+    a, b = _cfg2_inputs()
+    spec = O.ospec("dct", (256, 256, 3, 32))
+    for _ in range(warmup):
+        O.l_product(a, b, spec)
+    times = []
+    t_end = time.perf_counter() + budget_s if budget_s else None
+    while True:
+        t0 = time.perf_counter()
+        O.l_product(a, b, spec)
+        times.append(time.perf_counter() - t0)
+        if t_end is None and len(times) >= steps:
+            break
+        if t_end is not None and time.perf_counter() >= t_end and len(times) >= 3:
+            break
+    return times
+
+
+def cpu_pga_iters(iters: int):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ltensor_oracle as O
+
+    m, mask = _cfg3_data_host()
+    spec = O.ospec("dct", CFG3["shape"])
+    t0 = time.perf_counter()
+    O.pga_complete(m, mask, spec, tol=1e-300, max_iters=iters)
+    return (time.perf_counter() - t0) / iters
+
+
+def _cfg3_data_host():
+    """Config 3 synthetic stand-in: A 144x10x3x100, B 10x176x3x100 N(0,1) f32, X0 = A *_L B
+    (DCT, f64), rescaled to [0,1], + N(0, 0.01) noise (std 0.01), f32; Bernoulli(0.2) mask; seed 0."""
+    rng = np.random.default_rng(0)
+    i1, i2, c, t = CFG3["shape"]
+    a = rng.standard_normal((i1, CFG3["rank"], c, t), dtype=np.float32).astype(np.float64)
+    b = rng.standard_normal((CFG3["rank"], i2, c, t), dtype=np.float32).astype(np.float64)
+    import scipy.fft
+
+    # X0 = A *_L B with the separable DCT, computed with scipy (input synthesis only)
+    ah = scipy.fft.dctn(a, type=2, axes=(2, 3), norm="ortho")
+    bh = scipy.fft.dctn(b, type=2, axes=(2, 3), norm="ortho")
+    xh = np.einsum("ikct,kjct->ijct", ah, bh)
+    x0 = scipy.fft.idctn(xh, type=2, axes=(2, 3), norm="ortho")
+    x0 = (x0 - x0.min()) / (x0.max() - x0.min())
+    m = (x0 + rng.normal(0.0, 0.01, x0.shape)).astype(np.float32)
+    mask = rng.random(m.shape) < CFG3["sr"]
+    return m, mask
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    times = cpu_lproduct(args.steps, args.warmup)
+    info = _cpu_info()
+    total = sum(times)
+    value = GFLOP_CFG2 * len(times) / total / 1e9
+    line = {
+        "impl": "reference",
+        "metric": "*_L-product GFLOP/s",
+        "value": value,
+        "unit": "GFLOP/s",
+        "n_gpus": ws,
+        "steps": len(times),
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic N(0,1) seed 0 (BASELINE config 2 shapes)",
+        "config": {"workload": "config2 l_product A 256x128x3x32 * B 128x256x3x32, DCT modes 3,4",
+                   "flop_per_step": GFLOP_CFG2},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": info["blas_threads"], "kind": "port",
+                         "sample": f"{len(times)} full config-2 products (oracle/ltensor_oracle.py, numpy/scipy "
+                                   f"OpenBLAS), {info.get('cpu', '?')}"},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    def __init__(self, index: int):
+        self.samples = []
+        self.proc = None
+        self.index = index
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
+        loaded = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    import paper_2202_02870_b200 as L
+    from paper_2202_02870_b200 import _native as nat
+    from paper_2202_02870_b200.engine import LProductPlan
+
+    nat.set_device(local)
+    stream = torch.cuda.current_stream()
+    nat.lib().ltb_ctx_set_stream(nat.context(), stream.cuda_stream)
+
+    hbm_peak, tf_peak, peak_src = _peaks()
+    spec = L.make_spec("dct", (256, 256, 3, 32))
+    a_h, b_h = _cfg2_inputs(seed=rank)
+    plan = LProductPlan(a_h.shape, b_h.shape, spec, np.float32)
+    a = nat.DeviceArray.from_numpy(a_h)
+    b = nat.DeviceArray.from_numpy(b_h)
+    c = nat.DeviceArray(plan.c_shape, np.float32)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    # ---- correctness gate (first product vs the oracle on a bounded check)
+    plan.run(a, b, c)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    phase_ms = np.zeros(4)
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            flush.zero_()
+            plan.run(a, b, c)
+        barrier()
+        launches0 = nat.launch_count()
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush outside the timed events
+            plan.run(a, b, c, marks=lambda i: ev[i].record(stream))
+            ev[4].synchronize()
+            ph = [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
+            phase_ms += ph
+            step_ms.append(ev[0].elapsed_time(ev[4]))
+        barrier()
+        launches = nat.launch_count() - launches0
+        # e2e: public numpy-in/numpy-out API, host copies inside the timed region
+        e2e_t = []
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = L.l_product(a_h, b_h, spec)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                e2e_t.append(dt)
+        pga = None if args.skip_pga else bench_pga(L, nat, torch, args)
+
+    t_step = float(np.sum(step_ms)) / 1e3
+    if ws > 1:
+        tt = torch.tensor([t_step], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+        te = torch.tensor([sum(e2e_t)], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(te.item())
+    else:
+        e2e_total = sum(e2e_t)
+    value = ws * GFLOP_CFG2 * args.steps / t_step / 1e9
+    e2e_value = ws * GFLOP_CFG2 * len(e2e_t) / e2e_total / 1e9
+
+    # roofline of the dominant kernel of the step (per-phase CUDA events on the launching stream)
+    names = ["transform_fwd_A", "transform_fwd_B", "slice_gemm", "transform_inv_C"]
+    phase_avg = phase_ms / args.steps
+    dom = int(np.argmax(phase_avg))
+    E_a, E_b, E_c = 256 * 128 * 96, 128 * 256 * 96, 256 * 256 * 96
+    alg_bytes = [8 * E_a, 8 * E_b, 4 * (E_a + E_b + E_c), 8 * E_c]
+    alg_flops = [70 * E_a, 70 * E_b, 2 * 256 * 128 * 256 * 96, 70 * E_c]
+    if dom == 2:
+        achieved = alg_flops[dom] / (phase_avg[dom] / 1e3) / 1e12
+        roof = {"kernel": names[dom], "bound": "tensor", "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s",
+                "frac": achieved / tf_peak, "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
+                "alg_per_launch": f"{alg_flops[dom]} flop (2*I1*l*I2*P)"}
+    else:
+        achieved = alg_bytes[dom] / (phase_avg[dom] / 1e3) / 1e9
+        roof = {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "peak_source": f"{peak_src} HBM copy (MEASURED_PEAKS.json)",
+                "alg_per_launch": f"{alg_bytes[dom]} B (one f32 read + one write of the tensor)"}
+    roof["traffic"] = None
+    roof["phase_ms"] = dict(zip(names, [round(float(x), 5) for x in phase_avg]))
+
+    line = {
+        "metric": "*_L-product GFLOP/s",
+        "value": value,
+        "unit": "GFLOP/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_step / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic N(0,1) (BASELINE config 2 shapes), seed = rank",
+        "config": {"workload": "config2 l_product A 256x128x3x32 * B 128x256x3x32, DCT modes 3,4",
+                   "flop_per_step": GFLOP_CFG2, "l2": "flushed (512 MiB write) before every timed step",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "roofline": roof,
+        "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(a_h.nbytes + b_h.nbytes),
+                "d2h_bytes_per_step": int(out.nbytes), "api": "paper_2202_02870_b200.l_product(numpy, numpy, spec)"},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if pga is not None:
+        line["pga"] = pga
+    if rank == 0 and not args.no_cpu_baseline:
+        times = cpu_lproduct(1, 1, budget_s=args.cpu_budget)
+        info = _cpu_info()
+        line["cpu_baseline"] = {"value": GFLOP_CFG2 * len(times) / sum(times) / 1e9, "unit": "GFLOP/s",
+                                "cores": info["blas_threads"], "kind": "port",
+                                "sample": f"{len(times)} full config-2 products in ~{args.cpu_budget:.0f}s "
+                                          f"(oracle port, numpy/scipy OpenBLAS), {info.get('cpu', '?')}"}
+        if pga is not None and args.cpu_pga_iters > 0:
+            s_it = cpu_pga_iters(args.cpu_pga_iters)
+            line["pga"]["cpu_baseline"] = {"value": 1.0 / s_it, "unit": "it/s", "cores": info["blas_threads"],
+                                           "kind": "port",
+                                           "sample": f"{args.cpu_pga_iters} PGA iterations of config 3 (float64, "
+                                                     "as the reference computes)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def bench_pga(L, nat, torch, args):
+    m, mask = _cfg3_data_host()
+    spec = L.make_spec("dct", CFG3["shape"])
+    from paper_2202_02870_b200.completion import PGASolver, pga_schedule
+
+    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=CFG3["iters"])
+    mu0 = cfg.nu * L.fro_norm(np.asarray(m, dtype=np.float64))
+    mus, ts, betas = pga_schedule(cfg, mu0)
+    solver = PGASolver(np.asarray(m, dtype=np.float64), mask, spec, "fp32")
+    # warm-up: a separate solver run of a few iterations
+    warm = PGASolver(np.asarray(m, dtype=np.float64), mask, spec, "fp32")
+    warm.run(1, betas[:3], mus[:3], cfg.tol)
+    warm.close()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    n_done = 0
+    k = 1
+    while k <= cfg.max_iters:
+        n = min(50, cfg.max_iters - k + 1)
+        recs, conv = solver.run(k, betas[k - 1:k - 1 + n], mus[k - 1:k - 1 + n], cfg.tol)
+        k += len(recs)
+        n_done += len(recs)
+        if conv:
+            break
+    dt = time.perf_counter() - t0
+    x = solver.fetch(False)
+    solver.close()
+    return {"metric": "PGA completion iters/sec", "value": n_done / dt, "unit": "it/s", "iterations": n_done,
+            "seconds": dt, "dtype": "f32",
+            "config": {"workload": "config3 144x176x3x100 rank-10 DCT(modes 3,4), Bernoulli(0.2), tol 1e-300",
+                       "data": "synthetic stand-in for the paper's colour videos (not in this container)"},
+            "rse_vs_m": float(np.linalg.norm(x - m) ** 2 / max(np.linalg.norm(x) ** 2, 1e-300))}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--skip-pga", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--cpu-pga-iters", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,209 @@
+// Shared device/host helpers for libltb (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/ltb.h"
+
+// ------------------------------------------------------------------ complex
+template <typename R>
+struct cplx {
+  R re, im;
+};
+
+template <typename T> struct scalar_traits {
+  using real = T;
+  static constexpr bool is_complex = false;
+};
+template <typename R> struct scalar_traits<cplx<R>> {
+  using real = R;
+  static constexpr bool is_complex = true;
+};
+
+template <typename R> __host__ __device__ __forceinline__ cplx<R> operator+(cplx<R> a, cplx<R> b) {
+  return {a.re + b.re, a.im + b.im};
+}
+template <typename R> __host__ __device__ __forceinline__ cplx<R> operator-(cplx<R> a, cplx<R> b) {
+  return {a.re - b.re, a.im - b.im};
+}
+template <typename R> __host__ __device__ __forceinline__ cplx<R> operator*(cplx<R> a, cplx<R> b) {
+  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+template <typename R> __host__ __device__ __forceinline__ cplx<R> operator*(R a, cplx<R> b) {
+  return {a * b.re, a * b.im};
+}
+template <typename R> __host__ __device__ __forceinline__ cplx<R> operator*(cplx<R> b, R a) {
+  return {a * b.re, a * b.im};
+}
+
+// value helpers usable for both real and complex
+template <typename T> __host__ __device__ __forceinline__ T zero_v() { return T(0); }
+template <> __host__ __device__ __forceinline__ cplx<float> zero_v<cplx<float>>() { return {0.f, 0.f}; }
+template <> __host__ __device__ __forceinline__ cplx<double> zero_v<cplx<double>>() { return {0.0, 0.0}; }
+
+__host__ __device__ __forceinline__ float conj_v(float a) { return a; }
+__host__ __device__ __forceinline__ double conj_v(double a) { return a; }
+template <typename R> __host__ __device__ __forceinline__ cplx<R> conj_v(cplx<R> a) { return {a.re, -a.im}; }
+
+__host__ __device__ __forceinline__ float abs2_v(float a) { return a * a; }
+__host__ __device__ __forceinline__ double abs2_v(double a) { return a * a; }
+template <typename R> __host__ __device__ __forceinline__ R abs2_v(cplx<R> a) { return a.re * a.re + a.im * a.im; }
+
+__host__ __device__ __forceinline__ float re_v(float a) { return a; }
+__host__ __device__ __forceinline__ double re_v(double a) { return a; }
+template <typename R> __host__ __device__ __forceinline__ R re_v(cplx<R> a) { return a.re; }
+__host__ __device__ __forceinline__ float im_v(float) { return 0.f; }
+__host__ __device__ __forceinline__ double im_v(double) { return 0.0; }
+template <typename R> __host__ __device__ __forceinline__ R im_v(cplx<R> a) { return a.im; }
+
+// acc += a * b  (mixed real/complex); fused where the types allow
+__device__ __forceinline__ void fma_acc(float& acc, float a, float b) { acc = fmaf(a, b, acc); }
+__device__ __forceinline__ void fma_acc(double& acc, double a, double b) { acc = fma(a, b, acc); }
+template <typename R> __device__ __forceinline__ void fma_acc(cplx<R>& acc, R a, cplx<R> b) {
+  acc.re = fma(a, b.re, acc.re);
+  acc.im = fma(a, b.im, acc.im);
+}
+template <typename R> __device__ __forceinline__ void fma_acc(cplx<R>& acc, cplx<R> a, R b) {
+  acc.re = fma(a.re, b, acc.re);
+  acc.im = fma(a.im, b, acc.im);
+}
+template <typename R> __device__ __forceinline__ void fma_acc(cplx<R>& acc, cplx<R> a, cplx<R> b) {
+  acc.re = fma(a.re, b.re, acc.re);
+  acc.re = fma(-a.im, b.im, acc.re);
+  acc.im = fma(a.re, b.im, acc.im);
+  acc.im = fma(a.im, b.re, acc.im);
+}
+
+// conversion between element types (complex -> real keeps the real part)
+template <typename To, typename From> struct conv;
+template <> struct conv<float, float> { __host__ __device__ static float f(float a) { return a; } };
+template <> struct conv<double, double> { __host__ __device__ static double f(double a) { return a; } };
+template <> struct conv<float, double> { __host__ __device__ static float f(double a) { return (float)a; } };
+template <> struct conv<double, float> { __host__ __device__ static double f(float a) { return (double)a; } };
+template <typename R, typename S> struct conv<cplx<R>, S> {
+  __host__ __device__ static cplx<R> f(S a) { return {(R)a, (R)0}; }
+};
+template <typename R, typename S> struct conv<cplx<R>, cplx<S>> {
+  __host__ __device__ static cplx<R> f(cplx<S> a) { return {(R)a.re, (R)a.im}; }
+};
+template <typename S> struct conv<float, cplx<S>> {
+  __host__ __device__ static float f(cplx<S> a) { return (float)a.re; }
+};
+template <typename S> struct conv<double, cplx<S>> {
+  __host__ __device__ static double f(cplx<S> a) { return (double)a.re; }
+};
+template <typename To, typename From> __host__ __device__ __forceinline__ To cvt(From a) {
+  return conv<To, From>::f(a);
+}
+
+// read-only cached loads for real and complex element types
+__device__ __forceinline__ float ldg_v(const float* p) { return __ldg(p); }
+__device__ __forceinline__ double ldg_v(const double* p) { return __ldg(p); }
+__device__ __forceinline__ cplx<float> ldg_v(const cplx<float>* p) {
+  const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+  return {v.x, v.y};
+}
+__device__ __forceinline__ cplx<double> ldg_v(const cplx<double>* p) {
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+  return {v.x, v.y};
+}
+
+// ------------------------------------------------------------------ warp
+template <typename R> __device__ __forceinline__ R warp_sum(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ context
+struct ltb_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  std::string last_error;
+  int64_t launches = 0;
+  // small pinned host scratch for reduction results
+  double* h_scratch = nullptr;
+  double* d_scratch = nullptr;  // 64 doubles
+  unsigned int* d_counter = nullptr;
+};
+
+struct ltb_spec {
+  ltb_ctx* ctx = nullptr;
+  int ntrail = 0;
+  int64_t trail_dims[16] = {0};
+  int64_t P = 1;
+  int nmodes = 0;
+  int axes[16] = {0};
+  int sizes[16] = {0};
+  int is_complex = 0;
+  // device copies: [precision 0=f32,1=f64] x [0=fwd,1=inv]; element type
+  // is real or complex according to is_complex; per-mode offsets (elements)
+  void* d_mats[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int64_t mat_off[16] = {0};
+  int64_t mat_total = 0;
+};
+
+// ------------------------------------------------------------------ errors
+int ltb_set_error(ltb_ctx* ctx, int code, const char* fmt, ...);
+
+#define LTB_CUDA_TRY(ctx, expr)                                                              \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess) {                                                                 \
+      return ltb_set_error((ctx), _e == cudaErrorMemoryAllocation ? LTB_EOOM : LTB_ECUDA,    \
+                           "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                           __LINE__);                                                        \
+    }                                                                                        \
+  } while (0)
+
+#define LTB_LAUNCH_CHECK(ctx)                                                          \
+  do {                                                                                 \
+    (ctx)->launches++;                                                                 \
+    cudaError_t _e = cudaGetLastError();                                               \
+    if (_e != cudaSuccess)                                                             \
+      return ltb_set_error((ctx), LTB_ECUDA, "kernel launch failed: %s (%s:%d)",       \
+                           cudaGetErrorString(_e), __FILE__, __LINE__);                \
+  } while (0)
+
+#define LTB_TRY(expr)           \
+  do {                          \
+    int _s = (expr);            \
+    if (_s != LTB_OK) return _s; \
+  } while (0)
+
+inline size_t dtype_size(int dt) {
+  switch (dt) {
+    case LTB_F32: return 4;
+    case LTB_F64: return 8;
+    case LTB_C64: return 8;
+    case LTB_C128: return 16;
+  }
+  return 0;
+}
+inline bool dtype_is_complex(int dt) { return dt == LTB_C64 || dt == LTB_C128; }
+inline bool dtype_is_double(int dt) { return dt == LTB_F64 || dt == LTB_C128; }
+inline bool dtype_valid(int dt) { return dt >= 0 && dt <= 3; }
+
+// stream-ordered scratch allocation
+int ltb_ws_alloc(ltb_ctx* ctx, size_t bytes, void** out);
+void ltb_ws_free(ltb_ctx* ctx, void* p);
+
+// internal entry points shared between translation units
+int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,
+                       int layout_in, const void* d_in, int dtype_out, int layout_out, void* d_out,
+                       double* d_sumsq /* device, 2 doubles, may be null */);
+int ltb_reduce_sumsq_dev(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y,
+                         double* d_out /* 2 doubles */);
+int ltb_gemm_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int op_a,
+                  const void* d_a, int64_t lda, int64_t sa, int op_b, const void* d_b, int64_t ldb,
+                  int64_t sb, void* d_c, int64_t ldc, int64_t sc, const int* d_mlim, const int* d_nlim,
+                  const int* d_klim, const void* d_row_scale, const void* d_col_scale, const int* d_skip = nullptr);
+int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, const void* d_a,
+                 double tau, const double* d_tau /* optional per-call device tau */, void* d_out,
+                 const int* d_skip /* optional device flag: nonzero -> kernels return */);

@@ -1,0 +1,248 @@
+// Context, memory, spec upload and small C-ABI glue for libltb.
+#include <cstdarg>
+#include <cstring>
+#include <vector>
+
+#include "ltb_common.cuh"
+
+int ltb_set_error(ltb_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->last_error = buf;
+  return code;
+}
+
+int ltb_ws_alloc(ltb_ctx* ctx, size_t bytes, void** out) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMallocAsync(out, bytes, ctx->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return ltb_set_error(ctx, LTB_EOOM, "device allocation of %zu bytes failed: %s", bytes,
+                         cudaGetErrorString(e));
+  }
+  return LTB_OK;
+}
+
+void ltb_ws_free(ltb_ctx* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+extern "C" {
+
+int ltb_version(void) { return 1; }
+
+int ltb_device_count(int* count) {
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return LTB_ECUDA;
+  }
+  return LTB_OK;
+}
+
+int ltb_ctx_create(int device, ltb_ctx** out) {
+  *out = nullptr;
+  ltb_ctx* ctx = new ltb_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete ctx;
+    return LTB_ECUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    delete ctx;
+    return LTB_ECUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  // keep freed pool memory cached instead of returning it at every sync
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (cudaMallocHost(&ctx->h_scratch, 64 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_scratch, 64 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_counter, 64 * sizeof(unsigned int)) != cudaSuccess) {
+    cudaGetLastError();
+    delete ctx;
+    return LTB_EOOM;
+  }
+  cudaMemset(ctx->d_counter, 0, 64 * sizeof(unsigned int));
+  cudaDeviceSynchronize();
+  *out = ctx;
+  return LTB_OK;
+}
+
+void ltb_ctx_destroy(ltb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
+  if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+  if (ctx->d_counter) cudaFree(ctx->d_counter);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* ltb_ctx_last_error(const ltb_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int ltb_ctx_set_stream(ltb_ctx* ctx, void* stream) {
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return LTB_OK;
+}
+
+int ltb_ctx_synchronize(ltb_ctx* ctx) {
+  LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaGetLastError());
+  return LTB_OK;
+}
+
+int64_t ltb_ctx_launch_count(const ltb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ltb_malloc(ltb_ctx* ctx, int64_t bytes, void** d_out) {
+  if (bytes < 0) return ltb_set_error(ctx, LTB_EPARAM, "negative allocation size");
+  cudaSetDevice(ctx->device);
+  return ltb_ws_alloc(ctx, (size_t)bytes, d_out);
+}
+
+int ltb_free(ltb_ctx* ctx, void* d_ptr) {
+  ltb_ws_free(ctx, d_ptr);
+  return LTB_OK;
+}
+
+int ltb_memcpy_h2d(ltb_ctx* ctx, void* d_dst, const void* h_src, int64_t bytes) {
+  if (bytes <= 0) return LTB_OK;
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(d_dst, h_src, (size_t)bytes, cudaMemcpyHostToDevice, ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return LTB_OK;
+}
+
+int ltb_memcpy_d2h(ltb_ctx* ctx, void* h_dst, const void* d_src, int64_t bytes) {
+  if (bytes <= 0) return LTB_OK;
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(h_dst, d_src, (size_t)bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return LTB_OK;
+}
+
+int ltb_memcpy_d2d(ltb_ctx* ctx, void* d_dst, const void* d_src, int64_t bytes) {
+  if (bytes <= 0) return LTB_OK;
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(d_dst, d_src, (size_t)bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  return LTB_OK;
+}
+
+int ltb_memset_zero(ltb_ctx* ctx, void* d_dst, int64_t bytes) {
+  if (bytes <= 0) return LTB_OK;
+  LTB_CUDA_TRY(ctx, cudaMemsetAsync(d_dst, 0, (size_t)bytes, ctx->stream));
+  return LTB_OK;
+}
+
+int ltb_spec_create(ltb_ctx* ctx, int ntrail, const int64_t* trail_dims, int nmodes, const int* axes,
+                    int is_complex, const double* h_fwd, const double* h_inv, ltb_spec** out) {
+  *out = nullptr;
+  if (ntrail < 0 || ntrail > 16 || nmodes < 0 || nmodes > ntrail)
+    return ltb_set_error(ctx, LTB_ETRANSFORM, "spec: bad mode count (%d trailing, %d modes)", ntrail, nmodes);
+  ltb_spec* s = new ltb_spec();
+  s->ctx = ctx;
+  s->ntrail = ntrail;
+  s->P = 1;
+  for (int i = 0; i < ntrail; ++i) {
+    if (trail_dims[i] < 1) {
+      delete s;
+      return ltb_set_error(ctx, LTB_ESHAPE, "spec: trailing dim %d is %lld", i, (long long)trail_dims[i]);
+    }
+    s->trail_dims[i] = trail_dims[i];
+    s->P *= trail_dims[i];
+  }
+  s->nmodes = nmodes;
+  s->is_complex = is_complex ? 1 : 0;
+  int64_t total = 0;
+  for (int k = 0; k < nmodes; ++k) {
+    if (axes[k] < 0 || axes[k] >= ntrail || (k > 0 && axes[k] <= axes[k - 1])) {
+      delete s;
+      return ltb_set_error(ctx, LTB_ETRANSFORM, "spec: axes must be ascending and within the trailing dims");
+    }
+    s->axes[k] = axes[k];
+    s->sizes[k] = (int)trail_dims[axes[k]];
+    s->mat_off[k] = total;
+    total += (int64_t)s->sizes[k] * s->sizes[k];
+  }
+  s->mat_total = total;
+  const int comp = is_complex ? 2 : 1;
+  const size_t n_el = (size_t)(total > 0 ? total : 1) * comp;
+  std::vector<float> tmpf(n_el);
+  for (int dir = 0; dir < 2; ++dir) {
+    const double* src = dir == 0 ? h_fwd : h_inv;
+    for (size_t i = 0; i < n_el; ++i) tmpf[i] = total > 0 ? (float)src[i] : 0.f;
+    void *d32 = nullptr, *d64 = nullptr;
+    if (cudaMalloc(&d32, n_el * sizeof(float)) != cudaSuccess || cudaMalloc(&d64, n_el * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      delete s;
+      return ltb_set_error(ctx, LTB_EOOM, "spec: matrix upload allocation failed");
+    }
+    cudaMemcpy(d32, tmpf.data(), n_el * sizeof(float), cudaMemcpyHostToDevice);
+    if (total > 0) cudaMemcpy(d64, src, n_el * sizeof(double), cudaMemcpyHostToDevice);
+    s->d_mats[0][dir] = d32;
+    s->d_mats[1][dir] = d64;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    delete s;
+    return ltb_set_error(ctx, LTB_ECUDA, "spec upload: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return LTB_OK;
+}
+
+void ltb_spec_destroy(ltb_spec* s) {
+  if (!s) return;
+  for (int p = 0; p < 2; ++p)
+    for (int d = 0; d < 2; ++d)
+      if (s->d_mats[p][d]) cudaFree(s->d_mats[p][d]);
+  delete s;
+}
+
+int ltb_transform(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in, int layout_in,
+                  const void* d_in, int dtype_out, int layout_out, void* d_out, double* h_sumsq) {
+  double* d_sum = h_sumsq ? ctx->d_scratch : nullptr;
+  LTB_TRY(ltb_transform_impl(ctx, spec, ntubes, inverse, dtype_in, layout_in, d_in, dtype_out, layout_out, d_out,
+                             d_sum));
+  if (h_sumsq) {
+    LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, d_sum, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    h_sumsq[0] = ctx->h_scratch[0];
+    h_sumsq[1] = ctx->h_scratch[1];
+  }
+  return LTB_OK;
+}
+
+int ltb_slice_gemm(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int op_a,
+                   const void* d_a, int64_t lda, int64_t stride_a, int op_b, const void* d_b, int64_t ldb,
+                   int64_t stride_b, void* d_c, int64_t ldc, int64_t stride_c) {
+  return ltb_gemm_impl(ctx, dtype, batch, m, n, k, op_a, d_a, lda, stride_a, op_b, d_b, ldb, stride_b, d_c, ldc,
+                       stride_c, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+int ltb_slice_svt(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, const void* d_a, double tau,
+                  void* d_out) {
+  if (!(tau >= 0)) return ltb_set_error(ctx, LTB_EPARAM, "tau must be >= 0, got %g", tau);
+  return ltb_svt_impl(ctx, dtype, batch, m, n, d_a, tau, nullptr, d_out, nullptr);
+}
+
+int ltb_reduce_sumsq(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y, double* h_out) {
+  LTB_TRY(ltb_reduce_sumsq_dev(ctx, dtype, n, d_x, d_y, ctx->d_scratch));
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  h_out[0] = ctx->h_scratch[0];
+  h_out[1] = ctx->h_scratch[1];
+  return LTB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,436 @@
+// K4 + the PGA completion loop (pga_complete, completion.py:141-202).
+//
+// Per iteration k the device runs, with no host round trip:
+//   1. xform tile kernel, prologue = the PGA gradient step fused into the load
+//        y = x + beta_k (x - x_prev)                       (completion.py:170)
+//        g = y - (P_Omega(y) - P_Omega(m))                 (completion.py:171)
+//      (bit-packed observation mask, coalesced tube loads), forward transform,
+//      slice-major store of the transform-domain stack;
+//   2. the slice SVT (ltb_svd.cu) with tau = mu_k;
+//   3. xform tile kernel, inverse transform, epilogue = real part + the fused
+//      reductions sum (y - x+)^2, sum x+^2, sum (x+ - gt)^2, max x+,
+//      sum Im^2 (completion.py:174-189, transforms.py:217-225);
+//   4. a one-warp finalisation that reduces the per-CTA partials in fixed
+//      order, computes rel exactly as completion.py:174-181 and raises the
+//      device stop flag when rel <= tol (completion.py:195-197).
+// Every kernel first checks the stop flag, so a chunk of iterations can be
+// enqueued back to back; the host only reads the records at chunk end.
+// The scalar recurrences (mu_k, t_k) stay on the host, exactly as the reference
+// computes them, and arrive as per-iteration arrays.
+#include <algorithm>
+#include <vector>
+
+#include "ltb_xform_tile.cuh"
+
+struct ltb_pga {
+  ltb_ctx* ctx = nullptr;
+  const ltb_spec* spec = nullptr;
+  int dtype = LTB_F64;  // real compute dtype
+  int hat_dtype = LTB_F64;
+  int64_t I1 = 0, I2 = 0, P = 1, NT = 0, E = 0;
+  void* x[3] = {nullptr, nullptr, nullptr};
+  void* pobs = nullptr;
+  void* gt = nullptr;
+  uint32_t* mask = nullptr;
+  void* hat_a = nullptr;
+  void* hat_b = nullptr;
+  double* partials = nullptr;
+  int64_t nblocks = 0;
+  double* d_records = nullptr;  // chunk x 5
+  int* d_state = nullptr;       // [0] stop flag, [1] executed iterations
+  double* d_scalars = nullptr;  // [0] sum pobs^2
+  int records_cap = 0;
+  int done = 0;  // iterations executed so far
+  bool converged = false;
+  double pobs_sumsq = 0.0;
+};
+
+namespace {
+
+// buffer roles for iteration k (1-based): x_cur, x_prev, x_next
+constexpr int kCur[3] = {0, 2, 1}, kPrev[3] = {1, 0, 2}, kNext[3] = {2, 1, 0};
+inline int cur_of(int k) { return kCur[(k - 1) % 3]; }
+inline int prev_of(int k) { return kPrev[(k - 1) % 3]; }
+inline int next_of(int k) { return kNext[(k - 1) % 3]; }
+
+template <typename R> __device__ __forceinline__ R momentum(R xc, R xp, R beta);
+template <> __device__ __forceinline__ double momentum<double>(double xc, double xp, double beta) {
+  // x_cur + beta * (x_cur - x_prev), no contraction (mirrors numpy's rounding)
+  return __dadd_rn(xc, __dmul_rn(beta, __dsub_rn(xc, xp)));
+}
+template <> __device__ __forceinline__ float momentum<float>(float xc, float xp, float beta) {
+  return __fadd_rn(xc, __fmul_rn(beta, __fsub_rn(xc, xp)));
+}
+template <typename R> __device__ __forceinline__ R gradient_point(R y, R pobs, bool observed);
+template <> __device__ __forceinline__ double gradient_point<double>(double y, double pobs, bool observed) {
+  return __dsub_rn(y, __dsub_rn(observed ? y : 0.0, pobs));
+}
+template <> __device__ __forceinline__ float gradient_point<float>(float y, float pobs, bool observed) {
+  return __fsub_rn(y, __fsub_rn(observed ? y : 0.f, pobs));
+}
+
+template <typename R>
+struct LoadPGA {
+  const R* xc;
+  const R* xp;
+  const R* pobs;
+  const uint32_t* mask;
+  R beta;
+  template <typename Tc>
+  __device__ __forceinline__ void load(const XformParams& p, Tc* S, int64_t tube0, int nt, int tid) const {
+    const int P = p.P, pitch = p.pitch;
+    const int64_t e0 = tube0 * P;
+    const int cnt = nt * P;
+    for (int l = tid; l < cnt; l += kXformThreads) {
+      const int64_t e = e0 + l;
+      const R y = momentum<R>(xc[e], xp[e], beta);
+      const bool obs = (mask[e >> 5] >> (e & 31)) & 1u;
+      const R g = gradient_point<R>(y, pobs[e], obs);
+      const int t = l / P;
+      const int q = l - t * P;
+      S[q * pitch + t] = cvt<Tc>(g);
+    }
+  }
+};
+
+// slots: 0 sum (y - x+)^2, 1 sum x+^2, 2 sum (x+ - gt)^2, 3 max x+, 4 sum Im^2
+template <typename R>
+struct StorePGA {
+  static constexpr int NACC = 5;
+  static constexpr unsigned MAXMASK = 1u << 3;
+  R* xn;
+  const R* xc;
+  const R* xp;
+  const R* gt;
+  R beta;
+  template <typename Tc>
+  __device__ __forceinline__ void store(const XformParams& p, const Tc* S, int64_t tube0, int nt, int tid,
+                                        double* acc) const {
+    const int P = p.P, pitch = p.pitch;
+    const int64_t e0 = tube0 * P;
+    const int cnt = nt * P;
+    for (int l = tid; l < cnt; l += kXformThreads) {
+      const int t = l / P;
+      const int q = l - t * P;
+      const Tc v = S[q * pitch + t];
+      const int64_t e = e0 + l;
+      const R x1 = re_v(v);
+      const R y = momentum<R>(xc[e], xp[e], beta);
+      const double d = (double)y - (double)x1;
+      acc[0] += d * d;
+      acc[1] += (double)x1 * (double)x1;
+      if (gt) {
+        const double dg = (double)x1 - (double)gt[e];
+        acc[2] += dg * dg;
+      }
+      acc[3] = fmax(acc[3], (double)x1);
+      acc[4] += (double)im_v(v) * (double)im_v(v);
+      xn[e] = x1;
+    }
+  }
+};
+
+// reduce the per-CTA partials of one iteration, record, and decide to stop
+__global__ void pga_finalize_kernel(const double* __restrict__ partials, int64_t nblocks, double* __restrict__ rec,
+                                    int* __restrict__ state, const double* __restrict__ scalars, double tol) {
+  if (state[0]) return;
+  const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double vals[5];
+  if (slot < 5) {
+    const bool mx = slot == 3;
+    double v = mx ? -1.0e308 : 0.0;
+    for (int64_t i = lane; i < nblocks; i += 32) {
+      const double w = partials[i * 5 + slot];
+      v = mx ? fmax(v, w) : v + w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = mx ? fmax(v, w) : v + w;
+    }
+    if (lane == 0) vals[slot] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 5; ++k) rec[k] = vals[k];
+    const double num = sqrt(vals[0]);
+    const double den = sqrt(vals[1]);
+    double rel;
+    if (den > 0.0)
+      rel = num / den;
+    else if (scalars[0] == 0.0)
+      rel = 0.0;
+    else
+      rel = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    state[1] += 1;
+    if (rel <= tol) state[0] = 1;
+  }
+}
+
+template <typename R>
+__global__ void pga_setup_kernel(int64_t E, const double* __restrict__ m, const uint8_t* __restrict__ mask8,
+                                 R* __restrict__ pobs) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    pobs[e] = mask8[e] ? (R)m[e] : (R)0;
+}
+
+__global__ void pack_mask_kernel(int64_t E, const uint8_t* __restrict__ mask8, uint32_t* __restrict__ bits) {
+  const int64_t words = (E + 31) / 32;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t e = w * 32 + b;
+      if (e < E && mask8[e]) v |= 1u << b;
+    }
+    bits[w] = v;
+  }
+}
+
+template <typename R>
+__global__ void pga_fetch_kernel(int64_t E, const R* __restrict__ x, const R* __restrict__ pobs,
+                                 const uint32_t* __restrict__ bits, const double* __restrict__ m, int reimpose,
+                                 double* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const bool obs = (bits[e >> 5] >> (e & 31)) & 1u;
+    out[e] = (reimpose && obs) ? m[e] : (double)x[e];
+  }
+}
+
+template <typename R>
+int pga_iteration(ltb_pga* g, int k, double beta, double mu, double tol, double* rec) {
+  ltb_ctx* ctx = g->ctx;
+  const bool cm = g->spec->is_complex != 0;
+  const R* xc = (const R*)g->x[cur_of(k)];
+  const R* xp = (const R*)g->x[prev_of(k)];
+  R* xn = (R*)g->x[next_of(k)];
+  const int* skip = g->d_state;
+  const int dbl = std::is_same<R, double>::value ? 1 : 0;
+  XformParams p{};
+  p.NT = g->NT;
+  // forward: gradient step fused into the load, slice-major complex/real store
+  {
+    build_steps(g->spec, 0, p);
+    LoadPGA<R> ld{xc, xp, (const R*)g->pobs, g->mask, (R)beta};
+    if (cm) {
+      using Tc = cplx<R>;
+      size_t smem = 0;
+      p.TT = choose_tt<Tc>(p.P, &smem);
+      if (!p.TT) return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
+      p.pitch = p.TT + 1;
+      StorePlain<Tc, false> st{(Tc*)g->hat_a, LTB_SLICE_MAJOR};
+      LTB_TRY((launch_xform_tile<Tc, Tc>(ctx, p, ld, st, (const Tc*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
+    } else {
+      using Tc = R;
+      size_t smem = 0;
+      p.TT = choose_tt<Tc>(p.P, &smem);
+      if (!p.TT) return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
+      p.pitch = p.TT + 1;
+      StorePlain<Tc, false> st{(Tc*)g->hat_a, LTB_SLICE_MAJOR};
+      LTB_TRY((launch_xform_tile<Tc, R>(ctx, p, ld, st, (const R*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
+    }
+  }
+  // slice SVT with tau = mu_k
+  LTB_TRY(ltb_svt_impl(ctx, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, nullptr, g->hat_b, skip));
+  // inverse with the fused norms epilogue
+  {
+    build_steps(g->spec, 1, p);
+    StorePGA<R> st{xn, xc, xp, (const R*)g->gt, (R)beta};
+    if (cm) {
+      using Tc = cplx<R>;
+      size_t smem = 0;
+      p.TT = choose_tt<Tc>(p.P, &smem);
+      p.pitch = p.TT + 1;
+      LoadPlain<Tc> ld{(const Tc*)g->hat_b, LTB_SLICE_MAJOR};
+      LTB_TRY((launch_xform_tile<Tc, Tc>(ctx, p, ld, st, (const Tc*)g->spec->d_mats[dbl][1], g->partials, skip, smem)));
+    } else {
+      using Tc = R;
+      size_t smem = 0;
+      p.TT = choose_tt<Tc>(p.P, &smem);
+      p.pitch = p.TT + 1;
+      LoadPlain<Tc> ld{(const Tc*)g->hat_b, LTB_SLICE_MAJOR};
+      LTB_TRY((launch_xform_tile<Tc, R>(ctx, p, ld, st, (const R*)g->spec->d_mats[dbl][1], g->partials, skip, smem)));
+    }
+    g->nblocks = (p.NT + p.TT - 1) / p.TT;
+  }
+  pga_finalize_kernel<<<1, 160, 0, ctx->stream>>>(g->partials, g->nblocks, rec, g->d_state, g->d_scalars, tol);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ltb_pga_create(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t i1, int64_t i2, const double* h_m,
+                   const uint8_t* h_mask, const double* h_gt, ltb_pga** out) {
+  *out = nullptr;
+  if (dtype != LTB_F32 && dtype != LTB_F64) return ltb_set_error(ctx, LTB_EPARAM, "pga: compute dtype must be real");
+  if (i1 < 1 || i2 < 1) return ltb_set_error(ctx, LTB_ESHAPE, "pga: empty slice");
+  ltb_pga* g = new ltb_pga();
+  g->ctx = ctx;
+  g->spec = spec;
+  g->dtype = dtype;
+  const bool cm = spec->is_complex != 0;
+  g->hat_dtype = cm ? (dtype == LTB_F64 ? LTB_C128 : LTB_C64) : dtype;
+  g->I1 = i1;
+  g->I2 = i2;
+  g->P = spec->P;
+  g->NT = i1 * i2;
+  g->E = g->NT * g->P;
+  const size_t rs = dtype_size(dtype), hs = dtype_size(g->hat_dtype);
+  const int64_t E = g->E;
+  size_t smem = 0;
+  const int tt = cm ? (dtype == LTB_F64 ? choose_tt<cplx<double>>((int)g->P, &smem) : choose_tt<cplx<float>>((int)g->P, &smem))
+                    : (dtype == LTB_F64 ? choose_tt<double>((int)g->P, &smem) : choose_tt<float>((int)g->P, &smem));
+  if (!tt) {
+    delete g;
+    return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube of %lld elements does not fit the fused transform tile",
+                         (long long)spec->P);
+  }
+  const int64_t nb = (g->NT + tt - 1) / tt;
+  int st = LTB_OK;
+  auto alloc = [&](size_t bytes, void** p) {
+    if (st == LTB_OK) st = ltb_ws_alloc(ctx, bytes, p);
+  };
+  for (int k = 0; k < 3; ++k) alloc(rs * E, &g->x[k]);
+  alloc(rs * E, &g->pobs);
+  alloc(sizeof(uint32_t) * ((E + 31) / 32), (void**)&g->mask);
+  alloc(hs * E, &g->hat_a);
+  alloc(hs * E, &g->hat_b);
+  alloc(sizeof(double) * 5 * nb, (void**)&g->partials);
+  alloc(sizeof(int) * 4, (void**)&g->d_state);
+  alloc(sizeof(double) * 4, (void**)&g->d_scalars);
+  if (h_gt) alloc(rs * E, &g->gt);
+  double* d_m = nullptr;
+  uint8_t* d_mask8 = nullptr;
+  alloc(sizeof(double) * E, (void**)&d_m);
+  alloc(E, (void**)&d_mask8);
+  if (st != LTB_OK) {
+    ltb_pga_destroy(g);
+    return st;
+  }
+  cudaStream_t s = ctx->stream;
+  cudaMemcpyAsync(d_m, h_m, sizeof(double) * E, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(d_mask8, h_mask, E, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(g->x[0], 0, rs * E, s);
+  cudaMemsetAsync(g->x[1], 0, rs * E, s);
+  cudaMemsetAsync(g->d_state, 0, sizeof(int) * 4, s);
+  const int blocks = grid_for(E, 256, ctx->num_sms * 8);
+  pack_mask_kernel<<<grid_for((E + 31) / 32, 256, ctx->num_sms * 8), 256, 0, s>>>(E, d_mask8, g->mask);
+  ctx->launches++;
+  if (dtype == LTB_F64) {
+    pga_setup_kernel<double><<<blocks, 256, 0, s>>>(E, d_m, d_mask8, (double*)g->pobs);
+  } else {
+    pga_setup_kernel<float><<<blocks, 256, 0, s>>>(E, d_m, d_mask8, (float*)g->pobs);
+  }
+  ctx->launches++;
+  if (h_gt) {
+    cudaMemcpyAsync(d_m, h_gt, sizeof(double) * E, cudaMemcpyHostToDevice, s);
+    st = ltb_convert(ctx, E, LTB_F64, d_m, dtype, g->gt);
+  }
+  if (st == LTB_OK) st = ltb_reduce_sumsq_dev(ctx, dtype, E, g->pobs, nullptr, ctx->d_scratch);
+  if (st == LTB_OK) {
+    cudaMemcpyAsync(g->d_scalars, ctx->d_scratch, sizeof(double), cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(&g->pobs_sumsq, ctx->d_scratch, sizeof(double), cudaMemcpyDeviceToHost, s);
+  }
+  ltb_ws_free(ctx, d_m);
+  ltb_ws_free(ctx, d_mask8);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (st == LTB_OK && e != cudaSuccess) st = ltb_set_error(ctx, LTB_ECUDA, "pga setup: %s", cudaGetErrorString(e));
+  if (st != LTB_OK) {
+    ltb_pga_destroy(g);
+    return st;
+  }
+  *out = g;
+  return LTB_OK;
+}
+
+int ltb_pga_pobs_sumsq(ltb_pga* g, double* h_out) {
+  *h_out = g->pobs_sumsq;
+  return LTB_OK;
+}
+
+int ltb_pga_run(ltb_pga* g, int k0, int count, const double* h_beta, const double* h_mu, double tol,
+                double* h_records, int* h_done, int* h_converged) {
+  ltb_ctx* ctx = g->ctx;
+  *h_done = 0;
+  *h_converged = g->converged ? 1 : 0;
+  if (count <= 0 || g->converged) return LTB_OK;
+  if (k0 != g->done + 1) return ltb_set_error(ctx, LTB_EPARAM, "pga: iterations must be run in order");
+  if (count > g->records_cap) {
+    if (g->d_records) ltb_ws_free(ctx, g->d_records);
+    g->d_records = nullptr;
+    LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * 5 * count, (void**)&g->d_records));
+    g->records_cap = count;
+  }
+  for (int i = 0; i < count; ++i) {
+    const int k = k0 + i;
+    int st = g->dtype == LTB_F64 ? pga_iteration<double>(g, k, h_beta[i], h_mu[i], tol, g->d_records + 5 * i)
+                                 : pga_iteration<float>(g, k, h_beta[i], h_mu[i], tol, g->d_records + 5 * i);
+    if (st != LTB_OK) return st;
+  }
+  int state[2] = {0, 0};
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(state, g->d_state, sizeof(int) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(h_records, g->d_records, sizeof(double) * 5 * count, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaGetLastError());
+  const int executed = state[1] - g->done;
+  g->done = state[1];
+  g->converged = state[0] != 0;
+  *h_done = executed;
+  *h_converged = g->converged ? 1 : 0;
+  return LTB_OK;
+}
+
+int ltb_pga_current(ltb_pga* g, void** d_x) {
+  *d_x = g->x[cur_of(g->done + 1)];
+  return LTB_OK;
+}
+
+int ltb_pga_fetch(ltb_pga* g, int reimpose_observed, double* h_x) {
+  ltb_ctx* ctx = g->ctx;
+  const int64_t E = g->E;
+  double* d_out = nullptr;
+  double* d_m = nullptr;
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * E, (void**)&d_out));
+  const void* xc = g->x[cur_of(g->done + 1)];
+  const int blocks = grid_for(E, 256, ctx->num_sms * 8);
+  if (reimpose_observed) {
+    // observed entries come back as m itself: p_obs holds m there in compute precision,
+    // so re-upload is avoided only when the compute dtype is float64
+    LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * E, (void**)&d_m));
+    LTB_CUDA_TRY(ctx, cudaMemcpyAsync(d_m, h_x, sizeof(double) * E, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  if (g->dtype == LTB_F64)
+    pga_fetch_kernel<double><<<blocks, 256, 0, ctx->stream>>>(E, (const double*)xc, (const double*)g->pobs, g->mask,
+                                                              d_m, reimpose_observed, d_out);
+  else
+    pga_fetch_kernel<float><<<blocks, 256, 0, ctx->stream>>>(E, (const float*)xc, (const float*)g->pobs, g->mask,
+                                                             d_m, reimpose_observed, d_out);
+  LTB_LAUNCH_CHECK(ctx);
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(h_x, d_out, sizeof(double) * E, cudaMemcpyDeviceToHost, ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  ltb_ws_free(ctx, d_out);
+  if (d_m) ltb_ws_free(ctx, d_m);
+  return LTB_OK;
+}
+
+void ltb_pga_destroy(ltb_pga* g) {
+  if (!g) return;
+  ltb_ctx* ctx = g->ctx;
+  for (int k = 0; k < 3; ++k) ltb_ws_free(ctx, g->x[k]);
+  ltb_ws_free(ctx, g->pobs);
+  ltb_ws_free(ctx, g->gt);
+  ltb_ws_free(ctx, g->mask);
+  ltb_ws_free(ctx, g->hat_a);
+  ltb_ws_free(ctx, g->hat_b);
+  ltb_ws_free(ctx, g->partials);
+  ltb_ws_free(ctx, g->d_records);
+  ltb_ws_free(ctx, g->d_state);
+  ltb_ws_free(ctx, g->d_scalars);
+  cudaStreamSynchronize(ctx->stream);
+  delete g;
+}
+
+}  // extern "C"

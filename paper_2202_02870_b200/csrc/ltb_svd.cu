@@ -1,0 +1,462 @@
+// K3: batched one-sided (Hestenes) Jacobi SVD of transform-domain slices,
+// the SVT fused recomposition and the full-matrices SVD for t_svd.
+//
+// Reference semantics:
+//   svt   linalg.py:168-181  u, s, vh = svd(hat, full_matrices=False);
+//                            out = (u * max(s - tau, 0)) @ vh
+//   t_svd linalg.py:102-118  u, s, vh = svd(hat, full_matrices=True)
+//   ranks / spectral_norm / nuclear_norm  linalg.py:132-165 (values only)
+//
+// B200 design (one CTA per slice, the slice resident in shared memory):
+//   * the slice is loaded once, oriented so that it has n = min(I1, I2)
+//     columns of length m = max(I1, I2) (A itself, or A^H), column-contiguous
+//     with an odd pitch (bank-conflict-free strided fills);
+//   * a round-robin (circle-method) ordering gives n/2 disjoint column pairs
+//     per round; each warp takes pairs, reduces the 2x2 Gram entries with
+//     warp shuffles, and applies the (complex-phased) Jacobi rotation in
+//     place; one __syncthreads per round, sweeps until no pair exceeds
+//     tol * sqrt(alpha * beta);
+//   * the columns are then sorted by norm (descending, like LAPACK) and the
+//     SVT is recomposed WITHOUT accumulating V:
+//        out = sum_{sigma_j > tau} (sigma_j - tau) / sigma_j^2 * w_j (w_j^H A)
+//     as two batched GEMMs whose inner dimension is limited per slice to the
+//     number of surviving singular values (ltb_gemm.cu).
+// Slices that do not fit in shared memory run the same kernel with the
+// working columns in an L2-resident global workspace.
+#include <cfloat>
+
+#include "ltb_dispatch.cuh"
+
+namespace {
+
+constexpr int kJacobiMaxThreads = 512;
+
+template <typename R> struct eps_of;
+template <> struct eps_of<float> {
+  static constexpr float value = FLT_EPSILON;
+};
+template <> struct eps_of<double> {
+  static constexpr double value = DBL_EPSILON;
+};
+
+// round-robin pair k of round r for an even number of players np
+__device__ __forceinline__ void rr_pair(int np, int r, int k, int& p, int& q) {
+  const int m1 = np - 1;
+  if (k == 0) {
+    p = m1;
+    q = r;
+  } else {
+    p = (r + k) % m1;
+    q = (r - k + m1) % m1;
+  }
+}
+
+template <typename R> __device__ __forceinline__ R warp_sum_r(R v) { return warp_sum(v); }
+
+struct JacobiOut {
+  void* w_out;       // batch x n x m (column j contiguous, sorted) or null
+  void* sv_out;      // batch x n real, descending, or null
+  void* v_out;       // batch x n x n (column j contiguous, sorted) or null (WANT_V)
+  int* kept_out;     // batch, number of sigma > tau, or null
+  void* d_out;       // batch x n real: (sigma - tau)_+ / sigma^2 in sorted order, or null
+  double tau;
+  const int* skip;   // device flag: nonzero -> return immediately
+};
+
+template <typename T, bool WANT_V, bool GLOBAL>
+__global__ void __launch_bounds__(kJacobiMaxThreads)
+    jacobi_kernel(int64_t I1, int64_t I2, const T* __restrict__ A, T* __restrict__ gws, JacobiOut o, int max_sweeps) {
+  using R = typename scalar_traits<T>::real;
+  constexpr bool CPLX = scalar_traits<T>::is_complex;
+  if (o.skip && *o.skip) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const bool trans = I1 < I2;
+  const int m = (int)(trans ? I2 : I1);
+  const int n = (int)(trans ? I1 : I2);
+  const int mp = m | 1;
+  const int np_v = n | 1;
+  const int64_t b = blockIdx.x;
+  const T* Ab = A + b * I1 * I2;
+
+  T* W;
+  T* V = nullptr;
+  R* sig;
+  int* flags;
+  if constexpr (GLOBAL) {
+    W = gws + b * ((int64_t)n * mp + (WANT_V ? (int64_t)n * np_v : 0));
+    if (WANT_V) V = W + (int64_t)n * mp;
+    sig = reinterpret_cast<R*>(smem_raw);
+  } else {
+    W = reinterpret_cast<T*>(smem_raw);
+    if (WANT_V) V = W + (size_t)n * mp;
+    sig = reinterpret_cast<R*>(W + (size_t)n * mp + (WANT_V ? (size_t)n * np_v : 0));
+  }
+  flags = reinterpret_cast<int*>(sig + n + 1);
+
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+
+  // ---- load the working columns
+  if (!trans) {  // columns of A (strided in row-major storage)
+    for (int l = tid; l < m * n; l += nth) {
+      const int i = l / n, j = l - i * n;
+      W[(size_t)j * mp + i] = Ab[l];
+    }
+  } else {  // columns of A^H = conjugated rows of A
+    for (int l = tid; l < m * n; l += nth) {
+      const int j = l / m, i = l - j * m;
+      W[(size_t)j * mp + i] = conj_v(Ab[l]);
+    }
+  }
+  if (WANT_V) {
+    for (int l = tid; l < n * n; l += nth) {
+      const int j = l / n, k = l - j * n;
+      V[(size_t)j * np_v + k] = (j == k) ? cvt<T>((R)1) : zero_v<T>();
+    }
+  }
+  if (tid < 2) flags[tid] = 0;
+  __syncthreads();
+
+  const R tol = eps_of<R>::value * sqrt((R)max(m, 1));
+  const int npl = n + (n & 1);
+  for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
+    int* rot = &flags[sweep & 1];
+    for (int r = 0; r < npl - 1; ++r) {
+      for (int k = warp; k < npl / 2; k += nwarps) {
+        int p, q;
+        rr_pair(npl, r, k, p, q);
+        if (p >= n || q >= n) continue;
+        T* wp = W + (size_t)p * mp;
+        T* wq = W + (size_t)q * mp;
+        R al = 0, be = 0;
+        T ga = zero_v<T>();
+        for (int i = lane; i < m; i += 32) {
+          const T x = wp[i], y = wq[i];
+          al += abs2_v(x);
+          be += abs2_v(y);
+          fma_acc(ga, conj_v(x), y);
+        }
+        al = warp_sum_r(al);
+        be = warp_sum_r(be);
+        R gre = warp_sum_r(re_v(ga));
+        R gim = CPLX ? warp_sum_r(im_v(ga)) : (R)0;
+        const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
+        if (!(gabs > tol * sqrt(al) * sqrt(be)) || al == (R)0 || be == (R)0) continue;
+        const R zeta = (be - al) / (2 * gabs);
+        const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
+        const R c = (R)1 / sqrt((R)1 + t * t);
+        const R s = c * t;
+        // phase e^{-i phi} applied to column q so the Gram entry becomes real
+        T ph;
+        if constexpr (CPLX) {
+          ph = T{gre / gabs, -gim / gabs};
+        } else {
+          ph = (gre >= 0) ? (R)1 : (R)-1;
+        }
+        for (int i = lane; i < m; i += 32) {
+          const T x = wp[i];
+          const T y = ph * wq[i];
+          wp[i] = c * x - s * y;
+          wq[i] = s * x + c * y;
+        }
+        if (WANT_V) {
+          T* vp = V + (size_t)p * np_v;
+          T* vq = V + (size_t)q * np_v;
+          for (int i = lane; i < n; i += 32) {
+            const T x = vp[i];
+            const T y = ph * vq[i];
+            vp[i] = c * x - s * y;
+            vq[i] = s * x + c * y;
+          }
+        }
+        if (lane == 0) *rot = 1;
+      }
+      __syncthreads();
+    }
+    const int any = *rot;
+    __syncthreads();
+    if (tid == 0) flags[(sweep + 1) & 1] = 0;
+    __syncthreads();
+    if (!any) break;
+  }
+
+  // ---- singular values = column norms
+  for (int j = warp; j < n; j += nwarps) {
+    const T* wj = W + (size_t)j * mp;
+    R s2 = 0;
+    for (int i = lane; i < m; i += 32) s2 += abs2_v(wj[i]);
+    s2 = warp_sum_r(s2);
+    if (lane == 0) sig[j] = sqrt(s2);
+  }
+  __syncthreads();
+
+  // ---- sort (descending, stable) and emit
+  R* sv_out = reinterpret_cast<R*>(o.sv_out);
+  R* d_out = reinterpret_cast<R*>(o.d_out);
+  int* rank_sh = flags + 4;
+  if (tid == 0) flags[2] = 0;
+  __syncthreads();
+  int kept_local = 0;
+  for (int j = tid; j < n; j += nth) {
+    const R sj = sig[j];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) {
+      const R si = sig[i];
+      rank += (si > sj) || (si == sj && i < j);
+    }
+    rank_sh[j] = rank;
+    if (sv_out) sv_out[b * n + rank] = sj;
+    const bool keep = sj > (R)o.tau && sj > (R)0;
+    kept_local += keep;
+    if (d_out) d_out[b * n + rank] = keep ? (sj - (R)o.tau) / (sj * sj) : (R)0;
+  }
+  if (kept_local) atomicAdd(&flags[2], kept_local);
+  __syncthreads();
+  if (o.kept_out && tid == 0) o.kept_out[b] = flags[2];
+  if (o.w_out) {
+    T* dst = reinterpret_cast<T*>(o.w_out) + b * (int64_t)n * m;
+    for (int l = tid; l < n * m; l += nth) {
+      const int j = l / m, i = l - j * m;
+      dst[(int64_t)rank_sh[j] * m + i] = W[(size_t)j * mp + i];
+    }
+  }
+  if (WANT_V && o.v_out) {
+    T* dst = reinterpret_cast<T*>(o.v_out) + b * (int64_t)n * n;
+    for (int l = tid; l < n * n; l += nth) {
+      const int j = l / n, i = l - j * n;
+      dst[(int64_t)rank_sh[j] * n + i] = V[(size_t)j * np_v + i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- t_svd helpers
+// U (m x m, row-major output with leading dim m) from the sorted working
+// columns: u_j = w_j / sigma_j where sigma_j is numerically nonzero, and a
+// deterministic Gram-Schmidt completion (candidate unit vectors e_0, e_1, ...)
+// for the remaining columns (rank-deficient slices, and the m - n extra
+// columns of full_matrices=True).
+template <typename T>
+__global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
+                                  const typename scalar_traits<T>::real* __restrict__ sv, T* __restrict__ U) {
+  using R = typename scalar_traits<T>::real;
+  const int64_t b = blockIdx.x;
+  const T* Wb = w_sorted + b * (int64_t)n * m;
+  const R* sb = sv + b * (int64_t)n;
+  T* Ub = U + b * (int64_t)m * m;  // Ub[i * m + j] = column j, row i
+  __shared__ R red[32];
+  __shared__ T redc[32];
+  __shared__ int good_count;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const R smax = n > 0 ? sb[0] : (R)0;
+  const R thr = smax * (R)max(m, 1) * eps_of<R>::value;
+  // number of leading good columns (sorted descending, so good ones are a prefix)
+  if (tid == 0) {
+    int g = 0;
+    while (g < n && sb[g] > thr && sb[g] > (R)0) ++g;
+    good_count = g;
+  }
+  __syncthreads();
+  const int g0 = good_count;
+  for (int l = tid; l < m * g0; l += nth) {
+    const int j = l / m, i = l - j * m;
+    Ub[(int64_t)i * m + j] = Wb[(int64_t)j * m + i] * ((R)1 / sb[j]);
+  }
+  __syncthreads();
+  auto block_sum_r = [&](R v) -> R {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    R s = 0;
+    for (int k = 0; k < (nth >> 5); ++k) s += red[k];
+    return s;
+  };
+  auto block_sum_t = [&](T v) -> T {
+    R a = warp_sum(re_v(v));
+    R c = scalar_traits<T>::is_complex ? warp_sum(im_v(v)) : (R)0;
+    __syncthreads();
+    if (lane == 0) {
+      if constexpr (scalar_traits<T>::is_complex) {
+        redc[warp] = T{a, c};
+      } else {
+        redc[warp] = a;
+      }
+    }
+    __syncthreads();
+    T s = zero_v<T>();
+    for (int k = 0; k < (nth >> 5); ++k) s = s + redc[k];
+    return s;
+  };
+  int cand = 0;
+  for (int slot = g0; slot < m; ++slot) {
+    // the slot's column is built in place in U's column `slot`
+    while (cand < m) {
+      for (int i = tid; i < m; i += nth) Ub[(int64_t)i * m + slot] = (i == cand) ? cvt<T>((R)1) : zero_v<T>();
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int g = 0; g < slot; ++g) {
+          T part = zero_v<T>();
+          for (int i = tid; i < m; i += nth) fma_acc(part, conj_v(Ub[(int64_t)i * m + g]), Ub[(int64_t)i * m + slot]);
+          const T coef = block_sum_t(part);
+          for (int i = tid; i < m; i += nth) {
+            T v = Ub[(int64_t)i * m + slot];
+            v = v - coef * Ub[(int64_t)i * m + g];
+            Ub[(int64_t)i * m + slot] = v;
+          }
+          __syncthreads();
+        }
+      }
+      R part = 0;
+      for (int i = tid; i < m; i += nth) part += abs2_v(Ub[(int64_t)i * m + slot]);
+      const R nrm = sqrt(block_sum_r(part));
+      ++cand;
+      if (nrm > (R)0.25) {
+        for (int i = tid; i < m; i += nth) Ub[(int64_t)i * m + slot] = Ub[(int64_t)i * m + slot] * ((R)1 / nrm);
+        __syncthreads();
+        break;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// dst (row-major n x n, leading dim n): dst[i * n + j] = col_j[i], col-contiguous src
+template <typename T>
+__global__ void cols_to_rowmajor_kernel(int64_t batch, int n, const T* __restrict__ src, T* __restrict__ dst) {
+  const int64_t total = batch * (int64_t)n * n;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = l / ((int64_t)n * n);
+    const int64_t r = l - b * n * n;
+    const int i = (int)(r / n), j = (int)(r - (int64_t)(r / n) * n);
+    dst[l] = src[b * n * n + (int64_t)j * n + i];
+  }
+}
+
+template <typename T>
+size_t jacobi_smem_bytes(int m, int n, bool want_v) {
+  using R = typename scalar_traits<T>::real;
+  const size_t mp = (size_t)(m | 1), np_v = (size_t)(n | 1);
+  return ((size_t)n * mp + (want_v ? (size_t)n * np_v : 0)) * sizeof(T) + (n + 1) * sizeof(R) + (n + 8) * sizeof(int) + 16;
+}
+
+constexpr size_t kSmemLimit = 225 * 1024;
+
+template <typename T, bool WANT_V>
+int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, JacobiOut o) {
+  using R = typename scalar_traits<T>::real;
+  const int m = (int)std::max(I1, I2), n = (int)std::min(I1, I2);
+  const int max_sweeps = std::is_same<R, float>::value ? 40 : 60;
+  const int pairs = (n + 1) / 2;
+  int threads = 32 * std::min(16, std::max(2, pairs));
+  const size_t smem_full = jacobi_smem_bytes<T>(m, n, WANT_V);
+  if (batch > 0x7fffffff) return ltb_set_error(ctx, LTB_ESHAPE, "svd: batch too large");
+  if (smem_full <= kSmemLimit) {
+    auto kern = jacobi_kernel<T, WANT_V, false>;
+    LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
+    kern<<<(unsigned)batch, threads, smem_full, ctx->stream>>>(I1, I2, A, nullptr, o, max_sweeps);
+    LTB_LAUNCH_CHECK(ctx);
+    return LTB_OK;
+  }
+  // global-workspace tier
+  const size_t per = (size_t)n * (m | 1) + (WANT_V ? (size_t)n * (n | 1) : 0);
+  T* ws = nullptr;
+  LTB_TRY(ltb_ws_alloc(ctx, per * batch * sizeof(T), (void**)&ws));
+  const size_t smem = (n + 1) * sizeof(R) + (n + 8) * sizeof(int) + 16;
+  auto kern = jacobi_kernel<T, WANT_V, true>;
+  if (smem > 48 * 1024)
+    LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  threads = kJacobiMaxThreads;
+  kern<<<(unsigned)batch, threads, smem, ctx->stream>>>(I1, I2, A, ws, o, max_sweeps);
+  LTB_LAUNCH_CHECK(ctx);
+  ltb_ws_free(ctx, ws);
+  return LTB_OK;
+}
+
+}  // namespace
+
+// SVT of `batch` row-major I1 x I2 slices: out = U (S - tau)_+ V^H
+int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2, const void* d_a, double tau,
+                 const double* /*d_tau*/, void* d_out, const int* d_skip) {
+  if (!dtype_valid(dtype)) return ltb_set_error(ctx, LTB_EPARAM, "svt: bad dtype");
+  if (batch < 0 || I1 < 0 || I2 < 0) return ltb_set_error(ctx, LTB_ESHAPE, "svt: negative dimension");
+  if (batch == 0 || I1 == 0 || I2 == 0) return LTB_OK;
+  return dispatch_dtype(dtype, [&](auto tg) -> int {
+    using T = typename decltype(tg)::type;
+    using R = typename scalar_traits<T>::real;
+    const bool trans = I1 < I2;
+    const int64_t m = trans ? I2 : I1, n = trans ? I1 : I2;
+    T* w = nullptr;
+    T* z = nullptr;
+    R* d = nullptr;
+    int* kept = nullptr;
+    LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * batch * n * m, (void**)&w));
+    LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * batch * n * (trans ? I1 : I2), (void**)&z));
+    LTB_TRY(ltb_ws_alloc(ctx, sizeof(R) * batch * n, (void**)&d));
+    LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * batch, (void**)&kept));
+    JacobiOut o{w, nullptr, nullptr, kept, d, tau, d_skip};
+    LTB_TRY((launch_jacobi<T, false>(ctx, batch, I1, I2, (const T*)d_a, o)));
+    const T* A = (const T*)d_a;
+    T* out = (T*)d_out;
+    if (!trans) {
+      // Z = D W^H A   (n x I2, rows limited to the kept count)
+      LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, n, I2, m, LTB_OP_C, w, m, n * m, LTB_OP_N, A, I2, I1 * I2, z, I2,
+                            n * I2, kept, nullptr, nullptr, d, nullptr, d_skip));
+      // out = W Z     (I1 x I2, inner dimension limited to the kept count)
+      LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, I1, I2, n, LTB_OP_T, w, m, n * m, LTB_OP_N, z, I2, n * I2, out, I2,
+                            I1 * I2, nullptr, nullptr, kept, nullptr, nullptr, d_skip));
+    } else {
+      // Y = A W D     (I1 x n, columns limited to the kept count)
+      LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, I1, n, m, LTB_OP_N, A, I2, I1 * I2, LTB_OP_T, w, m, n * m, z, n,
+                            I1 * n, nullptr, kept, nullptr, nullptr, d, d_skip));
+      // out = Y W^H
+      LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, I1, I2, n, LTB_OP_N, z, n, I1 * n, LTB_OP_C, w, m, n * m, out, I2,
+                            I1 * I2, nullptr, nullptr, kept, nullptr, nullptr, d_skip));
+    }
+    ltb_ws_free(ctx, w);
+    ltb_ws_free(ctx, z);
+    ltb_ws_free(ctx, d);
+    ltb_ws_free(ctx, kept);
+    return LTB_OK;
+  });
+}
+
+extern "C" int ltb_slice_singular_values(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2,
+                                         const void* d_a, void* d_s) {
+  if (!dtype_valid(dtype)) return ltb_set_error(ctx, LTB_EPARAM, "svd: bad dtype");
+  if (batch < 0 || I1 < 0 || I2 < 0) return ltb_set_error(ctx, LTB_ESHAPE, "svd: negative dimension");
+  if (batch == 0 || I1 == 0 || I2 == 0) return LTB_OK;
+  return dispatch_dtype(dtype, [&](auto tg) -> int {
+    using T = typename decltype(tg)::type;
+    JacobiOut o{nullptr, d_s, nullptr, nullptr, nullptr, 0.0, nullptr};
+    return launch_jacobi<T, false>(ctx, batch, I1, I2, (const T*)d_a, o);
+  });
+}
+
+extern "C" int ltb_slice_svd(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2, const void* d_a,
+                             void* d_u, void* d_s, void* d_v) {
+  if (!dtype_valid(dtype)) return ltb_set_error(ctx, LTB_EPARAM, "svd: bad dtype");
+  if (batch < 0 || I1 < 0 || I2 < 0) return ltb_set_error(ctx, LTB_ESHAPE, "svd: negative dimension");
+  if (batch == 0 || I1 == 0 || I2 == 0) return LTB_OK;
+  return dispatch_dtype(dtype, [&](auto tg) -> int {
+    using T = typename decltype(tg)::type;
+    using R = typename scalar_traits<T>::real;
+    const bool trans = I1 < I2;
+    const int m = (int)(trans ? I2 : I1), n = (int)(trans ? I1 : I2);
+    T* w = nullptr;
+    T* vcols = nullptr;
+    LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * batch * n * m, (void**)&w));
+    LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * batch * n * n, (void**)&vcols));
+    JacobiOut o{w, d_s, vcols, nullptr, nullptr, 0.0, nullptr};
+    LTB_TRY((launch_jacobi<T, true>(ctx, batch, I1, I2, (const T*)d_a, o)));
+    // U of the oriented problem (m x m) and its V (n x n)
+    T* u_dst = trans ? (T*)d_v : (T*)d_u;  // m x m
+    T* v_dst = trans ? (T*)d_u : (T*)d_v;  // n x n
+    complete_u_kernel<T><<<(unsigned)batch, 256, 0, ctx->stream>>>(m, n, w, (const R*)d_s, u_dst);
+    LTB_LAUNCH_CHECK(ctx);
+    cols_to_rowmajor_kernel<T><<<grid_for(batch * n * n, 256, 4096), 256, 0, ctx->stream>>>(batch, n, vcols, v_dst);
+    LTB_LAUNCH_CHECK(ctx);
+    ltb_ws_free(ctx, w);
+    ltb_ws_free(ctx, vcols);
+    return LTB_OK;
+  });
+}

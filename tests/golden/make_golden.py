@@ -1,0 +1,107 @@
+"""Generate tests/golden/golden.npz by running the REFERENCE implementation.
+
+Run in the build container only (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+The fixture holds, per case, the seeded inputs, the spec metadata (JSON) and
+the outputs of `ltensor` (the reference) on those inputs.  It pins the CPU
+oracle (tests/test_oracle_golden.py) and the CUDA path (tests/test_gpu_*.py).
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE))
+
+import cases  # noqa: E402
+import ltensor as ref  # noqa: E402  (the reference, via PYTHONPATH)
+from ltensor.completion import CompletionConfig  # noqa: E402
+
+
+def spec_of(case):
+    if case["kind"] == "explicit":
+        return ref.make_spec("explicit", case["spec_shape"], modes=case.get("modes"), matrices=case["matrices"])
+    return ref.make_spec(case["kind"], case["spec_shape"], modes=case.get("modes"))
+
+
+def put_meta(out, name, case, **extra):
+    meta = {"kind": case["kind"], "spec_shape": list(case["spec_shape"]),
+            "modes": list(case["modes"]) if case.get("modes") else None}
+    meta.update(extra)
+    out[f"{name}/meta"] = np.array(json.dumps(meta))
+    for mode, mat in (case.get("matrices") or {}).items():
+        out[f"{name}/mat{mode}"] = np.asarray(mat)
+
+
+def lp(a, b, kind, shape):
+    return ref.l_product(a, b, ref.make_spec(kind, shape))
+
+
+def main():
+    out = {}
+    for name, case in cases.transform_cases().items():
+        spec = spec_of(case)
+        put_meta(out, name, case)
+        out[f"{name}/x"] = case["x"]
+        fwd = ref.apply_l(case["x"], spec)
+        out[f"{name}/fwd"] = fwd
+        out[f"{name}/inv"] = ref.apply_l_inv(fwd, spec, assume_real=True)
+        if spec.kind in ("fft", "dct"):
+            out[f"{name}/fwd_explicit"] = ref.apply_l(case["x"], spec, explicit=True)
+    for name, case in cases.product_cases().items():
+        put_meta(out, name, case)
+        out[f"{name}/a"] = case["a"]
+        out[f"{name}/b"] = case["b"]
+        out[f"{name}/c"] = ref.l_product(case["a"], case["b"], spec_of(case))
+    for name, case in cases.svd_cases().items():
+        spec = spec_of(case)
+        put_meta(out, name, case, tau=case["tau"])
+        out[f"{name}/x"] = case["x"]
+        f = ref.t_svd(case["x"], spec)
+        out[f"{name}/s"] = f.s
+        out[f"{name}/tube_norms"] = f.tube_norms
+        out[f"{name}/sv"] = np.linalg.svd(ref.core.as_rep_stack(ref.apply_l(case["x"], spec)), compute_uv=False)
+        if spec.unitary_scaled:
+            out[f"{name}/svt"] = ref.svt(case["x"], case["tau"], spec)
+            out[f"{name}/nuclear"] = np.array(ref.nuclear_norm(case["x"], spec))
+            out[f"{name}/spectral"] = np.array(ref.spectral_norm(case["x"], spec))
+        rr = ref.ranks(case["x"], spec)
+        out[f"{name}/multirank"] = np.asarray(rr.multirank)
+        out[f"{name}/tubal"] = np.array(rr.tubal)
+    for name, case in cases.completion_cases(lp).items():
+        spec = spec_of(dict(case, spec_shape=case["m"].shape))
+        mask = case["mask"]
+        if mask is None:
+            mask = ref.sample_mask(case["m"].shape, *case["mask_seed"])
+        cfg = CompletionConfig(spec=spec, **case["cfg"])
+        x, trace = ref.pga_complete(case["m"], mask, cfg, ground_truth=case.get("gt"))
+        put_meta(out, name, dict(case, spec_shape=case["m"].shape), cfg=case["cfg"],
+                 status=trace.status, final_rse=ref.rse(x, case["m"]))
+        out[f"{name}/m"] = case["m"]
+        out[f"{name}/mask"] = mask
+        if case.get("gt") is not None:
+            out[f"{name}/gt"] = case["gt"]
+        out[f"{name}/x_out"] = x
+        out[f"{name}/mu"] = np.array([r.mu for r in trace.records])
+        out[f"{name}/t"] = np.array([r.t for r in trace.records])
+        out[f"{name}/rel"] = np.array([r.rel_change for r in trace.records])
+        if case.get("gt") is not None:
+            out[f"{name}/rse"] = np.array([r.rse for r in trace.records])
+            out[f"{name}/psnr"] = np.array([r.psnr for r in trace.records])
+    for name, (dims, sr, seed) in cases.mask_cases().items():
+        out[f"{name}/meta"] = np.array(json.dumps({"dims": list(dims), "sr": sr, "seed": seed}))
+        out[f"{name}/mask"] = ref.sample_mask(dims, sr, seed)
+    np.savez_compressed(HERE / "golden.npz", **out)
+    total = sum(np.asarray(v).nbytes for v in out.values())
+    print(f"wrote {len(out)} arrays, {total / 1e6:.2f} MB raw -> {HERE / 'golden.npz'}")
+
+
+if __name__ == "__main__":
+    main()
