@@ -224,8 +224,10 @@ def run_ours(args):
     from paper_2202_02870_b200.engine import LProductPlan
 
     nat.set_device(local)
-    stream = torch.cuda.current_stream()
-    nat.lib().ltb_ctx_set_stream(nat.context(), stream.cuda_stream)
+    # one explicit (non-default) stream shared by torch (events, L2 flush) and libltb
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    nat.check(nat.lib().ltb_ctx_set_stream(nat.context(), stream.cuda_stream))
 
     hbm_peak, tf_peak, peak_src = _peaks()
     spec = L.make_spec("dct", (256, 256, 3, 32))
@@ -355,7 +357,7 @@ def bench_pga(L, nat, torch, args):
     spec = L.make_spec("dct", CFG3["shape"])
     from paper_2202_02870_b200.completion import PGASolver, pga_schedule
 
-    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=CFG3["iters"])
+    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=args.pga_iters)
     mu0 = cfg.nu * L.fro_norm(np.asarray(m, dtype=np.float64))
     mus, ts, betas = pga_schedule(cfg, mu0)
     solver = PGASolver(np.asarray(m, dtype=np.float64), mask, spec, "fp32")
@@ -394,6 +396,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--cpu-pga-iters", type=int, default=2)
+    ap.add_argument("--pga-iters", type=int, default=CFG3["iters"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

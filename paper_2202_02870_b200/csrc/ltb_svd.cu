@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
     if (sv_out) sv_out[b * n + rank] = sj;
     const bool keep = sj > (R)o.tau && sj > (R)0;
     kept_local += keep;
-    if (d_out) d_out[b * n + rank] = keep ? (sj - (R)o.tau) / (sj * sj) : (R)0;
+    // u_j u_j^H A / sigma_j scaled by (sigma_j - tau): w_j (w_j^H A) (sigma_j - tau) / sigma_j^3
+    if (d_out) d_out[b * n + rank] = keep ? (((sj - (R)o.tau) / sj) / sj) / sj : (R)0;
   }
   if (kept_local) atomicAdd(&flags[2], kept_local);
   __syncthreads();

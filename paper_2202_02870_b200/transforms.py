@@ -231,6 +231,28 @@ def imag_tol(dtype) -> float:
 
 
 # ----------------------------------------------------------------- device spec
+def hermitian_rows(m: np.ndarray, tol: float = 1e-12) -> np.ndarray:
+    """If row (n - i) mod n of `m` is conj(row i) up to rounding (the DFT), make it exactly so.
+
+    With exactly conjugate rows, a real tensor's transform-domain slices q and -q
+    are bitwise conjugates, every slice kernel (Jacobi, GEMM) is conjugation-
+    equivariant, and the real-output contract (transforms.py:217-225) holds
+    structurally instead of up to the conditioning of the slice SVD."""
+    n = m.shape[0]
+    idx = (-np.arange(n)) % n
+    scale = max(1.0, float(np.abs(m).max(initial=0.0)))
+    if np.abs(m[idx] - np.conj(m)).max(initial=0.0) > tol * scale:
+        return m
+    out = m.copy()
+    for i in range(n):
+        j = idx[i]
+        if i < j:
+            out[j] = np.conj(out[i])
+        elif i == j:
+            out[i] = out[i].real
+    return out
+
+
 def device_spec(spec: TransformSpec, trailing: tuple):
     """ltb_spec handle for tensors whose trailing dims are `trailing` (cached on the spec)."""
     trailing = tuple(int(d) for d in trailing)
@@ -243,6 +265,8 @@ def device_spec(spec: TransformSpec, trailing: tuple):
     fwd, inv = [], []
     for m in spec.modes:
         a = np.asarray(spec.mode_matrix(m), dtype=np.complex128 if cplx else np.float64)
+        if cplx:
+            a = hermitian_rows(a)
         b = np.asarray(spec._device_inverse(m), dtype=np.complex128 if cplx else np.float64)
         fwd.append(np.ascontiguousarray(a).ravel())
         inv.append(np.ascontiguousarray(b).ravel())

@@ -1,0 +1,123 @@
+"""Kernel-level checks through the C ABI (device pointers), against numpy on the
+same inputs: slice GEMM for every op / dtype, SVT / SVD / singular values for
+both slice orientations, the layout-only transform, reductions."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2202_02870_b200 import _native as nat
+
+pytestmark = pytest.mark.gpu
+
+DTYPES = [np.float32, np.float64, np.complex64, np.complex128]
+
+
+def rand(rng, shape, dt):
+    x = rng.standard_normal(shape)
+    if np.issubdtype(dt, np.complexfloating):
+        x = x + 1j * rng.standard_normal(shape)
+    return x.astype(dt)
+
+
+def tol(dt):
+    return 2e-5 if dt in (np.float32, np.complex64) else 1e-12
+
+
+def op_apply(x, op):
+    return {0: x, 1: np.swapaxes(x, -1, -2), 2: np.conj(x), 3: np.conj(np.swapaxes(x, -1, -2))}[op]
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("op_a", [0, 1, 2, 3])
+@pytest.mark.parametrize("op_b", [0, 1, 2, 3])
+@pytest.mark.parametrize("mnk", [(5, 7, 3), (70, 45, 130), (129, 131, 17)])
+def test_slice_gemm(dt, op_a, op_b, mnk):
+    rng = np.random.default_rng(hash((op_a, op_b, mnk)) % 2**32)
+    m, n, k = mnk
+    batch = 3
+    a_log = rand(rng, (batch, m, k), dt)
+    b_log = rand(rng, (batch, k, n), dt)
+    a_st = np.ascontiguousarray(op_apply(a_log, op_a) if op_a in (0, 2) else op_apply(a_log, op_a))
+    b_st = np.ascontiguousarray(op_apply(b_log, op_b) if op_b in (0, 2) else op_apply(b_log, op_b))
+    # stored operands are op^{-1}(logical); op(stored) == logical for all four ops
+    a_st = np.ascontiguousarray({0: a_log, 1: np.swapaxes(a_log, 1, 2), 2: np.conj(a_log),
+                                 3: np.conj(np.swapaxes(a_log, 1, 2))}[op_a])
+    b_st = np.ascontiguousarray({0: b_log, 1: np.swapaxes(b_log, 1, 2), 2: np.conj(b_log),
+                                 3: np.conj(np.swapaxes(b_log, 1, 2))}[op_b])
+    da = nat.DeviceArray.from_numpy(a_st)
+    db = nat.DeviceArray.from_numpy(b_st)
+    dc = nat.DeviceArray((batch, m, n), dt)
+    lda = a_st.shape[2]
+    ldb = b_st.shape[2]
+    nat.check(nat.lib().ltb_slice_gemm(nat.context(), nat.dtype_code(dt), batch, m, n, k, op_a, da.ptr, lda,
+                                       m * k, op_b, db.ptr, ldb, k * n, dc.ptr, n, m * n))
+    ref = np.matmul(a_log.astype(np.complex128), b_log.astype(np.complex128))
+    got = dc.numpy()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < tol(dt)
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("shape", [(6, 4), (4, 6), (1, 5), (5, 1), (33, 70), (70, 33), (64, 64)])
+def test_slice_svt_and_values(dt, shape):
+    rng = np.random.default_rng(7)
+    batch = 4
+    a = rand(rng, (batch,) + shape, dt)
+    u, s, vh = np.linalg.svd(a.astype(np.complex128 if np.iscomplexobj(a) else np.float64), full_matrices=False)
+    tau = float(np.median(s))
+    ref = np.matmul(u * np.maximum(s - tau, 0)[:, None, :], vh)
+    da = nat.DeviceArray.from_numpy(a)
+    out = nat.DeviceArray(a.shape, dt)
+    nat.check(nat.lib().ltb_slice_svt(nat.context(), nat.dtype_code(dt), batch, shape[0], shape[1], da.ptr, tau,
+                                      out.ptr))
+    got = out.numpy()
+    assert np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30) < 50 * tol(dt)
+    sv = nat.DeviceArray((batch, min(shape)), nat.real_of(dt))
+    nat.check(nat.lib().ltb_slice_singular_values(nat.context(), nat.dtype_code(dt), batch, shape[0], shape[1],
+                                                  da.ptr, sv.ptr))
+    np.testing.assert_allclose(sv.numpy(), s, rtol=50 * tol(dt), atol=50 * tol(dt) * s.max())
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("shape", [(6, 4), (4, 6), (5, 5), (3, 1)])
+def test_slice_svd_full(dt, shape):
+    rng = np.random.default_rng(9)
+    batch = 3
+    a = rand(rng, (batch,) + shape, dt)
+    if shape == (5, 5):
+        a[:, :, 3:] = 0  # rank deficient -> completion path
+    m, n = shape
+    da = nat.DeviceArray.from_numpy(a)
+    u = nat.DeviceArray((batch, m, m), dt)
+    v = nat.DeviceArray((batch, n, n), dt)
+    s = nat.DeviceArray((batch, min(m, n)), nat.real_of(dt))
+    nat.check(nat.lib().ltb_slice_svd(nat.context(), nat.dtype_code(dt), batch, m, n, da.ptr, u.ptr, s.ptr, v.ptr))
+    U, S, V = u.numpy(), s.numpy(), v.numpy()
+    k = min(m, n)
+    sig = np.zeros((batch, m, n))
+    sig[:, np.arange(k), np.arange(k)] = S
+    recon = U @ sig @ np.conj(np.swapaxes(V, 1, 2))
+    t = 50 * tol(dt)
+    assert np.linalg.norm(recon - a) / np.linalg.norm(a) < t
+    eye_m = np.broadcast_to(np.eye(m), (batch, m, m))
+    eye_n = np.broadcast_to(np.eye(n), (batch, n, n))
+    assert np.abs(np.conj(np.swapaxes(U, 1, 2)) @ U - eye_m).max() < t
+    assert np.abs(np.conj(np.swapaxes(V, 1, 2)) @ V - eye_n).max() < t
+    assert np.all(np.diff(S, axis=1) <= 0)
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+def test_reductions(dt):
+    rng = np.random.default_rng(3)
+    x = rand(rng, (1000, 37), dt)
+    y = rand(rng, (1000, 37), dt)
+    dx, dy = nat.DeviceArray.from_numpy(x), nat.DeviceArray.from_numpy(y)
+    out = (C.c_double * 2)()
+    nat.check(nat.lib().ltb_reduce_sumsq(nat.context(), dx.code, dx.size, dx.ptr, dy.ptr, out))
+    ref = np.sum(np.abs(x.astype(np.complex128) - y) ** 2)
+    assert abs(out[0] - ref) / ref < 1e-6
+    assert out[1] == pytest.approx(float(np.max(x.real)))
+    nat.check(nat.lib().ltb_reduce_dot(nat.context(), dx.code, dx.size, dx.ptr, dy.ptr, out))
+    ref = np.vdot(x.astype(np.complex128), y.astype(np.complex128))
+    assert abs(complex(out[0], out[1]) - ref) / abs(ref) < 1e-5
