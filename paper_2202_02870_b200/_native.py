@@ -44,6 +44,7 @@ _SIGNATURES = {
     "ltb_ctx_set_stream": ([_vp, _vp], _int),
     "ltb_ctx_synchronize": ([_vp], _int),
     "ltb_ctx_launch_count": ([_vp], _i64),
+    "ltb_ctx_stats": ([_vp, C.POINTER(_i64), _int], _int),
     "ltb_malloc": ([_vp, _i64, C.POINTER(_vp)], _int),
     "ltb_free": ([_vp, _vp], _int),
     "ltb_memcpy_h2d": ([_vp, _vp, _vp, _i64], _int),
@@ -144,6 +145,13 @@ def lib():
 
 def launch_count() -> int:
     return int(lib().ltb_ctx_launch_count(context()))
+
+
+def jacobi_stats(reset: bool = False) -> tuple:
+    """(slices solved, sweeps run) by the Jacobi kernels since the last reset."""
+    out = (_i64 * 2)()
+    check(lib().ltb_ctx_stats(context(), out, int(reset)))
+    return int(out[0]), int(out[1])
 
 
 def dtype_code(dt) -> int:

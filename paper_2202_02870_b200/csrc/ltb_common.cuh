@@ -131,6 +131,7 @@ struct ltb_ctx {
   double* h_scratch = nullptr;
   double* d_scratch = nullptr;  // 64 doubles
   unsigned int* d_counter = nullptr;
+  unsigned long long* d_stats = nullptr;  // [0] Jacobi slices, [1] Jacobi sweeps
 };
 
 struct ltb_spec {

@@ -69,12 +69,14 @@ int ltb_ctx_create(int device, ltb_ctx** out) {
   }
   if (cudaMallocHost(&ctx->h_scratch, 64 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&ctx->d_scratch, 64 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_counter, 64 * sizeof(unsigned int)) != cudaSuccess) {
+      cudaMalloc(&ctx->d_counter, 64 * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_stats, 8 * sizeof(unsigned long long)) != cudaSuccess) {
     cudaGetLastError();
     delete ctx;
     return LTB_EOOM;
   }
   cudaMemset(ctx->d_counter, 0, 64 * sizeof(unsigned int));
+  cudaMemset(ctx->d_stats, 0, 8 * sizeof(unsigned long long));
   cudaDeviceSynchronize();
   *out = ctx;
   return LTB_OK;
@@ -105,6 +107,16 @@ int ltb_ctx_synchronize(ltb_ctx* ctx) {
 }
 
 int64_t ltb_ctx_launch_count(const ltb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ltb_ctx_stats(ltb_ctx* ctx, int64_t* h_out, int reset) {
+  unsigned long long v[2] = {0, 0};
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(v, ctx->d_stats, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  h_out[0] = (int64_t)v[0];
+  h_out[1] = (int64_t)v[1];
+  if (reset) LTB_CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_stats, 0, sizeof(v), ctx->stream));
+  return LTB_OK;
+}
 
 int ltb_malloc(ltb_ctx* ctx, int64_t bytes, void** d_out) {
   if (bytes < 0) return ltb_set_error(ctx, LTB_EPARAM, "negative allocation size");

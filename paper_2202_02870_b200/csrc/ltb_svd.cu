@@ -29,7 +29,7 @@
 
 namespace {
 
-constexpr int kJacobiMaxThreads = 512;
+constexpr int kJacobiMaxThreads = 1024;
 
 template <typename R> struct eps_of;
 template <> struct eps_of<float> {
@@ -61,9 +61,10 @@ struct JacobiOut {
   void* d_out;       // batch x n real: (sigma - tau)_+ / sigma^2 in sorted order, or null
   double tau;
   const int* skip;   // device flag: nonzero -> return immediately
+  unsigned long long* stats;  // optional: [0] += slices, [1] += sweeps
 };
 
-template <typename T, bool WANT_V, bool GLOBAL>
+template <typename T, bool WANT_V, bool GLOBAL, int MPL>
 __global__ void __launch_bounds__(kJacobiMaxThreads)
     jacobi_kernel(int64_t I1, int64_t I2, const T* __restrict__ A, T* __restrict__ gws, JacobiOut o, int max_sweeps) {
   using R = typename scalar_traits<T>::real;
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
 
   const R tol = eps_of<R>::value * sqrt((R)max(m, 1));
   const int npl = n + (n & 1);
+  int sweeps_done = 0;
   for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
     int* rot = &flags[sweep & 1];
     for (int r = 0; r < npl - 1; ++r) {
@@ -130,11 +132,26 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
         T* wq = W + (size_t)q * mp;
         R al = 0, be = 0;
         T ga = zero_v<T>();
-        for (int i = lane; i < m; i += 32) {
-          const T x = wp[i], y = wq[i];
-          al += abs2_v(x);
-          be += abs2_v(y);
-          fma_acc(ga, conj_v(x), y);
+        // register-resident pair (MPL elements per lane): one shared-memory read
+        // and one write per element per rotation
+        T xr[MPL > 0 ? MPL : 1], yr[MPL > 0 ? MPL : 1];
+        if constexpr (MPL > 0) {
+#pragma unroll
+          for (int e = 0; e < MPL; ++e) {
+            const int i = lane + 32 * e;
+            xr[e] = (i < m) ? wp[i] : zero_v<T>();
+            yr[e] = (i < m) ? wq[i] : zero_v<T>();
+            al += abs2_v(xr[e]);
+            be += abs2_v(yr[e]);
+            fma_acc(ga, conj_v(xr[e]), yr[e]);
+          }
+        } else {
+          for (int i = lane; i < m; i += 32) {
+            const T x = wp[i], y = wq[i];
+            al += abs2_v(x);
+            be += abs2_v(y);
+            fma_acc(ga, conj_v(x), y);
+          }
         }
         al = warp_sum_r(al);
         be = warp_sum_r(be);
@@ -153,11 +170,23 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
         } else {
           ph = (gre >= 0) ? (R)1 : (R)-1;
         }
-        for (int i = lane; i < m; i += 32) {
-          const T x = wp[i];
-          const T y = ph * wq[i];
-          wp[i] = c * x - s * y;
-          wq[i] = s * x + c * y;
+        if constexpr (MPL > 0) {
+#pragma unroll
+          for (int e = 0; e < MPL; ++e) {
+            const int i = lane + 32 * e;
+            const T y = ph * yr[e];
+            if (i < m) {
+              wp[i] = c * xr[e] - s * y;
+              wq[i] = s * xr[e] + c * y;
+            }
+          }
+        } else {
+          for (int i = lane; i < m; i += 32) {
+            const T x = wp[i];
+            const T y = ph * wq[i];
+            wp[i] = c * x - s * y;
+            wq[i] = s * x + c * y;
+          }
         }
         if (WANT_V) {
           T* vp = V + (size_t)p * np_v;
@@ -177,7 +206,12 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
     __syncthreads();
     if (tid == 0) flags[(sweep + 1) & 1] = 0;
     __syncthreads();
+    sweeps_done = sweep + 1;
     if (!any) break;
+  }
+  if (o.stats && tid == 0) {
+    atomicAdd(&o.stats[0], 1ull);
+    atomicAdd(&o.stats[1], (unsigned long long)sweeps_done);
   }
 
   // ---- singular values = column norms
@@ -347,26 +381,43 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
   using R = typename scalar_traits<T>::real;
   const int m = (int)std::max(I1, I2), n = (int)std::min(I1, I2);
   const int max_sweeps = std::is_same<R, float>::value ? 40 : 60;
-  const int pairs = (n + 1) / 2;
-  int threads = 32 * std::min(16, std::max(2, pairs));
+  const int pairs = std::max(1, (n + 1) / 2);
   const size_t smem_full = jacobi_smem_bytes<T>(m, n, WANT_V);
   if (batch > 0x7fffffff) return ltb_set_error(ctx, LTB_ESHAPE, "svd: batch too large");
+  o.stats = ctx->d_stats;
   if (smem_full <= kSmemLimit) {
-    auto kern = jacobi_kernel<T, WANT_V, false>;
-    LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
-    kern<<<(unsigned)batch, threads, smem_full, ctx->stream>>>(I1, I2, A, nullptr, o, max_sweeps);
-    LTB_LAUNCH_CHECK(ctx);
-    return LTB_OK;
+    // warps per CTA: balance the n/2 pairs of a round, up to 24 warps when two
+    // CTAs share an SM and 32 when the slice needs the whole shared memory
+    const int maxw = smem_full <= 113 * 1024 ? 24 : 32;
+    const int per_warp = (pairs + maxw - 1) / maxw;
+    const int nwarps = std::max(1, (pairs + per_warp - 1) / per_warp);
+    const int threads = 32 * nwarps;
+    auto go = [&](auto kern) -> int {
+      LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
+      kern<<<(unsigned)batch, threads, smem_full, ctx->stream>>>(I1, I2, A, nullptr, o, max_sweeps);
+      LTB_LAUNCH_CHECK(ctx);
+      return LTB_OK;
+    };
+    constexpr bool big = std::is_same<T, cplx<double>>::value;
+    if (m <= 32) return go(jacobi_kernel<T, WANT_V, false, 1>);
+    if (m <= 64) return go(jacobi_kernel<T, WANT_V, false, 2>);
+    if (m <= 128) return go(jacobi_kernel<T, WANT_V, false, 4>);
+    if constexpr (!big) {
+      if (m <= 192) return go(jacobi_kernel<T, WANT_V, false, 6>);
+      if (m <= 256) return go(jacobi_kernel<T, WANT_V, false, 8>);
+    }
+    return go(jacobi_kernel<T, WANT_V, false, 0>);
   }
+  int threads = kJacobiMaxThreads;
   // global-workspace tier
   const size_t per = (size_t)n * (m | 1) + (WANT_V ? (size_t)n * (n | 1) : 0);
   T* ws = nullptr;
   LTB_TRY(ltb_ws_alloc(ctx, per * batch * sizeof(T), (void**)&ws));
   const size_t smem = (n + 1) * sizeof(R) + (n + 8) * sizeof(int) + 16;
-  auto kern = jacobi_kernel<T, WANT_V, true>;
+  auto kern = jacobi_kernel<T, WANT_V, true, 0>;
   if (smem > 48 * 1024)
     LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  threads = kJacobiMaxThreads;
+  threads = 512;
   kern<<<(unsigned)batch, threads, smem, ctx->stream>>>(I1, I2, A, ws, o, max_sweeps);
   LTB_LAUNCH_CHECK(ctx);
   ltb_ws_free(ctx, ws);
