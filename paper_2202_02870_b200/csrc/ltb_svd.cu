@@ -64,7 +64,7 @@ struct JacobiOut {
   unsigned long long* stats;  // optional: [0] += slices, [1] += sweeps
 };
 
-template <typename T, bool WANT_V, bool GLOBAL, int MPL>
+template <typename T, bool WANT_V, bool GLOBAL, int TS, int MPL>
 __global__ void __launch_bounds__(kJacobiMaxThreads)
     jacobi_kernel(int64_t I1, int64_t I2, const T* __restrict__ A, T* __restrict__ gws, JacobiOut o, int max_sweeps) {
   using R = typename scalar_traits<T>::real;
@@ -120,45 +120,56 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
 
   const R tol = eps_of<R>::value * sqrt((R)max(m, 1));
   const int npl = n + (n & 1);
+  const int npairs = npl / 2;
+  // teams of TS lanes each own one column pair per round (TPW teams per warp)
+  constexpr int TPW = 32 / TS;
+  const int tl = lane % TS;
+  const int team = lane / TS;
+  R* nrm = sig;  // squared column norms, exact at each sweep start, updated analytically
   int sweeps_done = 0;
   for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
     int* rot = &flags[sweep & 1];
+    for (int j = warp; j < n; j += nwarps) {
+      const T* wj = W + (size_t)j * mp;
+      R s2 = 0;
+      for (int i = lane; i < m; i += 32) s2 += abs2_v(wj[i]);
+      s2 = warp_sum_r(s2);
+      if (lane == 0) nrm[j] = s2;
+    }
+    __syncthreads();
     for (int r = 0; r < npl - 1; ++r) {
-      for (int k = warp; k < npl / 2; k += nwarps) {
-        int p, q;
-        rr_pair(npl, r, k, p, q);
-        if (p >= n || q >= n) continue;
-        T* wp = W + (size_t)p * mp;
-        T* wq = W + (size_t)q * mp;
-        R al = 0, be = 0;
+      for (int base = warp * TPW; base < npairs; base += nwarps * TPW) {
+        const int k = base + team;
+        int p = 0, q = 0;
+        if (k < npairs) rr_pair(npl, r, k, p, q);
+        const bool active = k < npairs && p < n && q < n;
+        T* wp = W + (size_t)(active ? p : 0) * mp;
+        T* wq = W + (size_t)(active ? q : 0) * mp;
         T ga = zero_v<T>();
-        // register-resident pair (MPL elements per lane): one shared-memory read
-        // and one write per element per rotation
         T xr[MPL > 0 ? MPL : 1], yr[MPL > 0 ? MPL : 1];
         if constexpr (MPL > 0) {
 #pragma unroll
           for (int e = 0; e < MPL; ++e) {
-            const int i = lane + 32 * e;
-            xr[e] = (i < m) ? wp[i] : zero_v<T>();
-            yr[e] = (i < m) ? wq[i] : zero_v<T>();
-            al += abs2_v(xr[e]);
-            be += abs2_v(yr[e]);
+            const int i = tl + TS * e;
+            const bool ok = active && i < m;
+            xr[e] = ok ? wp[i] : zero_v<T>();
+            yr[e] = ok ? wq[i] : zero_v<T>();
             fma_acc(ga, conj_v(xr[e]), yr[e]);
           }
         } else {
-          for (int i = lane; i < m; i += 32) {
-            const T x = wp[i], y = wq[i];
-            al += abs2_v(x);
-            be += abs2_v(y);
-            fma_acc(ga, conj_v(x), y);
-          }
+          if (active)
+            for (int i = tl; i < m; i += TS) fma_acc(ga, conj_v(wp[i]), wq[i]);
         }
-        al = warp_sum_r(al);
-        be = warp_sum_r(be);
-        R gre = warp_sum_r(re_v(ga));
-        R gim = CPLX ? warp_sum_r(im_v(ga)) : (R)0;
+        R gre = re_v(ga), gim = im_v(ga);
+#pragma unroll
+        for (int o = TS / 2; o > 0; o >>= 1) {
+          gre += __shfl_xor_sync(0xffffffffu, gre, o);
+          if (CPLX) gim += __shfl_xor_sync(0xffffffffu, gim, o);
+        }
+        const R al = active ? nrm[p] : (R)0;
+        const R be = active ? nrm[q] : (R)0;
         const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
-        if (!(gabs > tol * sqrt(al) * sqrt(be)) || al == (R)0 || be == (R)0) continue;
+        if (!active || !(gabs > tol * sqrt(al) * sqrt(be)) || al == (R)0 || be == (R)0) continue;
         const R zeta = (be - al) / (2 * gabs);
         const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
         const R c = (R)1 / sqrt((R)1 + t * t);
@@ -173,7 +184,7 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
         if constexpr (MPL > 0) {
 #pragma unroll
           for (int e = 0; e < MPL; ++e) {
-            const int i = lane + 32 * e;
+            const int i = tl + TS * e;
             const T y = ph * yr[e];
             if (i < m) {
               wp[i] = c * xr[e] - s * y;
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
             }
           }
         } else {
-          for (int i = lane; i < m; i += 32) {
+          for (int i = tl; i < m; i += TS) {
             const T x = wp[i];
             const T y = ph * wq[i];
             wp[i] = c * x - s * y;
@@ -191,14 +202,19 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
         if (WANT_V) {
           T* vp = V + (size_t)p * np_v;
           T* vq = V + (size_t)q * np_v;
-          for (int i = lane; i < n; i += 32) {
+          for (int i = tl; i < n; i += TS) {
             const T x = vp[i];
             const T y = ph * vq[i];
             vp[i] = c * x - s * y;
             vq[i] = s * x + c * y;
           }
         }
-        if (lane == 0) *rot = 1;
+        if (tl == 0) {
+          // alpha' = alpha - t|gamma|, beta' = beta + t|gamma| for the rotation that zeroes gamma
+          nrm[p] = fmax(al - t * gabs, (R)0);
+          nrm[q] = be + t * gabs;
+          *rot = 1;
+        }
       }
       __syncthreads();
     }
@@ -389,24 +405,28 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
     // warps per CTA: balance the n/2 pairs of a round, up to 24 warps when two
     // CTAs share an SM and 32 when the slice needs the whole shared memory
     const int maxw = smem_full <= 113 * 1024 ? 24 : 32;
-    const int per_warp = (pairs + maxw - 1) / maxw;
-    const int nwarps = std::max(1, (pairs + per_warp - 1) / per_warp);
-    const int threads = 32 * nwarps;
-    auto go = [&](auto kern) -> int {
+    auto go = [&](auto kern, int ts) -> int {
+      const int teams = std::max(1, (pairs * ts + 31) / 32);  // warps needed for one pair per team
+      const int per_warp = (teams + maxw - 1) / maxw;
+      const int nwarps = std::max(1, (teams + per_warp - 1) / per_warp);
+      const int threads = 32 * nwarps;
       LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
       kern<<<(unsigned)batch, threads, smem_full, ctx->stream>>>(I1, I2, A, nullptr, o, max_sweeps);
       LTB_LAUNCH_CHECK(ctx);
       return LTB_OK;
     };
     constexpr bool big = std::is_same<T, cplx<double>>::value;
-    if (m <= 32) return go(jacobi_kernel<T, WANT_V, false, 1>);
-    if (m <= 64) return go(jacobi_kernel<T, WANT_V, false, 2>);
-    if (m <= 128) return go(jacobi_kernel<T, WANT_V, false, 4>);
+    if (m <= 8) return go(jacobi_kernel<T, WANT_V, false, 8, 1>, 8);
+    if (m <= 32) return go(jacobi_kernel<T, WANT_V, false, 8, 4>, 8);
+    if (m <= 64) return go(jacobi_kernel<T, WANT_V, false, 16, 4>, 16);
     if constexpr (!big) {
-      if (m <= 192) return go(jacobi_kernel<T, WANT_V, false, 6>);
-      if (m <= 256) return go(jacobi_kernel<T, WANT_V, false, 8>);
+      if (m <= 128) return go(jacobi_kernel<T, WANT_V, false, 16, 8>, 16);
+      if (m <= 192) return go(jacobi_kernel<T, WANT_V, false, 16, 12>, 16);
+      if (m <= 256) return go(jacobi_kernel<T, WANT_V, false, 32, 8>, 32);
+    } else {
+      if (m <= 128) return go(jacobi_kernel<T, WANT_V, false, 32, 4>, 32);
     }
-    return go(jacobi_kernel<T, WANT_V, false, 0>);
+    return go(jacobi_kernel<T, WANT_V, false, 32, 0>, 32);
   }
   int threads = kJacobiMaxThreads;
   // global-workspace tier
@@ -414,7 +434,7 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
   T* ws = nullptr;
   LTB_TRY(ltb_ws_alloc(ctx, per * batch * sizeof(T), (void**)&ws));
   const size_t smem = (n + 1) * sizeof(R) + (n + 8) * sizeof(int) + 16;
-  auto kern = jacobi_kernel<T, WANT_V, true, 0>;
+  auto kern = jacobi_kernel<T, WANT_V, true, 32, 0>;
   if (smem > 48 * 1024)
     LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   threads = 512;
