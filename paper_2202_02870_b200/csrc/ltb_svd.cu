@@ -64,9 +64,10 @@ struct JacobiOut {
   unsigned long long* stats;  // optional: [0] += slices, [1] += sweeps
 };
 
-template <typename T, bool WANT_V, bool GLOBAL, int TS, int MPL>
-__global__ void __launch_bounds__(kJacobiMaxThreads)
-    jacobi_kernel(int64_t I1, int64_t I2, const T* __restrict__ A, T* __restrict__ gws, JacobiOut o, int max_sweeps) {
+template <typename T, bool WANT_V, bool GLOBAL, int TS, int MPL, int MINB>
+__global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
+    jacobi_kernel(int64_t I1, int64_t I2, const T* __restrict__ A, T* __restrict__ gws, JacobiOut o, int max_sweeps,
+                  int mp) {
   using R = typename scalar_traits<T>::real;
   constexpr bool CPLX = scalar_traits<T>::is_complex;
   if (o.skip && *o.skip) return;
@@ -74,7 +75,6 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
   const bool trans = I1 < I2;
   const int m = (int)(trans ? I2 : I1);
   const int n = (int)(trans ? I1 : I2);
-  const int mp = m | 1;
   const int np_v = n | 1;
   const int64_t b = blockIdx.x;
   const T* Ab = A + b * I1 * I2;
@@ -109,6 +109,13 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
       W[(size_t)j * mp + i] = conj_v(Ab[l]);
     }
   }
+  if (mp > m) {  // zero padding rows: register tiles need no row predicates
+    const int pad = mp - m;
+    for (int l = tid; l < n * pad; l += nth) {
+      const int j = l / pad, i = m + (l - j * pad);
+      W[(size_t)j * mp + i] = zero_v<T>();
+    }
+  }
   if (WANT_V) {
     for (int l = tid; l < n * n; l += nth) {
       const int j = l / n, k = l - j * n;
@@ -141,7 +148,18 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
       for (int base = warp * TPW; base < npairs; base += nwarps * TPW) {
         const int k = base + team;
         int p = 0, q = 0;
-        if (k < npairs) rr_pair(npl, r, k, p, q);
+        if (k < npairs) {  // circle-method pairing without integer division
+          const int m1 = npl - 1;
+          if (k == 0) {
+            p = m1;
+            q = r;
+          } else {
+            p = r + k;
+            p -= (p >= m1) ? m1 : 0;
+            q = r - k;
+            q += (q < 0) ? m1 : 0;
+          }
+        }
         const bool active = k < npairs && p < n && q < n;
         T* wp = W + (size_t)(active ? p : 0) * mp;
         T* wq = W + (size_t)(active ? q : 0) * mp;
@@ -150,10 +168,9 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
         if constexpr (MPL > 0) {
 #pragma unroll
           for (int e = 0; e < MPL; ++e) {
-            const int i = tl + TS * e;
-            const bool ok = active && i < m;
-            xr[e] = ok ? wp[i] : zero_v<T>();
-            yr[e] = ok ? wq[i] : zero_v<T>();
+            const int i = tl + TS * e;  // rows >= m are zero padding
+            xr[e] = wp[i];
+            yr[e] = wq[i];
             fma_acc(ga, conj_v(xr[e]), yr[e]);
           }
         } else {
@@ -186,10 +203,8 @@ __global__ void __launch_bounds__(kJacobiMaxThreads)
           for (int e = 0; e < MPL; ++e) {
             const int i = tl + TS * e;
             const T y = ph * yr[e];
-            if (i < m) {
-              wp[i] = c * xr[e] - s * y;
-              wq[i] = s * xr[e] + c * y;
-            }
+            wp[i] = c * xr[e] - s * y;
+            wq[i] = s * xr[e] + c * y;
           }
         } else {
           for (int i = tl; i < m; i += TS) {
@@ -384,61 +399,75 @@ __global__ void cols_to_rowmajor_kernel(int64_t batch, int n, const T* __restric
 }
 
 template <typename T>
-size_t jacobi_smem_bytes(int m, int n, bool want_v) {
+size_t jacobi_smem_bytes(int m, int n, bool want_v, int mp_) {
   using R = typename scalar_traits<T>::real;
-  const size_t mp = (size_t)(m | 1), np_v = (size_t)(n | 1);
+  const size_t mp = (size_t)mp_, np_v = (size_t)(n | 1);
   return ((size_t)n * mp + (want_v ? (size_t)n * np_v : 0)) * sizeof(T) + (n + 1) * sizeof(R) + (n + 8) * sizeof(int) + 16;
 }
 
 constexpr size_t kSmemLimit = 225 * 1024;
+
+// one shared-memory variant: TS lanes per column pair, MPL rows per lane (0 =
+// looped), MINB CTAs per SM (2 -> at most 576 threads and 56 registers)
+template <typename T, bool WANT_V, int TS, int MPL, int MINB>
+int launch_smem_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, const JacobiOut& o,
+                        int max_sweeps, int m, int n) {
+  const int mp = MPL > 0 ? TS * MPL : (m | 1);
+  const size_t smem = jacobi_smem_bytes<T>(m, n, WANT_V, mp);
+  const int pairs = std::max(1, (n + 1) / 2);
+  const int maxw = MINB == 2 ? 18 : 32;
+  const int teams = std::max(1, (pairs * TS + 31) / 32);  // warps for one pair per team
+  const int per_warp = (teams + maxw - 1) / maxw;
+  const int nwarps = std::max(1, (teams + per_warp - 1) / per_warp);
+  auto kern = jacobi_kernel<T, WANT_V, false, TS, MPL, MINB>;
+  LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         (int)cudaSharedmemCarveoutMaxShared));
+  kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, nullptr, o, max_sweeps, mp);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
+
+template <typename T, bool WANT_V, int TS, int MPL>
+int launch_smem(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, const JacobiOut& o, int max_sweeps,
+                int m, int n) {
+  const int mp = MPL > 0 ? TS * MPL : (m | 1);
+  // two CTAs per SM when two slices fit in shared memory (228 KB per SM, 1 KB reserved per CTA)
+  if (2 * (jacobi_smem_bytes<T>(m, n, WANT_V, mp) + 1024) <= 228 * 1024)
+    return launch_smem_variant<T, WANT_V, TS, MPL, 2>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+  return launch_smem_variant<T, WANT_V, TS, MPL, 1>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+}
 
 template <typename T, bool WANT_V>
 int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, JacobiOut o) {
   using R = typename scalar_traits<T>::real;
   const int m = (int)std::max(I1, I2), n = (int)std::min(I1, I2);
   const int max_sweeps = std::is_same<R, float>::value ? 40 : 60;
-  const int pairs = std::max(1, (n + 1) / 2);
-  const size_t smem_full = jacobi_smem_bytes<T>(m, n, WANT_V);
   if (batch > 0x7fffffff) return ltb_set_error(ctx, LTB_ESHAPE, "svd: batch too large");
   o.stats = ctx->d_stats;
-  if (smem_full <= kSmemLimit) {
-    // warps per CTA: balance the n/2 pairs of a round, up to 24 warps when two
-    // CTAs share an SM and 32 when the slice needs the whole shared memory
-    const int maxw = smem_full <= 113 * 1024 ? 24 : 32;
-    auto go = [&](auto kern, int ts) -> int {
-      const int teams = std::max(1, (pairs * ts + 31) / 32);  // warps needed for one pair per team
-      const int per_warp = (teams + maxw - 1) / maxw;
-      const int nwarps = std::max(1, (teams + per_warp - 1) / per_warp);
-      const int threads = 32 * nwarps;
-      LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
-      kern<<<(unsigned)batch, threads, smem_full, ctx->stream>>>(I1, I2, A, nullptr, o, max_sweeps);
-      LTB_LAUNCH_CHECK(ctx);
-      return LTB_OK;
-    };
-    constexpr bool big = std::is_same<T, cplx<double>>::value;
-    if (m <= 8) return go(jacobi_kernel<T, WANT_V, false, 8, 1>, 8);
-    if (m <= 32) return go(jacobi_kernel<T, WANT_V, false, 8, 4>, 8);
-    if (m <= 64) return go(jacobi_kernel<T, WANT_V, false, 16, 4>, 16);
-    if constexpr (!big) {
-      if (m <= 128) return go(jacobi_kernel<T, WANT_V, false, 16, 8>, 16);
-      if (m <= 192) return go(jacobi_kernel<T, WANT_V, false, 16, 12>, 16);
-      if (m <= 256) return go(jacobi_kernel<T, WANT_V, false, 32, 8>, 32);
-    } else {
-      if (m <= 128) return go(jacobi_kernel<T, WANT_V, false, 32, 4>, 32);
-    }
-    return go(jacobi_kernel<T, WANT_V, false, 32, 0>, 32);
+  constexpr bool big = std::is_same<T, cplx<double>>::value;
+  auto fits = [&](int mp) { return jacobi_smem_bytes<T>(m, n, WANT_V, mp) <= kSmemLimit; };
+  if (m <= 8 && fits(8)) return launch_smem<T, WANT_V, 8, 1>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+  if (m <= 32 && fits(32)) return launch_smem<T, WANT_V, 8, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+  if (m <= 64 && fits(64)) return launch_smem<T, WANT_V, 16, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+  if constexpr (!big) {
+    if (m <= 128 && fits(128)) return launch_smem<T, WANT_V, 16, 8>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+    if (m <= 192 && fits(192)) return launch_smem<T, WANT_V, 16, 12>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+    if (m <= 256 && fits(256)) return launch_smem<T, WANT_V, 32, 8>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+  } else {
+    if (m <= 128 && fits(128)) return launch_smem<T, WANT_V, 32, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   }
-  int threads = kJacobiMaxThreads;
-  // global-workspace tier
-  const size_t per = (size_t)n * (m | 1) + (WANT_V ? (size_t)n * (n | 1) : 0);
+  if (fits(m | 1)) return launch_smem<T, WANT_V, 32, 0>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+  // global-workspace tier: the working columns live in an L2-resident buffer
+  const int mp = m | 1;
+  const size_t per = (size_t)n * mp + (WANT_V ? (size_t)n * (n | 1) : 0);
   T* ws = nullptr;
   LTB_TRY(ltb_ws_alloc(ctx, per * batch * sizeof(T), (void**)&ws));
   const size_t smem = (n + 1) * sizeof(R) + (n + 8) * sizeof(int) + 16;
-  auto kern = jacobi_kernel<T, WANT_V, true, 32, 0>;
+  auto kern = jacobi_kernel<T, WANT_V, true, 32, 0, 1>;
   if (smem > 48 * 1024)
     LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  threads = 512;
-  kern<<<(unsigned)batch, threads, smem, ctx->stream>>>(I1, I2, A, ws, o, max_sweeps);
+  kern<<<(unsigned)batch, 512, smem, ctx->stream>>>(I1, I2, A, ws, o, max_sweeps, mp);
   LTB_LAUNCH_CHECK(ctx);
   ltb_ws_free(ctx, ws);
   return LTB_OK;
