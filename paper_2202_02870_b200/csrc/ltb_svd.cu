@@ -53,6 +53,11 @@ __device__ __forceinline__ void rr_pair(int np, int r, int k, int& p, int& q) {
 
 template <typename R> __device__ __forceinline__ R warp_sum_r(R v) { return warp_sum(v); }
 
+// two consecutive elements, one vector shared-memory access (LDS.64 / LDS.128)
+template <typename T> struct alignas(2 * sizeof(T)) vec2 {
+  T a, b;
+};
+
 struct JacobiOut {
   void* w_out;       // batch x n x m (column j contiguous, sorted) or null
   void* sv_out;      // batch x n real, descending, or null
@@ -71,7 +76,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   using R = typename scalar_traits<T>::real;
   constexpr bool CPLX = scalar_traits<T>::is_complex;
   if (o.skip && *o.skip) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const bool trans = I1 < I2;
   const int m = (int)(trans ? I2 : I1);
   const int n = (int)(trans ? I1 : I2);
@@ -166,12 +171,18 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
         T ga = zero_v<T>();
         T xr[MPL > 0 ? MPL : 1], yr[MPL > 0 ? MPL : 1];
         if constexpr (MPL > 0) {
+          // two consecutive rows per vector access (rows >= m are zero padding)
 #pragma unroll
-          for (int e = 0; e < MPL; ++e) {
-            const int i = tl + TS * e;  // rows >= m are zero padding
-            xr[e] = wp[i];
-            yr[e] = wq[i];
+          for (int e = 0; e < MPL; e += 2) {
+            const int i = 2 * tl + TS * e;
+            const vec2<T> vx = *reinterpret_cast<const vec2<T>*>(wp + i);
+            const vec2<T> vy = *reinterpret_cast<const vec2<T>*>(wq + i);
+            xr[e] = vx.a;
+            xr[e + 1] = vx.b;
+            yr[e] = vy.a;
+            yr[e + 1] = vy.b;
             fma_acc(ga, conj_v(xr[e]), yr[e]);
+            fma_acc(ga, conj_v(xr[e + 1]), yr[e + 1]);
           }
         } else {
           if (active)
@@ -199,12 +210,30 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
           ph = (gre >= 0) ? (R)1 : (R)-1;
         }
         if constexpr (MPL > 0) {
+          // real: fold the sign into the rotation; complex: phase the q column first
+          R cq = c, sq = s;
+          if constexpr (!CPLX) {
+            cq = c * re_v(ph);
+            sq = s * re_v(ph);
+          }
 #pragma unroll
-          for (int e = 0; e < MPL; ++e) {
-            const int i = tl + TS * e;
-            const T y = ph * yr[e];
-            wp[i] = c * xr[e] - s * y;
-            wq[i] = s * xr[e] + c * y;
+          for (int e = 0; e < MPL; e += 2) {
+            const int i = 2 * tl + TS * e;
+            vec2<T> vx, vy;
+            if constexpr (CPLX) {
+              const T y0 = ph * yr[e], y1 = ph * yr[e + 1];
+              vx.a = c * xr[e] - s * y0;
+              vx.b = c * xr[e + 1] - s * y1;
+              vy.a = s * xr[e] + c * y0;
+              vy.b = s * xr[e + 1] + c * y1;
+            } else {
+              vx.a = c * xr[e] - sq * yr[e];
+              vx.b = c * xr[e + 1] - sq * yr[e + 1];
+              vy.a = s * xr[e] + cq * yr[e];
+              vy.b = s * xr[e + 1] + cq * yr[e + 1];
+            }
+            *reinterpret_cast<vec2<T>*>(wp + i) = vx;
+            *reinterpret_cast<vec2<T>*>(wq + i) = vy;
           }
         } else {
           for (int i = tl; i < m; i += TS) {
@@ -447,7 +476,7 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
   o.stats = ctx->d_stats;
   constexpr bool big = std::is_same<T, cplx<double>>::value;
   auto fits = [&](int mp) { return jacobi_smem_bytes<T>(m, n, WANT_V, mp) <= kSmemLimit; };
-  if (m <= 8 && fits(8)) return launch_smem<T, WANT_V, 8, 1>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
+  if (m <= 8 && fits(8)) return launch_smem<T, WANT_V, 4, 2>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   if (m <= 32 && fits(32)) return launch_smem<T, WANT_V, 8, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   if (m <= 64 && fits(64)) return launch_smem<T, WANT_V, 16, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   if constexpr (!big) {
