@@ -86,8 +86,8 @@ struct LoadPGA {
       const R y = momentum<R>(xc[e], xp[e], beta);
       const bool obs = (mask[e >> 5] >> (e & 31)) & 1u;
       const R g = gradient_point<R>(y, pobs[e], obs);
-      const int t = l / P;
-      const int q = l - t * P;
+      int t, q;
+      split_tube(l, P, p.invP, t, q);
       S[q * pitch + t] = cvt<Tc>(g);
     }
   }
@@ -110,8 +110,8 @@ struct StorePGA {
     const int64_t e0 = tube0 * P;
     const int cnt = nt * P;
     for (int l = tid; l < cnt; l += kXformThreads) {
-      const int t = l / P;
-      const int q = l - t * P;
+      int t, q;
+      split_tube(l, P, p.invP, t, q);
       const Tc v = S[q * pitch + t];
       const int64_t e = e0 + l;
       const R x1 = re_v(v);
@@ -196,65 +196,53 @@ __global__ void pga_fetch_kernel(int64_t E, const R* __restrict__ x, const R* __
   }
 }
 
-template <typename R>
-int pga_iteration(ltb_pga* g, int k, double beta, double mu, double tol, double* rec) {
+// tile plan of the fused transforms for this spec and compute type (0 if too long)
+template <typename Tc, typename Tm>
+int pga_plan(const ltb_spec* spec, int64_t NT, int inverse, XformParams& p, size_t* smem) {
+  p = XformParams{};
+  p.NT = NT;
+  build_steps(spec, inverse, p);
+  return plan_tile<Tc, Tm>(p, smem);
+}
+
+template <typename R, typename Tc, typename Tm>
+int pga_transforms(ltb_pga* g, int k, double beta, double mu, double tol, double* rec) {
   ltb_ctx* ctx = g->ctx;
-  const bool cm = g->spec->is_complex != 0;
   const R* xc = (const R*)g->x[cur_of(k)];
   const R* xp = (const R*)g->x[prev_of(k)];
   R* xn = (R*)g->x[next_of(k)];
   const int* skip = g->d_state;
   const int dbl = std::is_same<R, double>::value ? 1 : 0;
-  XformParams p{};
-  p.NT = g->NT;
-  // forward: gradient step fused into the load, slice-major complex/real store
+  XformParams p;
+  size_t smem = 0;
+  // forward: gradient step fused into the load, slice-major store
+  if (!pga_plan<Tc, Tm>(g->spec, g->NT, 0, p, &smem))
+    return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
   {
-    build_steps(g->spec, 0, p);
     LoadPGA<R> ld{xc, xp, (const R*)g->pobs, g->mask, (R)beta};
-    if (cm) {
-      using Tc = cplx<R>;
-      size_t smem = 0;
-      p.TT = choose_tt<Tc>(p.P, &smem);
-      if (!p.TT) return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
-      p.pitch = p.TT + 1;
-      StorePlain<Tc, false> st{(Tc*)g->hat_a, LTB_SLICE_MAJOR};
-      LTB_TRY((launch_xform_tile<Tc, Tc>(ctx, p, ld, st, (const Tc*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
-    } else {
-      using Tc = R;
-      size_t smem = 0;
-      p.TT = choose_tt<Tc>(p.P, &smem);
-      if (!p.TT) return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
-      p.pitch = p.TT + 1;
-      StorePlain<Tc, false> st{(Tc*)g->hat_a, LTB_SLICE_MAJOR};
-      LTB_TRY((launch_xform_tile<Tc, R>(ctx, p, ld, st, (const R*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
-    }
+    StorePlain<Tc, false> st{(Tc*)g->hat_a, LTB_SLICE_MAJOR};
+    LTB_TRY((launch_xform_tile<Tc, Tm>(ctx, p, ld, st, (const Tm*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
   }
   // slice SVT with tau = mu_k
   LTB_TRY(ltb_svt_impl(ctx, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, nullptr, g->hat_b, skip));
   // inverse with the fused norms epilogue
+  if (!pga_plan<Tc, Tm>(g->spec, g->NT, 1, p, &smem))
+    return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
   {
-    build_steps(g->spec, 1, p);
     StorePGA<R> st{xn, xc, xp, (const R*)g->gt, (R)beta};
-    if (cm) {
-      using Tc = cplx<R>;
-      size_t smem = 0;
-      p.TT = choose_tt<Tc>(p.P, &smem);
-      p.pitch = p.TT + 1;
-      LoadPlain<Tc> ld{(const Tc*)g->hat_b, LTB_SLICE_MAJOR};
-      LTB_TRY((launch_xform_tile<Tc, Tc>(ctx, p, ld, st, (const Tc*)g->spec->d_mats[dbl][1], g->partials, skip, smem)));
-    } else {
-      using Tc = R;
-      size_t smem = 0;
-      p.TT = choose_tt<Tc>(p.P, &smem);
-      p.pitch = p.TT + 1;
-      LoadPlain<Tc> ld{(const Tc*)g->hat_b, LTB_SLICE_MAJOR};
-      LTB_TRY((launch_xform_tile<Tc, R>(ctx, p, ld, st, (const R*)g->spec->d_mats[dbl][1], g->partials, skip, smem)));
-    }
-    g->nblocks = (p.NT + p.TT - 1) / p.TT;
+    LoadPlain<Tc> ld{(const Tc*)g->hat_b, LTB_SLICE_MAJOR};
+    LTB_TRY((launch_xform_tile<Tc, Tm>(ctx, p, ld, st, (const Tm*)g->spec->d_mats[dbl][1], g->partials, skip, smem,
+                                       &g->nblocks)));
   }
   pga_finalize_kernel<<<1, 160, 0, ctx->stream>>>(g->partials, g->nblocks, rec, g->d_state, g->d_scalars, tol);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
+}
+
+template <typename R>
+int pga_iteration(ltb_pga* g, int k, double beta, double mu, double tol, double* rec) {
+  if (g->spec->is_complex) return pga_transforms<R, cplx<R>, cplx<R>>(g, k, beta, mu, tol, rec);
+  return pga_transforms<R, R, R>(g, k, beta, mu, tol, rec);
 }
 
 }  // namespace
@@ -280,8 +268,11 @@ int ltb_pga_create(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t i1, in
   const size_t rs = dtype_size(dtype), hs = dtype_size(g->hat_dtype);
   const int64_t E = g->E;
   size_t smem = 0;
-  const int tt = cm ? (dtype == LTB_F64 ? choose_tt<cplx<double>>((int)g->P, &smem) : choose_tt<cplx<float>>((int)g->P, &smem))
-                    : (dtype == LTB_F64 ? choose_tt<double>((int)g->P, &smem) : choose_tt<float>((int)g->P, &smem));
+  XformParams plan;
+  const int tt = cm ? (dtype == LTB_F64 ? pga_plan<cplx<double>, cplx<double>>(spec, g->NT, 1, plan, &smem)
+                                        : pga_plan<cplx<float>, cplx<float>>(spec, g->NT, 1, plan, &smem))
+                    : (dtype == LTB_F64 ? pga_plan<double, double>(spec, g->NT, 1, plan, &smem)
+                                        : pga_plan<float, float>(spec, g->NT, 1, plan, &smem));
   if (!tt) {
     delete g;
     return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube of %lld elements does not fit the fused transform tile",

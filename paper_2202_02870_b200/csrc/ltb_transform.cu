@@ -168,19 +168,18 @@ int run_transform(ltb_ctx* ctx, XformParams p, const void* in, int layout_in, vo
   constexpr bool residual = (IC || CM) && !OC;
   const Tm* mats = (const Tm*)mats_v;
   size_t smem = 0;
-  const int TT = choose_tt<Tc>(p.P, &smem);
+  const int TT = plan_tile<Tc, Tm>(p, &smem);
   if (!TT) return run_global<Tc, Tm, Tin, Tout>(ctx, p, in, layout_in, out, layout_out, mats, d_sumsq);
-  p.TT = TT;
-  p.pitch = TT + 1;
   const int64_t nblocks = (p.NT + TT - 1) / TT;
   double* partials = nullptr;
   if (residual && d_sumsq) LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * 2 * nblocks, (void**)&partials));
   LoadPlain<Tin> ld{(const Tin*)in, layout_in};
   StorePlain<Tout, residual> st{(Tout*)out, layout_out};
-  LTB_TRY((launch_xform_tile<Tc, Tm>(ctx, p, ld, st, mats, partials, nullptr, smem)));
+  int64_t grid = 0;
+  LTB_TRY((launch_xform_tile<Tc, Tm>(ctx, p, ld, st, mats, partials, nullptr, smem, &grid)));
   if (d_sumsq) {
     if (partials) {
-      finalize_partials_kernel<<<1, 64, 0, ctx->stream>>>(partials, nblocks, 2, 0u, d_sumsq);
+      finalize_partials_kernel<<<1, 64, 0, ctx->stream>>>(partials, grid, 2, 0u, d_sumsq);
       LTB_LAUNCH_CHECK(ctx);
       ltb_ws_free(ctx, partials);
     } else {

@@ -6,15 +6,19 @@
 // (core.py:110-122) along the spec's modes, ascending forward, reversed
 // inverse.  One CTA owns TT consecutive tubes (a tube = the P trailing
 // elements of one (i1, i2)); the tile lives in shared memory q-major with the
-// tube index fastest (pitch TT+1), so every mode product reads conflict-free
-// and the small per-mode matrices are warp-uniform broadcast loads.
+// tube index fastest (pitch TT+1), so every mode product reads conflict-free.
+// The per-mode matrices are staged once per CTA in shared memory, transposed
+// and zero-padded to a multiple of the register block, so each inner step is
+// one tile load + vector broadcast loads of RB matrix entries + RB FMAs.
 #pragma once
 #include "ltb_dispatch.cuh"
 
 struct ModeStep {
   int n;
+  int npad;  // n rounded up to the register block (smem matrix row length)
   int64_t hi, lo;
-  int64_t mat_off;
+  int64_t mat_off;   // element offset of the row-major matrix in global memory
+  int smem_off;      // element offset of the transposed padded matrix in shared memory
 };
 
 struct XformParams {
@@ -23,10 +27,16 @@ struct XformParams {
   int P;
   int64_t NT;
   int TT;
+  int ttshift;  // log2(TT)
   int pitch;
+  float invP;   // 1/P for division-free index math
+  int mats_in_smem;
+  int mat_smem_elems;
 };
 
 constexpr int kXformThreads = 256;
+
+template <typename Tc> constexpr int xform_rb() { return scalar_traits<Tc>::is_complex ? 4 : 8; }
 
 inline void build_steps(const ltb_spec* spec, int inverse, XformParams& p) {
   p.nsteps = spec->nmodes;
@@ -42,6 +52,33 @@ inline void build_steps(const ltb_spec* spec, int inverse, XformParams& p) {
     p.step[k].mat_off = spec->mat_off[m];
   }
   p.P = (int)spec->P;
+  p.invP = 1.0f / (float)p.P;
+}
+
+// smem layout of the matrices for compute type Tc (register block RB)
+template <typename Tc>
+inline void plan_matrices(XformParams& p) {
+  constexpr int RB = xform_rb<Tc>();
+  int off = 0;
+  for (int s = 0; s < p.nsteps; ++s) {
+    p.step[s].npad = (p.step[s].n + RB - 1) / RB * RB;
+    p.step[s].smem_off = off;
+    off += p.step[s].n * p.step[s].npad;
+  }
+  p.mat_smem_elems = off;
+}
+
+// l -> (t, q) with l = t * P + q, without an integer division (l < 2^24)
+__device__ __forceinline__ void split_tube(int l, int P, float invP, int& t, int& q) {
+  t = __float2int_rz((float)l * invP);
+  q = l - t * P;
+  if (q < 0) {
+    --t;
+    q += P;
+  } else if (q >= P) {
+    ++t;
+    q -= P;
+  }
 }
 
 // ---------------------------------------------------------------- loaders
@@ -56,15 +93,15 @@ struct LoadPlain {
       const Tin* src = in + tube0 * P;
       const int cnt = nt * P;
       for (int l = tid; l < cnt; l += kXformThreads) {
-        const int t = l / P;
-        const int q = l - t * P;
+        int t, q;
+        split_tube(l, P, p.invP, t, q);
         S[q * pitch + t] = cvt<Tc>(src[l]);
       }
     } else {
       const int cnt = P * TT;
       for (int l = tid; l < cnt; l += kXformThreads) {
-        const int q = l / TT;
-        const int t = l - q * TT;
+        const int q = l >> p.ttshift;
+        const int t = l & (TT - 1);
         if (t < nt) S[q * pitch + t] = cvt<Tc>(in[(int64_t)q * p.NT + tube0 + t]);
       }
     }
@@ -87,8 +124,8 @@ struct StorePlain {
       Tout* o = out + tube0 * P;
       const int cnt = nt * P;
       for (int l = tid; l < cnt; l += kXformThreads) {
-        const int t = l / P;
-        const int q = l - t * P;
+        int t, q;
+        split_tube(l, P, p.invP, t, q);
         const Tc v = S[q * pitch + t];
         if (RESIDUAL) {
           acc[0] += (double)abs2_v(v);
@@ -99,8 +136,8 @@ struct StorePlain {
     } else {
       const int cnt = P * TT;
       for (int l = tid; l < cnt; l += kXformThreads) {
-        const int q = l / TT;
-        const int t = l - q * TT;
+        const int q = l >> p.ttshift;
+        const int t = l & (TT - 1);
         if (t < nt) {
           const Tc v = S[q * pitch + t];
           if (RESIDUAL) {
@@ -114,37 +151,65 @@ struct StorePlain {
   }
 };
 
+// RB consecutive matrix entries, one or two vector loads
+template <typename Tm, int RB> struct alignas(sizeof(Tm) * RB >= 16 ? 16 : sizeof(Tm) * RB) mrow {
+  Tm v[RB];
+};
+
 // ---------------------------------------------------------------- kernel
 template <typename Tc, typename Tm, class Loader, class Storer>
 __global__ void __launch_bounds__(kXformThreads)
     xform_tile_kernel(XformParams p, Loader ld, Storer st, const Tm* __restrict__ mats, double* __restrict__ partials,
                       const int* __restrict__ skip) {
   if (skip && *skip) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Tc* S0 = reinterpret_cast<Tc*>(smem_raw);
+  constexpr int RB = xform_rb<Tc>();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Tm* Ms = reinterpret_cast<Tm*>(smem_raw);
+  const int mat_bytes = p.mats_in_smem ? (p.mat_smem_elems * (int)sizeof(Tm) + 127) / 128 * 128 : 0;
+  Tc* S0 = reinterpret_cast<Tc*>(smem_raw + mat_bytes);
   Tc* S1 = S0 + (size_t)p.P * p.pitch;
   const int tid = threadIdx.x;
   const int TT = p.TT;
   const int pitch = p.pitch;
-  const int64_t tube0 = (int64_t)blockIdx.x * TT;
-  const int nt = (int)min((int64_t)TT, p.NT - tube0);
 
+  // stage the transposed, zero-padded mode matrices once per (persistent) CTA:
+  // Ms[off + j * npad + i] = M[i][j]
+  if (p.mats_in_smem) {
+    for (int s = 0; s < p.nsteps; ++s) {
+      const int n = p.step[s].n, npad = p.step[s].npad;
+      const Tm* M = mats + p.step[s].mat_off;
+      Tm* dst = Ms + p.step[s].smem_off;
+      for (int l = tid; l < n * npad; l += kXformThreads) {
+        const int j = l / npad, i = l - j * npad;
+        dst[l] = (i < n) ? M[(size_t)i * n + j] : zero_v<Tm>();
+      }
+    }
+  }
+  double acc[Storer::NACC];
+#pragma unroll
+  for (int k = 0; k < Storer::NACC; ++k) acc[k] = ((Storer::MAXMASK >> k) & 1) ? -1.0e308 : 0.0;
+  const int64_t ntiles = (p.NT + TT - 1) / TT;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int64_t tube0 = tile * TT;
+  const int nt = (int)min((int64_t)TT, p.NT - tube0);
+  __syncthreads();  // previous tile's store has drained S0/S1
   ld.load(p, S0, tube0, nt, tid);
   __syncthreads();
 
-  constexpr int RB = scalar_traits<Tc>::is_complex ? 4 : 8;
   Tc* src = S0;
   Tc* dst = S1;
   for (int s = 0; s < p.nsteps; ++s) {
     const int n = p.step[s].n;
+    const int npad = p.step[s].npad;
     const int lo = (int)p.step[s].lo;
     const int hi = (int)p.step[s].hi;
-    const Tm* M = mats + p.step[s].mat_off;
-    const int nblk = (n + RB - 1) / RB;
+    const int nblk = npad / RB;
     const int work = hi * lo * nblk * TT;
+    const Tm* Mg = mats + p.step[s].mat_off;
+    const Tm* Msm = Ms + p.step[s].smem_off;
     for (int w = tid; w < work; w += kXformThreads) {
-      const int t = w % TT;
-      int r = w / TT;
+      const int t = w & (TT - 1);
+      int r = w >> p.ttshift;
       const int iblk = r % nblk;
       r /= nblk;
       const int lo_i = r % lo;
@@ -154,13 +219,21 @@ __global__ void __launch_bounds__(kXformThreads)
       Tc acc[RB];
 #pragma unroll
       for (int rr = 0; rr < RB; ++rr) acc[rr] = zero_v<Tc>();
-      for (int j = 0; j < n; ++j) {
-        const Tc v = src[(base + j * lo) * pitch + t];
+      if (p.mats_in_smem) {
+        for (int j = 0; j < n; ++j) {
+          const Tc v = src[(base + j * lo) * pitch + t];
+          const mrow<Tm, RB> mv = *reinterpret_cast<const mrow<Tm, RB>*>(Msm + j * npad + i0);
 #pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {
-          const int i = min(i0 + rr, n - 1);
-          const Tm mv = ldg_v(M + (size_t)i * n + j);
-          fma_acc(acc[rr], mv, v);
+          for (int rr = 0; rr < RB; ++rr) fma_acc(acc[rr], mv.v[rr], v);
+        }
+      } else {
+        for (int j = 0; j < n; ++j) {
+          const Tc v = src[(base + j * lo) * pitch + t];
+#pragma unroll
+          for (int rr = 0; rr < RB; ++rr) {
+            const int i = min(i0 + rr, n - 1);
+            fma_acc(acc[rr], ldg_v(Mg + (size_t)i * n + j), v);
+          }
         }
       }
 #pragma unroll
@@ -175,10 +248,8 @@ __global__ void __launch_bounds__(kXformThreads)
     dst = tmp;
   }
 
-  double acc[Storer::NACC];
-#pragma unroll
-  for (int k = 0; k < Storer::NACC; ++k) acc[k] = ((Storer::MAXMASK >> k) & 1) ? -1.0e308 : 0.0;
   st.store(p, src, tube0, nt, tid, acc);
+  }  // tiles
   if (partials) {
     __shared__ double red[Storer::NACC][kXformThreads / 32];
     const int wid = tid >> 5, lane = tid & 31;
@@ -203,31 +274,48 @@ __global__ void __launch_bounds__(kXformThreads)
   }
 }
 
-// pick tubes-per-tile; 0 => the tile does not fit in shared memory
-template <typename Tc>
-inline int choose_tt(int P, size_t* smem_out) {
-  auto smem_for = [&](int tt) { return (size_t)2 * P * (tt + 1) * sizeof(Tc); };
-  for (int tt = 32; tt >= 8; tt >>= 1)
-    if (smem_for(tt) <= 100 * 1024) {
-      *smem_out = smem_for(tt);
-      return tt;
-    }
-  for (int tt = 32; tt >= 1; tt >>= 1)
-    if (smem_for(tt) <= 200 * 1024) {
-      *smem_out = smem_for(tt);
-      return tt;
-    }
-  return 0;
+// Pick tubes-per-tile (power of two) and the matrix staging; returns 0 when
+// the tile does not fit in shared memory.  Fills p.TT / ttshift / pitch /
+// mats_in_smem and the total dynamic shared memory.
+template <typename Tc, typename Tm>
+inline int plan_tile(XformParams& p, size_t* smem_out) {
+  plan_matrices<Tc>(p);
+  const size_t mat_bytes = ((size_t)p.mat_smem_elems * sizeof(Tm) + 127) / 128 * 128;
+  p.mats_in_smem = mat_bytes <= 48 * 1024 ? 1 : 0;
+  const size_t mb = p.mats_in_smem ? mat_bytes : 0;
+  auto smem_for = [&](int tt) { return mb + (size_t)2 * p.P * (tt + 1) * sizeof(Tc); };
+  int TT = 0;
+  for (int tt = 32; tt >= 8 && !TT; tt >>= 1)
+    if (smem_for(tt) <= 100 * 1024) TT = tt;
+  for (int tt = 32; tt >= 1 && !TT; tt >>= 1)
+    if (smem_for(tt) <= 200 * 1024) TT = tt;
+  if (!TT) return 0;
+  p.TT = TT;
+  p.ttshift = 0;
+  while ((1 << p.ttshift) < TT) ++p.ttshift;
+  p.pitch = TT + 1;
+  *smem_out = smem_for(TT);
+  return TT;
+}
+
+// persistent grid: enough CTAs to fill every SM at the kernel's occupancy, capped by the tile count
+template <typename K>
+int64_t xform_grid(ltb_ctx* ctx, const XformParams& p, K kern, size_t smem) {
+  const int64_t ntiles = (p.NT + p.TT - 1) / p.TT;
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kXformThreads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return std::min<int64_t>(ntiles, (int64_t)per_sm * ctx->num_sms);
 }
 
 template <typename Tc, typename Tm, class Loader, class Storer>
 int launch_xform_tile(ltb_ctx* ctx, XformParams p, const Loader& ld, const Storer& st, const Tm* mats,
-                      double* partials, const int* skip, size_t smem) {
+                      double* partials, const int* skip, size_t smem, int64_t* grid_out = nullptr) {
   auto kern = xform_tile_kernel<Tc, Tm, Loader, Storer>;
   if (smem > 48 * 1024)
     LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t nblocks = (p.NT + p.TT - 1) / p.TT;
-  if (nblocks > 0x7fffffff) return ltb_set_error(ctx, LTB_ESHAPE, "transform: too many tubes");
+  const int64_t nblocks = xform_grid(ctx, p, kern, smem);
+  if (grid_out) *grid_out = nblocks;  // number of per-CTA partials written
   if (nblocks == 0) return LTB_OK;
   kern<<<(unsigned)nblocks, kXformThreads, smem, ctx->stream>>>(p, ld, st, mats, partials, skip);
   LTB_LAUNCH_CHECK(ctx);
