@@ -16,6 +16,8 @@
 struct ModeStep {
   int n;
   int npad;  // n rounded up to the register block (smem matrix row length)
+  int rb;    // register block (outputs per work item) for this mode
+  float inv_nblk, inv_lo;
   int64_t hi, lo;
   int64_t mat_off;   // element offset of the row-major matrix in global memory
   int smem_off;      // element offset of the transposed padded matrix in shared memory
@@ -61,9 +63,16 @@ inline void plan_matrices(XformParams& p) {
   constexpr int RB = xform_rb<Tc>();
   int off = 0;
   for (int s = 0; s < p.nsteps; ++s) {
-    p.step[s].npad = (p.step[s].n + RB - 1) / RB * RB;
-    p.step[s].smem_off = off;
-    off += p.step[s].n * p.step[s].npad;
+    ModeStep& ms = p.step[s];
+    int rb = 1;
+    while (rb < RB && rb < ms.n) rb <<= 1;  // smallest power of two >= n, capped at RB
+    ms.rb = rb;
+    ms.npad = (ms.n + rb - 1) / rb * rb;
+    ms.inv_nblk = 1.0f / (float)(ms.npad / rb);
+    ms.inv_lo = 1.0f / (float)ms.lo;
+    off = (off + RB - 1) / RB * RB;  // every matrix starts vector-aligned
+    ms.smem_off = off;
+    off += ms.n * ms.npad;
   }
   p.mat_smem_elems = off;
 }
@@ -156,6 +165,63 @@ template <typename Tm, int RB> struct alignas(sizeof(Tm) * RB >= 16 ? 16 : sizeo
   Tm v[RB];
 };
 
+// floor(a / d) for 0 <= a < 2^24 via a float reciprocal (exact after one correction)
+__device__ __forceinline__ int fdiv(int a, int d, float inv) {
+  int q = __float2int_rz((float)a * inv);
+  const int r = a - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
+}
+
+// one mode product out of shared memory: every work item produces RBM outputs
+// (rows i0 .. i0+RBM-1 of M times one fibre of the tile)
+template <typename Tc, typename Tm, int RBM>
+__device__ __forceinline__ void mode_step(const XformParams& p, const ModeStep& ms, const Tc* __restrict__ src,
+                                          Tc* __restrict__ dst, const Tm* __restrict__ Msm,
+                                          const Tm* __restrict__ Mg, int tid) {
+  const int n = ms.n, npad = ms.npad, lo = (int)ms.lo, hi = (int)ms.hi;
+  const int TT = p.TT, pitch = p.pitch;
+  const int nblk = npad / RBM;
+  const int work = hi * lo * nblk * TT;
+  for (int w = tid; w < work; w += kXformThreads) {
+    const int t = w & (TT - 1);
+    const int r0 = w >> p.ttshift;
+    const int r1 = fdiv(r0, nblk, ms.inv_nblk);
+    const int iblk = r0 - r1 * nblk;
+    const int hi_i = fdiv(r1, lo, ms.inv_lo);
+    const int lo_i = r1 - hi_i * lo;
+    const int i0 = iblk * RBM;
+    const int base = hi_i * n * lo + lo_i;
+    Tc acc[RBM];
+#pragma unroll
+    for (int rr = 0; rr < RBM; ++rr) acc[rr] = zero_v<Tc>();
+    const Tc* col = src + base * pitch + t;
+    const int jstride = lo * pitch;
+    if (p.mats_in_smem) {
+      const Tm* mrowp = Msm + i0;
+      for (int j = 0; j < n; ++j) {
+        const Tc v = col[j * jstride];
+        const mrow<Tm, RBM> mv = *reinterpret_cast<const mrow<Tm, RBM>*>(mrowp + j * npad);
+#pragma unroll
+        for (int rr = 0; rr < RBM; ++rr) fma_acc(acc[rr], mv.v[rr], v);
+      }
+    } else {
+      for (int j = 0; j < n; ++j) {
+        const Tc v = col[j * jstride];
+#pragma unroll
+        for (int rr = 0; rr < RBM; ++rr) {
+          const int i = min(i0 + rr, n - 1);
+          fma_acc(acc[rr], ldg_v(Mg + (size_t)i * n + j), v);
+        }
+      }
+    }
+    Tc* out = dst + base * pitch + t;
+#pragma unroll
+    for (int rr = 0; rr < RBM; ++rr)
+      if (i0 + rr < n) out[(i0 + rr) * jstride] = acc[rr];
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 template <typename Tc, typename Tm, class Loader, class Storer>
 __global__ void __launch_bounds__(kXformThreads)
@@ -199,48 +265,14 @@ __global__ void __launch_bounds__(kXformThreads)
   Tc* src = S0;
   Tc* dst = S1;
   for (int s = 0; s < p.nsteps; ++s) {
-    const int n = p.step[s].n;
-    const int npad = p.step[s].npad;
-    const int lo = (int)p.step[s].lo;
-    const int hi = (int)p.step[s].hi;
-    const int nblk = npad / RB;
-    const int work = hi * lo * nblk * TT;
-    const Tm* Mg = mats + p.step[s].mat_off;
-    const Tm* Msm = Ms + p.step[s].smem_off;
-    for (int w = tid; w < work; w += kXformThreads) {
-      const int t = w & (TT - 1);
-      int r = w >> p.ttshift;
-      const int iblk = r % nblk;
-      r /= nblk;
-      const int lo_i = r % lo;
-      const int hi_i = r / lo;
-      const int i0 = iblk * RB;
-      const int base = hi_i * n * lo + lo_i;
-      Tc acc[RB];
-#pragma unroll
-      for (int rr = 0; rr < RB; ++rr) acc[rr] = zero_v<Tc>();
-      if (p.mats_in_smem) {
-        for (int j = 0; j < n; ++j) {
-          const Tc v = src[(base + j * lo) * pitch + t];
-          const mrow<Tm, RB> mv = *reinterpret_cast<const mrow<Tm, RB>*>(Msm + j * npad + i0);
-#pragma unroll
-          for (int rr = 0; rr < RB; ++rr) fma_acc(acc[rr], mv.v[rr], v);
-        }
-      } else {
-        for (int j = 0; j < n; ++j) {
-          const Tc v = src[(base + j * lo) * pitch + t];
-#pragma unroll
-          for (int rr = 0; rr < RB; ++rr) {
-            const int i = min(i0 + rr, n - 1);
-            fma_acc(acc[rr], ldg_v(Mg + (size_t)i * n + j), v);
-          }
-        }
-      }
-#pragma unroll
-      for (int rr = 0; rr < RB; ++rr) {
-        const int i = i0 + rr;
-        if (i < n) dst[(base + i * lo) * pitch + t] = acc[rr];
-      }
+    const ModeStep& ms = p.step[s];
+    const Tm* Mg = mats + ms.mat_off;
+    const Tm* Msm = Ms + ms.smem_off;
+    switch (ms.rb) {
+      case 1: mode_step<Tc, Tm, 1>(p, ms, src, dst, Msm, Mg, tid); break;
+      case 2: mode_step<Tc, Tm, 2>(p, ms, src, dst, Msm, Mg, tid); break;
+      case 4: mode_step<Tc, Tm, 4>(p, ms, src, dst, Msm, Mg, tid); break;
+      default: mode_step<Tc, Tm, RB>(p, ms, src, dst, Msm, Mg, tid); break;
     }
     __syncthreads();
     Tc* tmp = src;
