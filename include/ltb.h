@@ -128,6 +128,16 @@ int ltb_slice_gemm(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,
                    int op_b, const void* d_b, int64_t ldb, int64_t stride_b,
                    void* d_c, int64_t ldc, int64_t stride_c);
 
+/* The fp32 tensor-core engine underneath K1/K1'/K2 (tcgen05 kind::tf32 with the
+ * 3xTF32 split when split == 3, plain TF32 when split == 1), exposed for the
+ * kernel tests: C[b] (m x n, ldc) = A[b] * B[b], A stored m x k (a_mn = 0) or
+ * k x m (a_mn = 1), B stored n x k (b_mn = 0) or k x n (b_mn = 1).  Leading
+ * dimensions and batch strides must be multiples of 4 elements.  Returns
+ * LTB_EUNSUPPORTED when the shape / alignment cannot use the tensor cores. */
+int ltb_tc_gemm(ltb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t k, int a_mn, const void* d_a,
+                int64_t lda, int64_t sa, int b_mn, const void* d_b, int64_t ldb, int64_t sb, void* d_c,
+                int64_t ldc, int64_t sc, int split);
+
 /* ---------------------------------------------------------------- K3
  * Batched one-sided Jacobi on `batch` row-major m x n slices (contiguous).
  *   ltb_slice_svt: svt's slice step (linalg.py:178-180): out = U (S - tau)_+ V^H.

@@ -1,0 +1,391 @@
+// 5th-generation tensor-core GEMM (tcgen05 + TMA + TMEM) for FP32 data with
+// the 3xTF32 split:  A*B ~= Ahi*Bhi + Ahi*Blo + Alo*Bhi,  hi = x with the low
+// 13 mantissa bits cleared (exactly representable in TF32), lo = x - hi.
+// Plain TF32 misses the 1e-4 parity bar on the *_L product (SURVEY.md §7
+// "hard part 2": 6.3e-4 measured); the split restores ~FP32 accuracy.
+//
+// C[b] (M x N, row-major, ldc) = A[b] (M x K) * B[b] (K x N), where each
+// operand is either K-major (A: M rows of K contiguous; B: N rows of K
+// contiguous) or MN-major (A stored K x M; B stored K x N).  This one kernel
+// serves the whole f32 *_L product (linalg.py:34-43):
+//   forward transform  tube->slice : C(P x NT) = Kron(P x P) * X^T         (A K-major, B K-major)
+//   slice GEMM         (K2)        : C_q = Ahat_q * Bhat_q                  (A K-major, B MN-major)
+//   inverse transform  slice->tube : C(NT x P) = H^T(NT x P) * Kinv^T       (A MN-major, B K-major)
+// with the transform applied as one dense Kronecker matrix (P <= 1024).
+//
+// Structure (one 128 x BN output tile per CTA, 8 warps):
+//   warp 0      TMA producer (one elected lane), 3-stage smem ring, 128B swizzle
+//   warp 1      TMEM allocator + MMA issuer (one lane): 3 tcgen05.mma kind::tf32
+//               per K=8 step, accumulator in TMEM, tcgen05.commit frees a stage
+//   warps 2-3   split converters: in place hi, separate lo buffer, then
+//               fence.proxy.async so the tensor core sees the generic writes
+//   warps 4-7   epilogue: tcgen05.ld 32x32b.x32 -> registers -> global
+#include <cuda.h>
+
+#include <cstring>
+
+#include "ltb_dispatch.cuh"
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int kStages = 3;
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, 128-byte swizzle (sm100 version bits = 1)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: kind::tf32, D f32, A/B tf32, M = 128, N = BN
+__host__ __device__ constexpr uint32_t idesc_tf32(int bn, bool a_mn, bool b_mn) {
+  return (1u << 4)                       // D format f32
+         | (2u << 7)                     // A format tf32
+         | (2u << 10)                    // B format tf32
+         | ((a_mn ? 1u : 0u) << 15)      // A major
+         | ((b_mn ? 1u : 0u) << 16)      // B major
+         | ((uint32_t)(bn >> 3) << 17)   // N >> 3
+         | ((uint32_t)(kBM >> 4) << 24);  // M >> 4
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%"
+      "20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ kernel
+template <int BN, bool A_MN, bool B_MN, int SPLIT>
+struct TcCfg {
+  static constexpr int A_BYTES = kBM * kBK * 4;  // 16 KB
+  static constexpr int B_BYTES = BN * kBK * 4;
+  static constexpr int STAGE_BYTES = (SPLIT == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
+  static constexpr int SMEM = kStages * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
+};
+
+template <int BN, bool A_MN, bool B_MN, int SPLIT>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K) {
+  using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // stage s: [A_hi | B_hi | A_lo | B_lo]
+  auto a_hi = [&](int s) { return base + s * Cfg::STAGE_BYTES; };
+  auto b_hi = [&](int s) { return base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES; };
+  auto a_lo = [&](int s) { return base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES + Cfg::B_BYTES; };
+  auto b_lo = [&](int s) { return base + s * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES + Cfg::B_BYTES; };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStages * Cfg::STAGE_BYTES);
+  uint64_t* full = bars;                 // TMA landed
+  uint64_t* conv = bars + kStages;       // split done
+  uint64_t* empty = bars + 2 * kStages;  // MMA consumed
+  uint64_t* accf = bars + 3 * kStages;   // accumulator ready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int batch = blockIdx.z;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
+  const int ktiles = (K + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], SPLIT == 3 ? 64 : 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // TMEM: BN fp32 columns x 128 lanes for the accumulator
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(BN < 32 ? 32 : BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % kStages;
+        mbar_wait(&empty[s], ((kt / kStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+        const int k0 = kt * kBK;
+        if (!A_MN) {
+          tma_load_3d(a_hi(s), &tmA, &full[s], k0, m0, batch);
+        } else {
+          for (int c = 0; c < kBM / 32; ++c) tma_load_3d(a_hi(s) + c * 4096, &tmA, &full[s], m0 + 32 * c, k0, batch);
+        }
+        if (!B_MN) {
+          tma_load_3d(b_hi(s), &tmB, &full[s], k0, n0, batch);
+        } else {
+          for (int c = 0; c < BN / 32; ++c) tma_load_3d(b_hi(s) + c * 4096, &tmB, &full[s], n0 + 32 * c, k0, batch);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = idesc_tf32(BN, A_MN, B_MN);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % kStages;
+      mbar_wait(SPLIT == 3 ? &conv[s] : &full[s], (kt / kStages) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < kBK / 8; ++kk) {
+          // K-major: a K=8 step is 32 bytes along the swizzled row; MN-major: one 8-row (1 KB) atom
+          const uint32_t koff = (A_MN ? 1024u : 32u) * kk;
+          const uint32_t kofb = (B_MN ? 1024u : 32u) * kk;
+          const uint32_t lboA = A_MN ? 4096u : 16u, lboB = B_MN ? 4096u : 16u;
+          const uint64_t dah = umma_desc(smem_u32(a_hi(s)) + koff, lboA, 1024u);
+          const uint64_t dbh = umma_desc(smem_u32(b_hi(s)) + kofb, lboB, 1024u);
+          const uint32_t acc = (kt > 0 || kk > 0) ? 1u : 0u;
+          umma_tf32(tmem, dah, dbh, idesc, acc);
+          if constexpr (SPLIT == 3) {
+            const uint64_t dal = umma_desc(smem_u32(a_lo(s)) + koff, lboA, 1024u);
+            const uint64_t dbl = umma_desc(smem_u32(b_lo(s)) + kofb, lboB, 1024u);
+            umma_tf32(tmem, dah, dbl, idesc, 1u);
+            umma_tf32(tmem, dal, dbh, idesc, 1u);
+          }
+        }
+        umma_commit(&empty[s]);  // stage reusable once these MMAs complete
+        if (kt == ktiles - 1) umma_commit(accf);
+      }
+      __syncwarp();
+    }
+  } else if (warp < 4) {
+    // ---------------------------------------------------------------- 3xTF32 split
+    if constexpr (SPLIT == 3) {
+      const int ct = threadIdx.x - 64;  // 0..63
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % kStages;
+        mbar_wait(&full[s], (kt / kStages) & 1);
+        float4* ah = reinterpret_cast<float4*>(a_hi(s));
+        float4* al = reinterpret_cast<float4*>(a_lo(s));
+        for (int i = ct; i < Cfg::A_BYTES / 16; i += 64) {
+          float4 x = ah[i], h, l;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          l.x = x.x - h.x;
+          l.y = x.y - h.y;
+          l.z = x.z - h.z;
+          l.w = x.w - h.w;
+          ah[i] = h;
+          al[i] = l;
+        }
+        float4* bh = reinterpret_cast<float4*>(b_hi(s));
+        float4* bl = reinterpret_cast<float4*>(b_lo(s));
+        for (int i = ct; i < Cfg::B_BYTES / 16; i += 64) {
+          float4 x = bh[i], h, l;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+          l.x = x.x - h.x;
+          l.y = x.y - h.y;
+          l.z = x.z - h.z;
+          l.w = x.w - h.w;
+          bh[i] = h;
+          bl[i] = l;
+        }
+        fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+        mbar_arrive(&conv[s]);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp - 4;  // TMEM lane quarter of this warp
+    mbar_wait(accf, 0);
+    tc_fence_after();
+    const int row = m0 + 32 * q + lane;
+    float* crow = C + (int64_t)batch * sc + (int64_t)row * ldc;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, r);
+      if (row < M) {
+        const int nc = min(32, N - (n0 + c0));
+        if (nc == 32 && ((ldc & 3) == 0) && (((n0 + c0) & 3) == 0)) {
+          float4* dst = reinterpret_cast<float4*>(crow + n0 + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nc) crow[n0 + c0 + j] = __uint_as_float(r[j]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
+  }
+}
+
+// ------------------------------------------------------------------ host: tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+// 3D fp32 map: dims {inner, rows, batch}, box {32, box_rows, 1}, 128B swizzle, zero OOB fill
+bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t rows, int64_t batch, int64_t ld,
+              int64_t bstride, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 4) % 16 || (bstride * 4) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(bstride * 4)};
+  cuuint32_t box[3] = {32u, (cuuint32_t)box_rows, 1u};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN, int SPLIT>
+int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t ldc, int64_t sc,
+              int64_t batch, int M, int N, int K) {
+  using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
+  auto kern = tc_gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT>;
+  LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + kBM - 1) / kBM), (unsigned)batch);
+  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, C, ldc, sc, M, N, K);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
+
+}  // namespace
+
+// C[b] = op(A[b]) op(B[b]) in fp32 on tcgen05 (3xTF32 when split == 3).
+// a_mn: A stored K x M (else M x K); b_mn: B stored K x N (else N x K).
+// Returns LTB_EUNSUPPORTED (no error text) when the shape / alignment / driver
+// cannot use the tensor-core path; the caller then falls back.
+int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K, bool a_mn, const float* A,
+                    int64_t lda, int64_t sa, bool b_mn, const float* B, int64_t ldb, int64_t sb, float* C,
+                    int64_t ldc, int64_t sc, int split) {
+  if (batch < 1 || M < 1 || N < 1 || K < 1 || batch > 65535) return LTB_EUNSUPPORTED;
+  if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return LTB_EUNSUPPORTED;
+  if ((M + kBM - 1) / kBM > 65535) return LTB_EUNSUPPORTED;
+  CUtensorMap ma, mb;
+  // A: K-major -> dims {K, M}, box {32, 128};  MN-major -> dims {M, K}, box {32 (M), 32 (K)}
+  const bool okA = a_mn ? make_map(&ma, A, M, K, batch, lda, sa, kBK) : make_map(&ma, A, K, M, batch, lda, sa, kBM);
+  const int BN = 128;
+  const bool okB = b_mn ? make_map(&mb, B, N, K, batch, ldb, sb, kBK) : make_map(&mb, B, K, N, batch, ldb, sb, BN);
+  if (!okA || !okB) return LTB_EUNSUPPORTED;
+  const int m = (int)M, n = (int)N, k = (int)K;
+  if (split == 3) {
+    if (!a_mn && !b_mn) return launch_tc<128, false, false, 3>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+    if (!a_mn && b_mn) return launch_tc<128, false, true, 3>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+    if (a_mn && !b_mn) return launch_tc<128, true, false, 3>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+    return launch_tc<128, true, true, 3>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+  }
+  if (!a_mn && !b_mn) return launch_tc<128, false, false, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+  if (!a_mn && b_mn) return launch_tc<128, false, true, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+  if (a_mn && !b_mn) return launch_tc<128, true, false, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+  return launch_tc<128, true, true, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+}
+
+// test hook: exported C entry for the kernel-level tests (fp32 only)
+extern "C" int ltb_tc_gemm(ltb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t k, int a_mn, const void* d_a,
+                           int64_t lda, int64_t sa, int b_mn, const void* d_b, int64_t ldb, int64_t sb, void* d_c,
+                           int64_t ldc, int64_t sc, int split) {
+  int st = ltb_tc_gemm_f32(ctx, batch, m, n, k, a_mn != 0, (const float*)d_a, lda, sa, b_mn != 0, (const float*)d_b,
+                           ldb, sb, (float*)d_c, ldc, sc, split);
+  if (st == LTB_EUNSUPPORTED) return ltb_set_error(ctx, LTB_EUNSUPPORTED, "tc_gemm: shape/alignment unsupported");
+  return st;
+}

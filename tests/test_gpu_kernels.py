@@ -121,3 +121,29 @@ def test_reductions(dt):
     nat.check(nat.lib().ltb_reduce_dot(nat.context(), dx.code, dx.size, dx.ptr, dy.ptr, out))
     ref = np.vdot(x.astype(np.complex128), y.astype(np.complex128))
     assert abs(complex(out[0], out[1]) - ref) / abs(ref) < 1e-5
+
+
+@pytest.mark.parametrize("split", [3, 1])
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("mnk", [(128, 128, 32), (256, 256, 128), (96, 200, 96), (300, 72, 36)])
+def test_tc_gemm_tf32(split, a_mn, b_mn, mnk):
+    """tcgen05 kind::tf32 engine (3xTF32 split) vs float64 numpy."""
+    rng = np.random.default_rng(11)
+    m, n, k = mnk
+    batch = 2
+    a = rng.standard_normal((batch, m, k)).astype(np.float32)
+    b = rng.standard_normal((batch, k, n)).astype(np.float32)
+    a_st = np.ascontiguousarray(np.swapaxes(a, 1, 2) if a_mn else a)  # a_mn: stored k x m
+    b_st = np.ascontiguousarray(b if b_mn else np.swapaxes(b, 1, 2))  # b_mn: stored k x n, else n x k
+    da, db = nat.DeviceArray.from_numpy(a_st), nat.DeviceArray.from_numpy(b_st)
+    dc = nat.DeviceArray((batch, m, n), np.float32)
+    lda, ldb = a_st.shape[2], b_st.shape[2]
+    st = nat.lib().ltb_tc_gemm(nat.context(), batch, m, n, k, a_mn, da.ptr, lda, a_st.shape[1] * lda, b_mn, db.ptr,
+                               ldb, b_st.shape[1] * ldb, dc.ptr, n, m * n, split)
+    if st == 3:
+        pytest.skip("tensor-core path unsupported for this alignment")
+    nat.check(st)
+    ref = np.matmul(a.astype(np.float64), b.astype(np.float64))
+    err = np.linalg.norm(dc.numpy() - ref) / np.linalg.norm(ref)
+    assert err < (2e-6 if split == 3 else 2e-3), err
