@@ -148,7 +148,18 @@ struct ltb_spec {
   void* d_mats[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   int64_t mat_off[16] = {0};
   int64_t mat_total = 0;
+  // real specs with P <= kKronMax: the dense Kronecker matrix of L and of L^{-1}
+  // (C-order trailing index), fp32, for the tensor-core transform path
+  float* d_kron[2] = {nullptr, nullptr};
 };
+
+constexpr int64_t kKronMax = 512;
+
+// fp32 tensor-core GEMM (ltb_tc_gemm.cu); LTB_EUNSUPPORTED when the shape /
+// alignment cannot take the tcgen05 path
+int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K, bool a_mn, const float* A,
+                    int64_t lda, int64_t sa, bool b_mn, const float* B, int64_t ldb, int64_t sb, float* C,
+                    int64_t ldc, int64_t sc, int split);
 
 // ------------------------------------------------------------------ errors
 int ltb_set_error(ltb_ctx* ctx, int code, const char* fmt, ...);

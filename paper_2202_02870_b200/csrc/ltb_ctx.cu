@@ -203,6 +203,52 @@ int ltb_spec_create(ltb_ctx* ctx, int ntrail, const int64_t* trail_dims, int nmo
     s->d_mats[0][dir] = d32;
     s->d_mats[1][dir] = d64;
   }
+  // dense Kronecker matrices K[q][q'] = prod_a F_a[k_a][k'_a] (F_a = M_a on
+  // transformed axes, I elsewhere; C-order q) for the tensor-core path
+  if (!is_complex && s->P <= kKronMax) {
+    const int64_t P = s->P;
+    std::vector<int> axis_mode(ntrail, -1);
+    for (int k = 0; k < nmodes; ++k) axis_mode[axes[k]] = k;
+    std::vector<float> kron((size_t)P * P);
+    std::vector<int> qi(ntrail), qj(ntrail);
+    for (int dir = 0; dir < 2; ++dir) {
+      const double* src = dir == 0 ? h_fwd : h_inv;
+      for (int64_t i = 0; i < P; ++i) {
+        int64_t r = i;
+        for (int a = ntrail - 1; a >= 0; --a) {
+          qi[a] = (int)(r % trail_dims[a]);
+          r /= trail_dims[a];
+        }
+        for (int64_t j = 0; j < P; ++j) {
+          int64_t c = j;
+          double v = 1.0;
+          for (int a = ntrail - 1; a >= 0 && v != 0.0; --a) {
+            qj[a] = (int)(c % trail_dims[a]);
+            c /= trail_dims[a];
+            const int k = axis_mode[a];
+            if (k < 0) {
+              v = (qi[a] == qj[a]) ? v : 0.0;
+            } else {
+              const int n = s->sizes[k];
+              v *= src[s->mat_off[k] + (int64_t)qi[a] * n + qj[a]];
+            }
+          }
+          kron[(size_t)i * P + j] = (float)v;
+        }
+      }
+      if (cudaMalloc(&s->d_kron[dir], sizeof(float) * P * P) != cudaSuccess) {
+        cudaGetLastError();
+        s->d_kron[dir] = nullptr;
+        break;
+      }
+      cudaMemcpy(s->d_kron[dir], kron.data(), sizeof(float) * P * P, cudaMemcpyHostToDevice);
+    }
+    if (!s->d_kron[0] || !s->d_kron[1]) {
+      for (int d = 0; d < 2; ++d)
+        if (s->d_kron[d]) cudaFree(s->d_kron[d]);
+      s->d_kron[0] = s->d_kron[1] = nullptr;
+    }
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     delete s;
@@ -217,6 +263,8 @@ void ltb_spec_destroy(ltb_spec* s) {
   for (int p = 0; p < 2; ++p)
     for (int d = 0; d < 2; ++d)
       if (s->d_mats[p][d]) cudaFree(s->d_mats[p][d]);
+  for (int d = 0; d < 2; ++d)
+    if (s->d_kron[d]) cudaFree(s->d_kron[d]);
   delete s;
 }
 

@@ -75,14 +75,18 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// UMMA shared-memory descriptor, 128-byte swizzle (sm100 version bits = 1)
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// UMMA shared-memory descriptor (sm100 version bits = 1).  K-major operands use
+// SWIZZLE_128B (layout 2, 8-row 1 KB atoms); 32-bit MN-major operands use
+// SWIZZLE_128B_BASE32B (layout 1, 4 K-row 512 B atoms), which is what the TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B mode writes.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              bool mn32 = false) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  d |= (uint64_t)1 << 46;                     // descriptor version (Blackwell)
+  d |= (uint64_t)(mn32 ? 1 : 2) << 61;        // SWIZZLE_128B_BASE32B : SWIZZLE_128B
   return d;
 }
 
@@ -136,7 +140,8 @@ struct TcCfg {
 template <int BN, bool A_MN, bool B_MN, int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K) {
+                        float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K, uint32_t mn_lbo,
+                        uint32_t mn_sbo) {
   using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -209,14 +214,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           // K-major: a K=8 step is 32 bytes along the swizzled row; MN-major: one 8-row (1 KB) atom
           const uint32_t koff = (A_MN ? 1024u : 32u) * kk;
           const uint32_t kofb = (B_MN ? 1024u : 32u) * kk;
-          const uint32_t lboA = A_MN ? 4096u : 16u, lboB = B_MN ? 4096u : 16u;
-          const uint64_t dah = umma_desc(smem_u32(a_hi(s)) + koff, lboA, 1024u);
-          const uint64_t dbh = umma_desc(smem_u32(b_hi(s)) + kofb, lboB, 1024u);
+          const uint32_t lboA = A_MN ? mn_lbo : 16u, lboB = B_MN ? mn_lbo : 16u;
+          const uint32_t sboA = A_MN ? mn_sbo : 1024u, sboB = B_MN ? mn_sbo : 1024u;
+          const uint64_t dah = umma_desc(smem_u32(a_hi(s)) + koff, lboA, sboA, A_MN);
+          const uint64_t dbh = umma_desc(smem_u32(b_hi(s)) + kofb, lboB, sboB, B_MN);
           const uint32_t acc = (kt > 0 || kk > 0) ? 1u : 0u;
           umma_tf32(tmem, dah, dbh, idesc, acc);
           if constexpr (SPLIT == 3) {
-            const uint64_t dal = umma_desc(smem_u32(a_lo(s)) + koff, lboA, 1024u);
-            const uint64_t dbl = umma_desc(smem_u32(b_lo(s)) + kofb, lboB, 1024u);
+            const uint64_t dal = umma_desc(smem_u32(a_lo(s)) + koff, lboA, sboA, A_MN);
+            const uint64_t dbl = umma_desc(smem_u32(b_lo(s)) + kofb, lboB, sboB, B_MN);
             umma_tf32(tmem, dah, dbl, idesc, 1u);
             umma_tf32(tmem, dal, dbh, idesc, 1u);
           }
@@ -303,6 +309,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------ host: tensor maps
+// MN-major 128B-swizzle descriptor strides (bytes): LBO = MN-chunk stride, SBO = 8-row K-group stride
+uint32_t g_mn_lbo = 4096, g_mn_sbo = 512;
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -324,7 +333,7 @@ EncodeTiledFn get_encode() {
 
 // 3D fp32 map: dims {inner, rows, batch}, box {32, box_rows, 1}, 128B swizzle, zero OOB fill
 bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t rows, int64_t batch, int64_t ld,
-              int64_t bstride, int box_rows) {
+              int64_t bstride, int box_rows, bool mn32 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 4) % 16 || (bstride * 4) % 16) return false;
@@ -333,7 +342,8 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t rows, i
   cuuint32_t box[3] = {32u, (cuuint32_t)box_rows, 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, mn32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -341,10 +351,11 @@ template <int BN, bool A_MN, bool B_MN, int SPLIT>
 int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t ldc, int64_t sc,
               int64_t batch, int M, int N, int K) {
   using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
+  const uint32_t mn_lbo = g_mn_lbo, mn_sbo = g_mn_sbo;
   auto kern = tc_gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT>;
   LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + kBM - 1) / kBM), (unsigned)batch);
-  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, C, ldc, sc, M, N, K);
+  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, C, ldc, sc, M, N, K, mn_lbo, mn_sbo);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -363,9 +374,9 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
   if ((M + kBM - 1) / kBM > 65535) return LTB_EUNSUPPORTED;
   CUtensorMap ma, mb;
   // A: K-major -> dims {K, M}, box {32, 128};  MN-major -> dims {M, K}, box {32 (M), 32 (K)}
-  const bool okA = a_mn ? make_map(&ma, A, M, K, batch, lda, sa, kBK) : make_map(&ma, A, K, M, batch, lda, sa, kBM);
+  const bool okA = a_mn ? make_map(&ma, A, M, K, batch, lda, sa, kBK, true) : make_map(&ma, A, K, M, batch, lda, sa, kBM);
   const int BN = 128;
-  const bool okB = b_mn ? make_map(&mb, B, N, K, batch, ldb, sb, kBK) : make_map(&mb, B, K, N, batch, ldb, sb, BN);
+  const bool okB = b_mn ? make_map(&mb, B, N, K, batch, ldb, sb, kBK, true) : make_map(&mb, B, K, N, batch, ldb, sb, BN);
   if (!okA || !okB) return LTB_EUNSUPPORTED;
   const int m = (int)M, n = (int)N, k = (int)K;
   if (split == 3) {
@@ -378,6 +389,11 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
   if (!a_mn && b_mn) return launch_tc<128, false, true, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
   if (a_mn && !b_mn) return launch_tc<128, true, false, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
   return launch_tc<128, true, true, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+}
+
+extern "C" void ltb_tc_debug_set_mn_strides(uint32_t lbo, uint32_t sbo) {
+  g_mn_lbo = lbo;
+  g_mn_sbo = sbo;
 }
 
 // test hook: exported C entry for the kernel-level tests (fp32 only)

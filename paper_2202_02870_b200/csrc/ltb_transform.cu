@@ -226,6 +226,27 @@ int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int i
     if (d_sumsq) LTB_CUDA_TRY(ctx, cudaMemsetAsync(d_sumsq, 0, 2 * sizeof(double), ctx->stream));
     return LTB_OK;
   }
+  // fp32 real specs: the transform as one dense Kronecker GEMM on the tensor
+  // cores (tcgen05 kind::tf32, 3xTF32 split), with the tube<->slice layout
+  // change folded into the operand / output orientation
+  if (!dbl && !ic && !oc && !cm && spec->d_kron[0] && spec->nmodes > 0 &&
+      !(layout_in == LTB_SLICE_MAJOR && layout_out == LTB_SLICE_MAJOR)) {
+    const int64_t P = spec->P, NT = ntubes;
+    const float* K = spec->d_kron[inverse ? 1 : 0];
+    const float* X = (const float*)d_in;
+    float* Y = (float*)d_out;
+    int st;
+    if (layout_in == LTB_TUBE_MAJOR && layout_out == LTB_SLICE_MAJOR)  // Y(P x NT) = K * X^T
+      st = ltb_tc_gemm_f32(ctx, 1, P, NT, P, false, K, P, 0, false, X, P, 0, Y, NT, 0, 3);
+    else if (layout_in == LTB_SLICE_MAJOR)  // Y(NT x P) = X^T(NT x P) * K^T, X stored P x NT
+      st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, true, X, NT, 0, false, K, P, 0, Y, P, 0, 3);
+    else  // tube -> tube: Y(NT x P) = X * K^T
+      st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, false, X, P, 0, false, K, P, 0, Y, P, 0, 3);
+    if (st != LTB_EUNSUPPORTED) {
+      if (st == LTB_OK && d_sumsq) LTB_CUDA_TRY(ctx, cudaMemsetAsync(d_sumsq, 0, 2 * sizeof(double), ctx->stream));
+      return st;
+    }
+  }
   if (dbl) return dispatch_io<double>(ctx, ic, oc, cm, p, d_in, layout_in, d_out, layout_out, mats, d_sumsq);
   return dispatch_io<float>(ctx, ic, oc, cm, p, d_in, layout_in, d_out, layout_out, mats, d_sumsq);
 }
