@@ -22,6 +22,7 @@
 //   warps 4-7   epilogue: tcgen05.ld 32x32b.x32 -> registers -> global
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "ltb_dispatch.cuh"
@@ -135,13 +136,14 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * kBK * 4;
   static constexpr int STAGE_BYTES = (SPLIT == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
   static constexpr int SMEM = kStages * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
+  static_assert(2 * BN <= 512, "two accumulators must fit in TMEM");
 };
 
 template <int BN, bool A_MN, bool B_MN, int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K, uint32_t mn_lbo,
-                        uint32_t mn_sbo) {
+                        float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K, int batches,
+                        uint32_t mn_lbo, uint32_t mn_sbo) {
   using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -151,16 +153,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto a_lo = [&](int s) { return base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES + Cfg::B_BYTES; };
   auto b_lo = [&](int s) { return base + s * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES + Cfg::B_BYTES; };
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStages * Cfg::STAGE_BYTES);
-  uint64_t* full = bars;                 // TMA landed
-  uint64_t* conv = bars + kStages;       // split done
-  uint64_t* empty = bars + 2 * kStages;  // MMA consumed
-  uint64_t* accf = bars + 3 * kStages;   // accumulator ready
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 1);
+  uint64_t* full = bars;                  // TMA landed
+  uint64_t* conv = bars + kStages;        // split done
+  uint64_t* empty = bars + 2 * kStages;   // MMA consumed the stage
+  uint64_t* accf = bars + 3 * kStages;    // [2] accumulator ready
+  uint64_t* acce = bars + 3 * kStages + 2;  // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int batch = blockIdx.z;
-  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
   const int ktiles = (K + kBK - 1) / kBK;
+  const int num_n = (N + BN - 1) / BN, num_m = (M + kBM - 1) / kBM;
+  const int total = batches * num_m * num_n;
+  auto decode = [&](int t, int& b, int& m0, int& n0) {
+    const int nb = t % num_n;
+    const int r = t / num_n;
+    m0 = (r % num_m) * kBM;
+    b = r / num_m;
+    n0 = nb * BN;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -168,12 +178,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&conv[s], SPLIT == 3 ? 64 : 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accf, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&accf[a], 1);
+      mbar_init(&acce[a], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // TMEM: BN fp32 columns x 128 lanes for the accumulator
+  if (warp == 1) {  // TMEM: two BN-column fp32 accumulators (128 lanes)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(BN < 32 ? 32 : BN));
+                 "n"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -184,127 +197,154 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
-      for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % kStages;
-        mbar_wait(&empty[s], ((kt / kStages) & 1) ^ 1);
-        mbar_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
-        const int k0 = kt * kBK;
-        if (!A_MN) {
-          tma_load_3d(a_hi(s), &tmA, &full[s], k0, m0, batch);
-        } else {
-          for (int c = 0; c < kBM / 32; ++c) tma_load_3d(a_hi(s) + c * 4096, &tmA, &full[s], m0 + 32 * c, k0, batch);
-        }
-        if (!B_MN) {
-          tma_load_3d(b_hi(s), &tmB, &full[s], k0, n0, batch);
-        } else {
-          for (int c = 0; c < BN / 32; ++c) tma_load_3d(b_hi(s) + c * 4096, &tmB, &full[s], n0 + 32 * c, k0, batch);
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int b, m0, n0;
+        decode(t, b, m0, n0);
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          mbar_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+          const int k0 = kt * kBK;
+          if (!A_MN) {
+            tma_load_3d(a_hi(s), &tmA, &full[s], k0, m0, b);
+          } else {
+            for (int c = 0; c < kBM / 32; ++c) tma_load_3d(a_hi(s) + c * 4096, &tmA, &full[s], m0 + 32 * c, k0, b);
+          }
+          if (!B_MN) {
+            tma_load_3d(b_hi(s), &tmB, &full[s], k0, n0, b);
+          } else {
+            for (int c = 0; c < BN / 32; ++c) tma_load_3d(b_hi(s) + c * 4096, &tmB, &full[s], n0 + 32 * c, k0, b);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_tf32(BN, A_MN, B_MN);
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % kStages;
-      mbar_wait(SPLIT == 3 ? &conv[s] : &full[s], (kt / kStages) & 1);
+    const uint32_t lboA = A_MN ? mn_lbo : 16u, lboB = B_MN ? mn_lbo : 16u;
+    const uint32_t sboA = A_MN ? mn_sbo : 1024u, sboB = B_MN ? mn_sbo : 1024u;
+    int it = 0, j = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      const int a = j & 1;
+      mbar_wait(&acce[a], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
       tc_fence_after();
-      if (lane == 0) {
+      const uint32_t dacc = tmem + (uint32_t)(a * BN);
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int s = it % kStages;
+        mbar_wait(SPLIT == 3 ? &conv[s] : &full[s], (it / kStages) & 1);
+        tc_fence_after();
+        if (lane == 0) {
 #pragma unroll
-        for (int kk = 0; kk < kBK / 8; ++kk) {
-          // K-major: a K=8 step is 32 bytes along the swizzled row; MN-major: one 8-row (1 KB) atom
-          const uint32_t koff = (A_MN ? 1024u : 32u) * kk;
-          const uint32_t kofb = (B_MN ? 1024u : 32u) * kk;
-          const uint32_t lboA = A_MN ? mn_lbo : 16u, lboB = B_MN ? mn_lbo : 16u;
-          const uint32_t sboA = A_MN ? mn_sbo : 1024u, sboB = B_MN ? mn_sbo : 1024u;
-          const uint64_t dah = umma_desc(smem_u32(a_hi(s)) + koff, lboA, sboA, A_MN);
-          const uint64_t dbh = umma_desc(smem_u32(b_hi(s)) + kofb, lboB, sboB, B_MN);
-          const uint32_t acc = (kt > 0 || kk > 0) ? 1u : 0u;
-          umma_tf32(tmem, dah, dbh, idesc, acc);
-          if constexpr (SPLIT == 3) {
-            const uint64_t dal = umma_desc(smem_u32(a_lo(s)) + koff, lboA, sboA, A_MN);
-            const uint64_t dbl = umma_desc(smem_u32(b_lo(s)) + kofb, lboB, sboB, B_MN);
-            umma_tf32(tmem, dah, dbl, idesc, 1u);
-            umma_tf32(tmem, dal, dbh, idesc, 1u);
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            // K-major: a K=8 step is 32 bytes along the swizzled row; MN-major: eight 128-byte K rows
+            const uint32_t koff = (A_MN ? 1024u : 32u) * kk;
+            const uint32_t kofb = (B_MN ? 1024u : 32u) * kk;
+            const uint64_t dah = umma_desc(smem_u32(a_hi(s)) + koff, lboA, sboA, A_MN);
+            const uint64_t dbh = umma_desc(smem_u32(b_hi(s)) + kofb, lboB, sboB, B_MN);
+            const uint32_t accum = (kt > 0 || kk > 0) ? 1u : 0u;
+            umma_tf32(dacc, dah, dbh, idesc, accum);
+            if constexpr (SPLIT == 3) {
+              const uint64_t dal = umma_desc(smem_u32(a_lo(s)) + koff, lboA, sboA, A_MN);
+              const uint64_t dbl = umma_desc(smem_u32(b_lo(s)) + kofb, lboB, sboB, B_MN);
+              umma_tf32(dacc, dah, dbl, idesc, 1u);
+              umma_tf32(dacc, dal, dbh, idesc, 1u);
+            }
           }
+          umma_commit(&empty[s]);  // stage reusable once these MMAs complete
+          if (kt == ktiles - 1) umma_commit(&accf[a]);
         }
-        umma_commit(&empty[s]);  // stage reusable once these MMAs complete
-        if (kt == ktiles - 1) umma_commit(accf);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else if (warp < 4) {
     // ---------------------------------------------------------------- 3xTF32 split
     if constexpr (SPLIT == 3) {
       const int ct = threadIdx.x - 64;  // 0..63
-      for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % kStages;
-        mbar_wait(&full[s], (kt / kStages) & 1);
-        float4* ah = reinterpret_cast<float4*>(a_hi(s));
-        float4* al = reinterpret_cast<float4*>(a_lo(s));
-        for (int i = ct; i < Cfg::A_BYTES / 16; i += 64) {
-          float4 x = ah[i], h, l;
-          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-          l.x = x.x - h.x;
-          l.y = x.y - h.y;
-          l.z = x.z - h.z;
-          l.w = x.w - h.w;
-          ah[i] = h;
-          al[i] = l;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          float4* ah = reinterpret_cast<float4*>(a_hi(s));
+          float4* al = reinterpret_cast<float4*>(a_lo(s));
+#pragma unroll 4
+          for (int i = ct; i < Cfg::A_BYTES / 16; i += 64) {
+            const float4 x = ah[i];
+            float4 h, l;
+            h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+            h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+            h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+            h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+            l.x = x.x - h.x;
+            l.y = x.y - h.y;
+            l.z = x.z - h.z;
+            l.w = x.w - h.w;
+            ah[i] = h;
+            al[i] = l;
+          }
+          float4* bh = reinterpret_cast<float4*>(b_hi(s));
+          float4* bl = reinterpret_cast<float4*>(b_lo(s));
+#pragma unroll 4
+          for (int i = ct; i < Cfg::B_BYTES / 16; i += 64) {
+            const float4 x = bh[i];
+            float4 h, l;
+            h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+            h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+            h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+            h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+            l.x = x.x - h.x;
+            l.y = x.y - h.y;
+            l.z = x.z - h.z;
+            l.w = x.w - h.w;
+            bh[i] = h;
+            bl[i] = l;
+          }
+          fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+          mbar_arrive(&conv[s]);
         }
-        float4* bh = reinterpret_cast<float4*>(b_hi(s));
-        float4* bl = reinterpret_cast<float4*>(b_lo(s));
-        for (int i = ct; i < Cfg::B_BYTES / 16; i += 64) {
-          float4 x = bh[i], h, l;
-          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-          l.x = x.x - h.x;
-          l.y = x.y - h.y;
-          l.z = x.z - h.z;
-          l.w = x.w - h.w;
-          bh[i] = h;
-          bl[i] = l;
-        }
-        fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
-        mbar_arrive(&conv[s]);
       }
     }
   } else {
     // ---------------------------------------------------------------- epilogue
     const int q = warp - 4;  // TMEM lane quarter of this warp
-    mbar_wait(accf, 0);
-    tc_fence_after();
-    const int row = m0 + 32 * q + lane;
-    float* crow = C + (int64_t)batch * sc + (int64_t)row * ldc;
+    int j = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      int b, m0, n0;
+      decode(t, b, m0, n0);
+      const int a = j & 1;
+      mbar_wait(&accf[a], (j >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + 32 * q + lane;
+      float* crow = C + (int64_t)b * sc + (int64_t)row * ldc;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, r);
-      if (row < M) {
-        const int nc = min(32, N - (n0 + c0));
-        if (nc == 32 && ((ldc & 3) == 0) && (((n0 + c0) & 3) == 0)) {
-          float4* dst = reinterpret_cast<float4*>(crow + n0 + c0);
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
+        if (row < M) {
+          const int nc = min(32, N - (n0 + c0));
+          if (nc == 32 && ((ldc & 3) == 0) && (((n0 + c0) & 3) == 0)) {
+            float4* dst = reinterpret_cast<float4*>(crow + n0 + c0);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-        } else {
+            for (int jj = 0; jj < 8; ++jj)
+              dst[jj] = make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                                    __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
+          } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nc) crow[n0 + c0 + j] = __uint_as_float(r[j]);
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj < nc) crow[n0 + c0 + jj] = __uint_as_float(r[jj]);
+          }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&acce[a]);  // accumulator a may be overwritten
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN < 32 ? 32 : BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
   }
 }
 
@@ -354,8 +394,10 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, float*
   const uint32_t mn_lbo = g_mn_lbo, mn_sbo = g_mn_sbo;
   auto kern = tc_gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT>;
   LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + kBM - 1) / kBM), (unsigned)batch);
-  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, C, ldc, sc, M, N, K, mn_lbo, mn_sbo);
+  // persistent: one CTA per SM, tiles strided over the grid
+  const int64_t tiles = batch * (int64_t)((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
+  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
