@@ -32,7 +32,8 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // fp32 elements per 128-byte swizzle row
 constexpr int kStages = 3;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 12 warps: TMA, MMA, 6 split converters, 4 epilogue
+constexpr int kConv = 192;     // split-converter threads (warps 2-7)
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -135,7 +136,8 @@ struct TcCfg {
   static constexpr int A_BYTES = kBM * kBK * 4;  // 16 KB
   static constexpr int B_BYTES = BN * kBK * 4;
   static constexpr int STAGE_BYTES = (SPLIT == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
-  static constexpr int SMEM = kStages * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
+  static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // per-warp 32x33 transpose buffers
+  static constexpr int SMEM = kStages * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */ + EPI_BYTES;
   static_assert(2 * BN <= 512, "two accumulators must fit in TMEM");
 };
 
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], SPLIT == 3 ? 64 : 1);
+      mbar_init(&conv[s], SPLIT == 3 ? kConv : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -257,10 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 8) {
     // ---------------------------------------------------------------- 3xTF32 split
     if constexpr (SPLIT == 3) {
-      const int ct = threadIdx.x - 64;  // 0..63
+      const int ct = threadIdx.x - 64;  // 0 .. kConv-1
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4* ah = reinterpret_cast<float4*>(a_hi(s));
           float4* al = reinterpret_cast<float4*>(a_lo(s));
 #pragma unroll 4
-          for (int i = ct; i < Cfg::A_BYTES / 16; i += 64) {
+          for (int i = ct; i < Cfg::A_BYTES / 16; i += kConv) {
             const float4 x = ah[i];
             float4 h, l;
             h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4* bh = reinterpret_cast<float4*>(b_hi(s));
           float4* bl = reinterpret_cast<float4*>(b_lo(s));
 #pragma unroll 4
-          for (int i = ct; i < Cfg::B_BYTES / 16; i += 64) {
+          for (int i = ct; i < Cfg::B_BYTES / 16; i += kConv) {
             const float4 x = bh[i];
             float4 h, l;
             h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
@@ -307,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int q = warp - 4;  // TMEM lane quarter of this warp
+    const int q = warp - 8;  // TMEM lane quarter of this warp (warps 8-11)
+    float* stage = reinterpret_cast<float*>(base + kStages * Cfg::STAGE_BYTES + 256) + q * 32 * 33;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
       int b, m0, n0;
@@ -315,26 +318,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int a = j & 1;
       mbar_wait(&accf[a], (j >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + 32 * q + lane;
-      float* crow = C + (int64_t)b * sc + (int64_t)row * ldc;
+      const int row0 = m0 + 32 * q;
+      float* cb = C + (int64_t)b * sc;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
-        if (row < M) {
-          const int nc = min(32, N - (n0 + c0));
-          if (nc == 32 && ((ldc & 3) == 0) && (((n0 + c0) & 3) == 0)) {
-            float4* dst = reinterpret_cast<float4*>(crow + n0 + c0);
+        // transpose the 32x32 chunk through shared memory so global stores are row-coalesced
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              dst[jj] = make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
-                                    __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
-          } else {
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (jj < nc) crow[n0 + c0 + jj] = __uint_as_float(r[jj]);
+        for (int jj = 0; jj < 32; ++jj) stage[lane * 33 + jj] = __uint_as_float(r[jj]);
+        __syncwarp();
+        const int col = n0 + c0 + lane;
+        if (col < N) {
+#pragma unroll 8
+          for (int rr = 0; rr < 32; ++rr) {
+            const int row = row0 + rr;
+            if (row < M) cb[(int64_t)row * ldc + col] = stage[rr * 33 + lane];
           }
         }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&acce[a]);  // accumulator a may be overwritten
