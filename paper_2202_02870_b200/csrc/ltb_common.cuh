@@ -202,6 +202,16 @@ inline bool dtype_is_complex(int dt) { return dt == LTB_C64 || dt == LTB_C128; }
 inline bool dtype_is_double(int dt) { return dt == LTB_F64 || dt == LTB_C128; }
 inline bool dtype_valid(int dt) { return dt >= 0 && dt <= 3; }
 
+// raise a kernel's dynamic shared-memory limit (and optionally prefer the max
+// smem carveout) only the first time a larger size is needed: the attribute
+// calls cost host time on every launch otherwise
+int ltb_ensure_smem(ltb_ctx* ctx, const void* kern, size_t smem, bool carveout = false);
+template <typename K> inline int ensure_smem(ltb_ctx* ctx, K kern, size_t smem, bool carveout = false) {
+  return ltb_ensure_smem(ctx, reinterpret_cast<const void*>(kern), smem, carveout);
+}
+// cached cudaOccupancyMaxActiveBlocksPerMultiprocessor
+int ltb_occupancy(const void* kern, int threads, size_t smem);
+
 // stream-ordered scratch allocation
 int ltb_ws_alloc(ltb_ctx* ctx, size_t bytes, void** out);
 void ltb_ws_free(ltb_ctx* ctx, void* p);

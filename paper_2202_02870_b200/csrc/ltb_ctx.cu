@@ -1,6 +1,10 @@
 // Context, memory, spec upload and small C-ABI glue for libltb.
 #include <cstdarg>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <unordered_map>
 #include <vector>
 
 #include "ltb_common.cuh"
@@ -28,6 +32,38 @@ int ltb_ws_alloc(ltb_ctx* ctx, size_t bytes, void** out) {
 
 void ltb_ws_free(ltb_ctx* ctx, void* p) {
   if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+namespace {
+std::mutex g_attr_mu;
+std::unordered_map<const void*, size_t> g_smem_set;
+std::map<std::tuple<const void*, int, size_t>, int> g_occ;
+}  // namespace
+
+int ltb_ensure_smem(ltb_ctx* ctx, const void* kern, size_t smem, bool carveout) {
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  auto it = g_smem_set.find(kern);
+  if (it != g_smem_set.end() && it->second >= smem) return LTB_OK;
+  if (smem > 48 * 1024) LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (carveout)
+    LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           (int)cudaSharedmemCarveoutMaxShared));
+  g_smem_set[kern] = smem;
+  return LTB_OK;
+}
+
+int ltb_occupancy(const void* kern, int threads, size_t smem) {
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  const auto key = std::make_tuple(kern, threads, smem);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) return it->second;
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  g_occ[key] = per_sm;
+  return per_sm;
 }
 
 extern "C" {

@@ -449,9 +449,7 @@ int launch_smem_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, con
   const int per_warp = (teams + maxw - 1) / maxw;
   const int nwarps = std::max(1, (teams + per_warp - 1) / per_warp);
   auto kern = jacobi_kernel<T, WANT_V, false, TS, MPL, MINB>;
-  LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         (int)cudaSharedmemCarveoutMaxShared));
+  LTB_TRY(ensure_smem(ctx, kern, smem, true));
   kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, nullptr, o, max_sweeps, mp);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
@@ -494,8 +492,7 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
   LTB_TRY(ltb_ws_alloc(ctx, per * batch * sizeof(T), (void**)&ws));
   const size_t smem = (n + 1) * sizeof(R) + (n + 8) * sizeof(int) + 16;
   auto kern = jacobi_kernel<T, WANT_V, true, 32, 0, 1>;
-  if (smem > 48 * 1024)
-    LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LTB_TRY(ensure_smem(ctx, kern, smem));
   kern<<<(unsigned)batch, 512, smem, ctx->stream>>>(I1, I2, A, ws, o, max_sweeps, mp);
   LTB_LAUNCH_CHECK(ctx);
   ltb_ws_free(ctx, ws);

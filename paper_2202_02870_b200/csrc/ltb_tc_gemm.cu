@@ -374,19 +374,54 @@ EncodeTiledFn get_encode() {
 }
 
 // 3D fp32 map: dims {inner, rows, batch}, box {32, box_rows, 1}, 128B swizzle, zero OOB fill
+// small cache of encoded tensor maps: the encode call costs microseconds of
+// host time, and repeated calls on the same buffers (benchmark steps, PGA
+// iterations) reuse identical maps
+struct MapKey {
+  const float* ptr;
+  int64_t inner, rows, batch, ld, bstride;
+  int box_rows;
+  bool mn32;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && inner == o.inner && rows == o.rows && batch == o.batch && ld == o.ld &&
+           bstride == o.bstride && box_rows == o.box_rows && mn32 == o.mn32;
+  }
+};
+struct MapEntry {
+  MapKey key;
+  CUtensorMap map;
+  bool valid;
+};
+MapEntry g_map_cache[32];
+int g_map_next = 0;
+
 bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t rows, int64_t batch, int64_t ld,
               int64_t bstride, int box_rows, bool mn32 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 4) % 16 || (bstride * 4) % 16) return false;
+  const MapKey key{ptr, inner, rows, batch, ld, bstride, box_rows, mn32};
+  for (auto& e : g_map_cache)
+    if (e.valid && e.key == key) {
+      *map = e.map;
+      return true;
+    }
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)batch};
   cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), (cuuint64_t)(bstride * 4)};
   cuuint32_t box[3] = {32u, (cuuint32_t)box_rows, 1u};
   cuuint32_t estr[3] = {1u, 1u, 1u};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, mn32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const bool ok = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      mn32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (ok) {
+    MapEntry& e = g_map_cache[g_map_next];
+    g_map_next = (g_map_next + 1) % 32;
+    e.key = key;
+    e.map = *map;
+    e.valid = true;
+  }
+  return ok;
 }
 
 template <int BN, bool A_MN, bool B_MN, int SPLIT>
@@ -395,7 +430,7 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, float*
   using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
   const uint32_t mn_lbo = g_mn_lbo, mn_sbo = g_mn_sbo;
   auto kern = tc_gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT>;
-  LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  LTB_TRY(ensure_smem(ctx, kern, Cfg::SMEM));
   // persistent: one CTA per SM, tiles strided over the grid
   const int64_t tiles = batch * (int64_t)((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);

@@ -334,9 +334,7 @@ inline int plan_tile(XformParams& p, size_t* smem_out) {
 template <typename K>
 int64_t xform_grid(ltb_ctx* ctx, const XformParams& p, K kern, size_t smem) {
   const int64_t ntiles = (p.NT + p.TT - 1) / p.TT;
-  int per_sm = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kXformThreads, smem) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
+  const int per_sm = ltb_occupancy(reinterpret_cast<const void*>(kern), kXformThreads, smem);
   return std::min<int64_t>(ntiles, (int64_t)per_sm * ctx->num_sms);
 }
 
@@ -344,8 +342,7 @@ template <typename Tc, typename Tm, class Loader, class Storer>
 int launch_xform_tile(ltb_ctx* ctx, XformParams p, const Loader& ld, const Storer& st, const Tm* mats,
                       double* partials, const int* skip, size_t smem, int64_t* grid_out = nullptr) {
   auto kern = xform_tile_kernel<Tc, Tm, Loader, Storer>;
-  if (smem > 48 * 1024)
-    LTB_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LTB_TRY(ensure_smem(ctx, kern, smem));
   const int64_t nblocks = xform_grid(ctx, p, kern, smem);
   if (grid_out) *grid_out = nblocks;  // number of per-CTA partials written
   if (nblocks == 0) return LTB_OK;
