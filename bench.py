@@ -250,21 +250,30 @@ def run_ours(args):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     phase_ms = np.zeros(4)
     step_ms = []
+    # one step = K1(A), K1(B), K2, K1' captured once as a CUDA graph, with CUDA
+    # events between the phases: replays carry no host enqueue cost
+    for _ in range(2):
+        plan.run(a, b, c)  # settle kernel attributes / tensor-map caches before capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    l0 = nat.launch_count()
+    with torch.cuda.graph(graph, stream=stream):
+        plan.run(a, b, c, marks=lambda i: ev[i].record(stream))
+    launches_per_step = nat.launch_count() - l0
     with ClockSampler(local) as clocks:
         for _ in range(args.warmup):
             flush.zero_()
-            plan.run(a, b, c)
+            graph.replay()
         barrier()
-        launches0 = nat.launch_count()
         for _ in range(args.steps):
             flush.zero_()  # L2 flush outside the timed events
-            plan.run(a, b, c, marks=lambda i: ev[i].record(stream))
+            graph.replay()
             ev[4].synchronize()
             ph = [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
             phase_ms += ph
             step_ms.append(ev[0].elapsed_time(ev[4]))
         barrier()
-        launches = nat.launch_count() - launches0
+        launches = launches_per_step * args.steps
         # e2e: public numpy-in/numpy-out API, host copies inside the timed region
         e2e_t = []
         for i in range(args.warmup + args.steps):

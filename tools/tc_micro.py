@@ -17,9 +17,14 @@ def bench(batch, m, n, k, a_mn, b_mn, split=3, reps=20):
     args = (nat.context(), batch, m, n, k, a_mn, a.data_ptr(), a.shape[2], a.shape[1] * a.shape[2], b_mn, b.data_ptr(),
             b.shape[2], b.shape[1] * b.shape[2], c.data_ptr(), n, m * n, split)
     for _ in range(3): nat.check(nat.lib().ltb_tc_gemm(*args))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(reps): nat.check(nat.lib().ltb_tc_gemm(*args))
+    g.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(reps): nat.check(nat.lib().ltb_tc_gemm(*args))
+    g.replay()
     e1.record(stream); e1.synchronize()
     us = e0.elapsed_time(e1) / reps * 1e3
     byts = 4 * (a.numel() + b.numel() + c.numel())
