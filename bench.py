@@ -250,24 +250,37 @@ def run_ours(args):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     phase_ms = np.zeros(4)
     step_ms = []
-    # one step = K1(A), K1(B), K2, K1' captured once as a CUDA graph, with CUDA
-    # events between the phases: replays carry no host enqueue cost
+    # each phase of the step (K1(A), K1(B), K2, K1') is captured once as a CUDA
+    # graph; replays carry no per-kernel host enqueue cost, and CUDA events
+    # recorded between the phase replays give the per-kernel device times
     for _ in range(2):
         plan.run(a, b, c)  # settle kernel attributes / tensor-map caches before capture
     torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
     l0 = nat.launch_count()
-    with torch.cuda.graph(graph, stream=stream):
-        plan.run(a, b, c, marks=lambda i: ev[i].record(stream))
+    graphs = []
+    for ph in range(4):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            plan.run(a, b, c, phases=(ph,))
+        graphs.append(g)
     launches_per_step = nat.launch_count() - l0
+
+    def step(marks=None):
+        for ph, g in enumerate(graphs):
+            if marks:
+                marks(ph)
+            g.replay()
+        if marks:
+            marks(4)
+
     with ClockSampler(local) as clocks:
         for _ in range(args.warmup):
             flush.zero_()
-            graph.replay()
+            step()
         barrier()
         for _ in range(args.steps):
             flush.zero_()  # L2 flush outside the timed events
-            graph.replay()
+            step(marks=lambda i: ev[i].record(stream))
             ev[4].synchronize()
             ph = [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
             phase_ms += ph

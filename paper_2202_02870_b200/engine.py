@@ -49,24 +49,33 @@ class LProductPlan:
         s = nat.real_of(self.hat_dtype).itemsize
         return s * (self.m * self.k + self.k * self.n + self.m * self.n) * self.P
 
-    def run(self, a: nat.DeviceArray, b: nat.DeviceArray, c: nat.DeviceArray, marks=None, check_real=False):
+    def run(self, a: nat.DeviceArray, b: nat.DeviceArray, c: nat.DeviceArray, marks=None, check_real=False,
+            phases=(0, 1, 2, 3)):
+        """Enqueue the phases K1(A)=0, K1(B)=1, K2=2, K1'=3 (all by default); `marks(i)`
+        is called before phase i and after the last one (i = 4)."""
         lib, ctx = nat.lib(), nat.context()
         h = self.handle.ptr
         mark = marks or (lambda i: None)
-        mark(0)
-        nat.check(lib.ltb_transform(ctx, h, self.m * self.k, 0, a.code, nat.TUBE_MAJOR, a.ptr, self.ha.code,
-                                    nat.SLICE_MAJOR, self.ha.ptr, None))
-        mark(1)
-        nat.check(lib.ltb_transform(ctx, h, self.k * self.n, 0, b.code, nat.TUBE_MAJOR, b.ptr, self.hb.code,
-                                    nat.SLICE_MAJOR, self.hb.ptr, None))
-        mark(2)
         m, k, n, P = self.m, self.k, self.n, self.P
-        nat.check(lib.ltb_slice_gemm(ctx, self.ha.code, P, m, n, k, nat.OP_N, self.ha.ptr, k, m * k, nat.OP_N,
-                                     self.hb.ptr, n, k * n, self.hc.ptr, n, m * n))
+        sums = None
+        mark(0)
+        if 0 in phases:
+            nat.check(lib.ltb_transform(ctx, h, m * k, 0, a.code, nat.TUBE_MAJOR, a.ptr, self.ha.code,
+                                        nat.SLICE_MAJOR, self.ha.ptr, None))
+        mark(1)
+        if 1 in phases:
+            nat.check(lib.ltb_transform(ctx, h, k * n, 0, b.code, nat.TUBE_MAJOR, b.ptr, self.hb.code,
+                                        nat.SLICE_MAJOR, self.hb.ptr, None))
+        mark(2)
+        if 2 in phases:
+            nat.check(lib.ltb_slice_gemm(ctx, self.ha.code, P, m, n, k, nat.OP_N, self.ha.ptr, k, m * k, nat.OP_N,
+                                         self.hb.ptr, n, k * n, self.hc.ptr, n, m * n))
         mark(3)
-        sums = self._sums if (check_real and self.out_real and np.iscomplexobj(np.zeros(0, self.hat_dtype))) else None
-        nat.check(lib.ltb_transform(ctx, h, m * n, 1, self.hc.code, nat.SLICE_MAJOR, self.hc.ptr, c.code,
-                                    nat.TUBE_MAJOR, c.ptr, sums))
+        if 3 in phases:
+            if check_real and self.out_real and np.iscomplexobj(np.zeros(0, self.hat_dtype)):
+                sums = self._sums
+            nat.check(lib.ltb_transform(ctx, h, m * n, 1, self.hc.code, nat.SLICE_MAJOR, self.hc.ptr, c.code,
+                                        nat.TUBE_MAJOR, c.ptr, sums))
         mark(4)
         if sums is not None:
             check_real_residual((sums[0], sums[1]), c.dtype)
