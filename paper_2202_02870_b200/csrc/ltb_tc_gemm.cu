@@ -130,6 +130,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 3xTF32 split of one smem tile (layout-agnostic, elementwise):
+//   hi = x with the low 13 mantissa bits cleared (what the tensor core reads from
+//        x itself: measured on B200, kind::tf32 truncates fp32 -> tf32, so with
+//        raw_hi the fp32 tile is left in place as the hi operand),
+//   lo = round-to-nearest-tf32(x - hi), so the tensor core's truncation of lo is
+//        exact and the residual error is unbiased.
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ float tf32_round(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+template <int N16>
+__device__ __forceinline__ void split_tile(float4* hi, float4* lo, int ct, int raw_hi) {
+#pragma unroll 4
+  for (int i = ct; i < N16; i += kConv) {
+    const float4 x = hi[i];
+    const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+    lo[i] = make_float4(tf32_round(x.x - h.x), tf32_round(x.y - h.y), tf32_round(x.z - h.z), tf32_round(x.w - h.w));
+    if (!raw_hi) hi[i] = h;
+  }
+}
+
 // ------------------------------------------------------------------ kernel
 template <int BN, bool A_MN, bool B_MN, int SPLIT>
 struct TcCfg {
@@ -145,7 +166,16 @@ template <int BN, bool A_MN, bool B_MN, int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K, int batches,
-                        uint32_t mn_lbo, uint32_t mn_sbo) {
+                        uint32_t mn_lbo, uint32_t mn_sbo, int raw_hi, unsigned long long* dbg, int epi_mode) {
+  // optional timeline instrumentation (CTA 0, %globaltimer ns) for the launch-cost analysis
+  auto stamp = [&](int slot) {
+    if (dbg && blockIdx.x == 0) {
+      unsigned long long tns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+      dbg[slot] = tns;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
   using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -195,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -206,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          if (it == 0) stamp(2);
           mbar_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
           const int k0 = kt * kBK;
           if (!A_MN) {
@@ -253,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_tf32(dacc, dal, dbh, idesc, 1u);
             }
           }
+          if (it == 0) stamp(4);
           umma_commit(&empty[s]);  // stage reusable once these MMAs complete
           if (kt == ktiles - 1) umma_commit(&accf[a]);
         }
@@ -268,41 +301,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
-          float4* ah = reinterpret_cast<float4*>(a_hi(s));
-          float4* al = reinterpret_cast<float4*>(a_lo(s));
-#pragma unroll 4
-          for (int i = ct; i < Cfg::A_BYTES / 16; i += kConv) {
-            const float4 x = ah[i];
-            float4 h, l;
-            h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-            h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-            h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-            h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-            l.x = x.x - h.x;
-            l.y = x.y - h.y;
-            l.z = x.z - h.z;
-            l.w = x.w - h.w;
-            ah[i] = h;
-            al[i] = l;
-          }
-          float4* bh = reinterpret_cast<float4*>(b_hi(s));
-          float4* bl = reinterpret_cast<float4*>(b_lo(s));
-#pragma unroll 4
-          for (int i = ct; i < Cfg::B_BYTES / 16; i += kConv) {
-            const float4 x = bh[i];
-            float4 h, l;
-            h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-            h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-            h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-            h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-            l.x = x.x - h.x;
-            l.y = x.y - h.y;
-            l.z = x.z - h.z;
-            l.w = x.w - h.w;
-            bh[i] = h;
-            bl[i] = l;
-          }
+          split_tile<Cfg::A_BYTES / 16>(reinterpret_cast<float4*>(a_hi(s)), reinterpret_cast<float4*>(a_lo(s)), ct,
+                                        raw_hi);
+          split_tile<Cfg::B_BYTES / 16>(reinterpret_cast<float4*>(b_hi(s)), reinterpret_cast<float4*>(b_lo(s)), ct,
+                                        raw_hi);
           fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+          if (it == 0 && ct == 0) stamp(3);
           mbar_arrive(&conv[s]);
         }
       }
@@ -317,28 +321,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode(t, b, m0, n0);
       const int a = j & 1;
       mbar_wait(&accf[a], (j >> 1) & 1);
+      if (j == 0 && q == 0 && lane == 0) stamp(5);
       tc_fence_after();
       const int row0 = m0 + 32 * q;
       float* cb = C + (int64_t)b * sc;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
+        const bool tl = (j == 0 && q == 0 && lane == 0 && c0 < 96);
+        if (tl) stamp(8 + 2 * (c0 / 32));
         tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
-        // transpose the 32x32 chunk through shared memory so global stores are row-coalesced
+        if (tl) stamp(9 + 2 * (c0 / 32));
+        // mode 1 (default): each thread stores its row segment with 16-byte vector stores
+        // (measured 2x faster than transposing through smem for row-coalesced stores)
+        if (epi_mode == 1) {
+          const int row = row0 + lane;
+          if (row < M) {
+            float* dst = cb + (int64_t)row * ldc + n0 + c0;
+            if (n0 + c0 + 32 <= N && (ldc & 3) == 0) {
+              float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) stage[lane * 33 + jj] = __uint_as_float(r[jj]);
-        __syncwarp();
-        const int col = n0 + c0 + lane;
-        if (col < N) {
-#pragma unroll 8
-          for (int rr = 0; rr < 32; ++rr) {
-            const int row = row0 + rr;
-            if (row < M) cb[(int64_t)row * ldc + col] = stage[rr * 33 + lane];
+              for (int jj = 0; jj < 8; ++jj)
+                d4[jj] = make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                                     __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj)
+                if (n0 + c0 + jj < N) dst[jj] = __uint_as_float(r[jj]);
+            }
           }
+        } else if (epi_mode == 0) {  // transpose through shared memory, row-coalesced stores
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) stage[lane * 33 + jj] = __uint_as_float(r[jj]);
+          __syncwarp();
+          const int col = n0 + c0 + lane;
+          if (col < N) {
+#pragma unroll 8
+            for (int rr = 0; rr < 32; ++rr) {
+              const int row = row0 + rr;
+              if (row < M) cb[(int64_t)row * ldc + col] = stage[rr * 33 + lane];
+            }
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
       tc_fence_before();
+      if (j == 0 && q == 0 && lane == 0) stamp(6);
       mbar_arrive(&acce[a]);  // accumulator a may be overwritten
     }
   }
@@ -346,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
+    if (lane == 0) stamp(7);
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
   }
 }
@@ -353,6 +382,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ host: tensor maps
 // MN-major 128B-swizzle descriptor strides (bytes): LBO = MN-chunk stride, SBO = 8-row K-group stride
 uint32_t g_mn_lbo = 4096, g_mn_sbo = 512;
+// 1: leave the fp32 tile in place as the "hi" operand (valid iff the tensor core
+// truncates fp32 -> tf32); 0: store hi = x with the low 13 bits cleared
+int g_raw_hi = 1;
+unsigned long long* g_dbg = nullptr;
+// epilogue store mode: 1 direct row stores (default), 0 smem-transposed coalesced stores,
+// 2 no stores (diagnostic only)
+int g_epi_mode = 1;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -434,7 +470,7 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, float*
   // persistent: one CTA per SM, tiles strided over the grid
   const int64_t tiles = batch * (int64_t)((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
-  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo);
+  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo, g_raw_hi, g_dbg, g_epi_mode);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -469,6 +505,10 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
   if (a_mn && !b_mn) return launch_tc<128, true, false, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
   return launch_tc<128, true, true, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
 }
+
+extern "C" void ltb_tc_debug_set_raw_hi(int v) { g_raw_hi = v; }
+extern "C" void ltb_tc_debug_set_epi_mode(int v) { g_epi_mode = v; }
+extern "C" void ltb_tc_debug_set_timeline(void* d_buf) { g_dbg = (unsigned long long*)d_buf; }
 
 extern "C" void ltb_tc_debug_set_mn_strides(uint32_t lbo, uint32_t sbo) {
   g_mn_lbo = lbo;
