@@ -176,6 +176,12 @@ int ltb_slice_transpose(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64
 int ltb_project_omega(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const uint8_t* d_mask,
                       void* d_out);
 
+/* the PGA gradient point of completion.py:170-171 on one row shard (multi-GPU
+ * driver): y = x + beta (x - x_prev), g = y - (where(mask, y, 0) - p_obs);
+ * real dtype, mask uint8, y may be NULL */
+int ltb_pga_gradient(ltb_ctx* ctx, int dtype, int64_t n, const void* d_xc, const void* d_xp,
+                     const void* d_pobs, const uint8_t* d_mask, double beta, void* d_y, void* d_g);
+
 /* ---------------------------------------------------------------- K4 + PGA
  * pga_complete (completion.py:141-202).  The host keeps the scalar
  * recurrences: it passes, per iteration k (1-based), beta_k = (t_{k-1}-1)/t_k

@@ -68,7 +68,8 @@ _SIGNATURES = {
     "ltb_embed_diag": ([_vp, _int, _i64, _i64, _i64, _vp, _vp], _int),
     "ltb_slice_transpose": ([_vp, _int, _i64, _i64, _i64, _int, _vp, _vp], _int),
     "ltb_project_omega": ([_vp, _int, _i64, _vp, _vp, _vp], _int),
-    "ltb_pga_create": ([_vp, _vp, _int, _i64, _i64, _dp, _vp, _dp, C.POINTER(_vp)], _int),
+    "ltb_pga_gradient": ([_vp, _int, _i64, _vp, _vp, _vp, _vp, C.c_double, _vp, _vp], _int),
+    "ltb_pga_create":([_vp, _vp, _int, _i64, _i64, _dp, _vp, _dp, C.POINTER(_vp)], _int),
     "ltb_pga_pobs_sumsq": ([_vp, _dp], _int),
     "ltb_pga_run": ([_vp, _int, _int, _dp, _dp, C.c_double, _dp, _ip, _ip], _int),
     "ltb_pga_fetch": ([_vp, _int, _dp], _int),

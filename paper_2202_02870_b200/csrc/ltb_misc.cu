@@ -78,6 +78,25 @@ __global__ void dot_partials_kernel(int64_t n, const T* __restrict__ x, const T*
   }
 }
 
+// PGA gradient point (completion.py:170-171) on a row shard, same rounding as the fused path:
+// y = x + beta (x - x_prev), g = y - (where(mask, y, 0) - p_obs)
+template <typename R>
+__global__ void pga_gradient_kernel(int64_t n, const R* __restrict__ xc, const R* __restrict__ xp,
+                                    const R* __restrict__ pobs, const uint8_t* __restrict__ mask, R beta,
+                                    R* __restrict__ y, R* __restrict__ g) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    R yi;
+    if constexpr (std::is_same<R, double>::value) {
+      yi = __dadd_rn(xc[i], __dmul_rn(beta, __dsub_rn(xc[i], xp[i])));
+      g[i] = __dsub_rn(yi, __dsub_rn(mask[i] ? yi : 0.0, pobs[i]));
+    } else {
+      yi = __fadd_rn(xc[i], __fmul_rn(beta, __fsub_rn(xc[i], xp[i])));
+      g[i] = __fsub_rn(yi, __fsub_rn(mask[i] ? yi : 0.f, pobs[i]));
+    }
+    if (y) y[i] = yi;
+  }
+}
+
 }  // namespace
 
 __global__ void finalize_partials_kernel(const double* __restrict__ partials, int64_t nblocks, int nacc,
@@ -125,6 +144,23 @@ int ltb_project_omega(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const
     LTB_LAUNCH_CHECK(ctx);
     return LTB_OK;
   });
+}
+
+int ltb_pga_gradient(ltb_ctx* ctx, int dtype, int64_t n, const void* d_xc, const void* d_xp, const void* d_pobs,
+                     const uint8_t* d_mask, double beta, void* d_y, void* d_g) {
+  if (dtype != LTB_F32 && dtype != LTB_F64) return ltb_set_error(ctx, LTB_EPARAM, "pga_gradient: real dtype only");
+  if (n <= 0) return LTB_OK;
+  const int blocks = grid_for(n, 256, ctx->num_sms * 8);
+  if (dtype == LTB_F64)
+    pga_gradient_kernel<double><<<blocks, 256, 0, ctx->stream>>>(n, (const double*)d_xc, (const double*)d_xp,
+                                                                 (const double*)d_pobs, d_mask, beta, (double*)d_y,
+                                                                 (double*)d_g);
+  else
+    pga_gradient_kernel<float><<<blocks, 256, 0, ctx->stream>>>(n, (const float*)d_xc, (const float*)d_xp,
+                                                                (const float*)d_pobs, d_mask, (float)beta,
+                                                                (float*)d_y, (float*)d_g);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
 }
 
 int ltb_reduce_dot(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y, double* h_out) {
