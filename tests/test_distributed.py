@@ -142,7 +142,8 @@ def _pga_worker(rank, world):
                                  OracleEngine(spec_o, (4,)), ground_truth_rows=torch.from_numpy(m[r0:r1]))
     ref, recs, status = O.pga_complete(m, mask, spec_o, max_iters=25, tol=1e-3, ground_truth=m)
     return (float(np.abs(x.numpy() - ref[r0:r1]).max()), trace.status == status, trace.iterations == len(recs),
-            max(abs(r.rel_change - rr[3]) / max(rr[3], 1e-300) for r, rr in zip(trace.records, recs)),
+            max((0.0 if r.rel_change == rr[3] else abs(r.rel_change - rr[3]) / max(rr[3], 1e-300))
+                for r, rr in zip(trace.records, recs)),
             # mu0 = nu ||M||_F: the sharded sum differs from numpy's BLAS order in the last bits
             bool(np.allclose([r.mu for r in trace.records], [rr[1] for rr in recs], rtol=1e-14, atol=0)),
             max((0.0 if (np.isnan(r.rse) and np.isnan(rr[4])) else abs(r.rse - rr[4]) / rr[4])
