@@ -210,14 +210,75 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- our arm
+def run_ours_dist(args):
+    """N > 1: the row-sharded *_L product of SURVEY.md §8(e) (weak scaling).  Rank g holds 256
+    rows of A (global I1 = 256 N) and 128/N rows of B; B-hat is all-gathered over NCCL; each
+    rank produces its 256 rows of C.  Time = max over ranks of the device (CUDA-event) step time."""
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2202_02870_b200 as L
+    from paper_2202_02870_b200 import _native as nat
+    from paper_2202_02870_b200.distributed import DeviceEngine, blocks, dist_l_product
+
+    nat.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    spec = L.make_spec("dct", (256 * ws, 256, 3, 32))
+    eng = DeviceEngine(spec, (3, 32))
+    a_h, b_full = _cfg2_inputs(seed=rank)
+    _, b_full = _cfg2_inputs(seed=0)  # B is one global operand, row-sharded
+    k0, k1 = blocks(128, ws)[rank]
+    a = torch.from_numpy(a_h).cuda()
+    b = torch.from_numpy(np.ascontiguousarray(b_full[k0:k1])).cuda()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    E_a, E_b, E_c = 256 * 128 * 96, 128 * 256 * 96, 256 * 256 * 96
+    flops_job = ws * (2 * 256 * 128 * 256 * 96 + 70 * (E_a + E_c)) + 70 * E_b
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    with ClockSampler(local) as clocks:
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            dist.barrier()
+            e0.record(stream)
+            c = dist_l_product(a, b, eng)
+            e1.record(stream)
+            e1.synchronize()
+            if i >= args.warmup:
+                times.append(e0.elapsed_time(e1) / 1e3)
+    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t.item())
+    hbm_peak, _, peak_src = _peaks()
+    alg_bytes = 4 * (E_a + E_b // ws + E_c)
+    achieved = alg_bytes * args.steps / t_step / 1e9
+    line = {
+        "metric": "*_L-product GFLOP/s", "value": flops_job * args.steps / t_step / 1e9, "unit": "GFLOP/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) (BASELINE config 2 shapes per rank), seeds = rank",
+        "config": {"workload": f"config2 l_product, A rows sharded: A {256 * ws}x128x3x32 * B 128x256x3x32, DCT modes 3,4",
+                   "flop_per_step": flops_job, "l2": "flushed (512 MiB write) before every timed step",
+                   "parallelism": f"row-sharded x{ws}, B-hat all-gather (NCCL)"},
+        "roofline": {"kernel": "whole sharded step", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": achieved / hbm_peak, "peak_source": f"{peak_src} HBM copy",
+                     "traffic": None},
+        "e2e": None, "gpu_launches": None, "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
 
     ws, rank, local = _dist()
     if ws > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_ours_dist(args)
     torch.cuda.set_device(local)
     import paper_2202_02870_b200 as L
     from paper_2202_02870_b200 import _native as nat

@@ -68,7 +68,9 @@ class DeviceEngine:
         self.trailing = tuple(int(d) for d in trailing)
         self.handle = device_spec(spec, self.trailing)
         self.P = self.handle.P
-        nat.check(nat.lib().ltb_ctx_set_stream(nat.context(), torch.cuda.current_stream().cuda_stream))
+        # share torch's current stream (handle 0 = the legacy default stream, cudaStreamLegacy)
+        s = torch.cuda.current_stream().cuda_stream
+        nat.check(nat.lib().ltb_ctx_set_stream(nat.context(), s if s else 1))
 
     def _xform(self, x: torch.Tensor, rows: int, cols: int, inverse: bool, layout_in, layout_out, out_dtype):
         out_shape = (self.P, rows, cols) if layout_out == nat.SLICE_MAJOR else (rows, cols) + self.trailing

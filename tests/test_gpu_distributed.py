@@ -1,0 +1,63 @@
+"""The multi-GPU driver's device engine (distributed.DeviceEngine on libltb) through NCCL with
+world_size 1 on cuda:0: the sharded l_product / SVT / PGA must reproduce the single-device
+API.  (More ranks than GPUs are never emulated on one GPU; the exchanges themselves are
+covered for world 2/3 by tests/test_distributed.py with gloo.)"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import paper_2202_02870_b200 as L
+from paper_2202_02870_b200.distributed import DeviceEngine, dist_l_product, dist_pga_complete, dist_svt
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl_world1():
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+def test_dist_l_product_device(nccl_world1):
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((64, 16, 3, 8)).astype(np.float32)
+    b = rng.standard_normal((16, 48, 3, 8)).astype(np.float32)
+    spec = L.make_spec("dct", (64, 48, 3, 8))
+    eng = DeviceEngine(spec, (3, 8))
+    c = dist_l_product(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), eng)
+    torch.cuda.synchronize()
+    assert rel_err(c.cpu().numpy(), L.l_product(a, b, spec)) < 1e-5
+
+
+def test_dist_svt_device(nccl_world1):
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((20, 12, 6))
+    spec = L.make_spec("fft", x.shape)
+    out = dist_svt(torch.from_numpy(x).cuda(), 0.9, 20, DeviceEngine(spec, (6,)))
+    torch.cuda.synchronize()
+    assert rel_err(out.cpu().numpy(), L.svt(x, 0.9, spec)) < 1e-10
+
+
+def test_dist_pga_device(nccl_world1, golden):
+    m = golden["c_dct/m"]
+    mask = golden["c_dct/mask"]
+    spec = L.make_spec("dct", m.shape)
+    cfg = L.CompletionConfig(spec=spec, max_iters=30)
+    x, trace = dist_pga_complete(torch.from_numpy(m).cuda(), torch.from_numpy(mask).cuda(), cfg, m.shape[0],
+                                 DeviceEngine(spec, m.shape[2:]))
+    ref, rtrace = L.pga_complete(m, mask, cfg)
+    assert trace.iterations == rtrace.iterations
+    assert rel_err(x.cpu().numpy(), ref) < 1e-10
