@@ -1,0 +1,134 @@
+"""BASELINE.json configurations at (or near) full size on the GPU, checked against the CPU
+oracle run here on the same seeded inputs (the oracle is the checker only), and through
+size-independent properties where the oracle would be too slow.  Tolerances (north_star):
+1e-4 relative Frobenius for float32 work, 1e-10 for float64."""
+
+import numpy as np
+import pytest
+
+import ltensor_oracle as O
+import paper_2202_02870_b200 as L
+from paper_2202_02870_b200 import core
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg2_inputs():
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((256, 128, 3, 32), dtype=np.float32)
+    b = rng.standard_normal((128, 256, 3, 32), dtype=np.float32)
+    return a, b
+
+
+def test_config2_l_product_full():
+    a, b = cfg2_inputs()
+    spec = L.make_spec("dct", (256, 256, 3, 32))
+    c = L.l_product(a, b, spec)
+    assert c.dtype == np.float32 and c.shape == (256, 256, 3, 32)
+    ref = O.l_product(a.astype(np.float64), b.astype(np.float64), O.ospec("dct", (256, 256, 3, 32)))
+    assert rel_err(c, ref) < 1e-4
+
+
+def test_config2_linearity_and_associativity():
+    """Size-independent checks at full size: L-linearity in A, and (A*B)*e == A*(B*e) for an
+    identity-like scalar tensor e."""
+    a, b = cfg2_inputs()
+    spec = L.make_spec("dct", (256, 256, 3, 32))
+    c1 = L.l_product(a, b, spec)
+    c2 = L.l_product(2.0 * a, b, spec)
+    assert rel_err(c2, 2.0 * c1) < 1e-6
+    eye = L.identity_tensor(256, (3, 32), spec).astype(np.float32)
+    assert rel_err(L.l_product(c1, eye, spec), c1) < 1e-5
+
+
+def cfg3_data(shape=(144, 176, 3, 100), rank=10, seed=0):
+    rng = np.random.default_rng(seed)
+    i1, i2, c, t = shape
+    a = rng.standard_normal((i1, rank, c, t), dtype=np.float32).astype(np.float64)
+    b = rng.standard_normal((rank, i2, c, t), dtype=np.float32).astype(np.float64)
+    x0 = O.l_product(a, b, O.ospec("dct", shape))
+    x0 = (x0 - x0.min()) / (x0.max() - x0.min())
+    m = (x0 + rng.normal(0.0, 0.01, x0.shape)).astype(np.float32)
+    mask = rng.random(m.shape) < 0.2
+    return m, mask
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+def test_config3_pga_full_size_first_iterations(precision, tol):
+    m, mask = cfg3_data()
+    spec = L.make_spec("dct", m.shape)
+    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=2)
+    x, trace = L.pga_complete(m, mask, cfg, precision=precision)
+    ref, recs, _ = O.pga_complete(m, mask, O.ospec("dct", m.shape), tol=1e-300, max_iters=2)
+    assert trace.iterations == 2
+    assert rel_err(x, ref) < tol
+    np.testing.assert_allclose([r.rel_change for r in trace.records], [r[3] for r in recs],
+                               rtol=1e-3 if precision == "fp32" else 1e-8)
+
+
+def test_config1_pga_full():
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((64, 5, 16))
+    b = rng.standard_normal((5, 64, 16))
+    spec = L.make_spec("dct", (64, 64, 16))
+    m = L.l_product(a, b, spec)
+    mask = rng.random(m.shape) < 0.5
+    cfg = L.CompletionConfig(spec=spec, mu0=0.01, mu_bar_ratio=1.0, tol=1e-300, max_iters=100)
+    x, trace = L.pga_complete(m, mask, cfg)
+    ref, recs, _ = O.pga_complete(m, mask, O.ospec("dct", m.shape), mu0=0.01, mu_bar_ratio=1.0, tol=1e-300,
+                                  max_iters=100)
+    assert trace.iterations == 100
+    assert rel_err(x, ref) < 1e-10
+    assert abs(O.rse(x, m) - 0.383) < 0.01  # oracle RSE after 100 iterations ~0.383
+
+
+@pytest.mark.parametrize("n", [128])
+def test_config5_svt_and_tsvd(n):
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((n, n, 4, 8, 16), dtype=np.float32)
+    spec = L.make_spec("dct", a.shape)
+    ospec = O.ospec("dct", a.shape)
+    sv_ref = O.singular_values(a.astype(np.float64), ospec)
+    tau = 0.1 * float(np.median(sv_ref))
+    out = L.svt(a, tau, spec)
+    ref = O.svt(a.astype(np.float64), tau, ospec)
+    assert out.dtype == np.float32 and rel_err(out, ref) < 1e-4
+    f = L.t_svd(a, spec)
+    # singular values (device slice order -> reference p-order) and the factor-independent S
+    sv = L.linalg._singular_values(a, spec)[core.slice_order_permutation(a.shape[2:])]
+    assert rel_err(sv, sv_ref) < 1e-5
+    assert rel_err(np.sort(f.tube_norms)[::-1], f.tube_norms) == 0.0
+    assert abs(float((f.tube_norms ** 2).sum()) - float((a.astype(np.float64) ** 2).sum())) \
+        < 1e-4 * float((a.astype(np.float64) ** 2).sum())
+
+
+def test_config5_n256_global_tier_properties():
+    """n = 256 slices exceed shared memory (global-workspace Jacobi tier): check svt(., 0) == id
+    and the Frobenius identity of the singular values on a 4-slice cut of config 5."""
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((256, 256, 4), dtype=np.float32)
+    spec = L.make_spec("dct", a.shape)
+    assert rel_err(L.svt(a, 0.0, spec), a) < 1e-4
+    sv = L.linalg._singular_values(a, spec)
+    assert abs(float((sv.astype(np.float64) ** 2).sum()) - float((a.astype(np.float64) ** 2).sum())) \
+        < 1e-4 * float((a.astype(np.float64) ** 2).sum())
+
+
+def test_config4_reduced_pga():
+    """Config 4 recipe at 128 x 128 x 3 x 64: explicit Q (x) F64, complex64
+    transform domain, Bernoulli(0.3), first iterations vs the oracle."""
+    rng = np.random.default_rng(0)
+    q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    f = L.build_fourier_matrix(64)
+    a = rng.standard_normal((128, 20, 3, 64), dtype=np.float32)
+    b = rng.standard_normal((20, 128, 3, 64), dtype=np.float32)
+    spec = L.make_spec("explicit", (128, 128, 3, 64), matrices={3: q, 4: f})
+    ospec = O.ospec("explicit", (128, 128, 3, 64), matrices={3: q, 4: f})
+    m = O.l_product(a.astype(np.float64), b.astype(np.float64), ospec)
+    mask = rng.random(m.shape) < 0.3
+    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=3)
+    x, trace = L.pga_complete(m.astype(np.float32), mask, cfg)
+    ref, recs, _ = O.pga_complete(m, mask, ospec, tol=1e-300, max_iters=3)
+    assert trace.iterations == 3
+    assert rel_err(x, ref) < 1e-4
