@@ -358,6 +358,7 @@ def run_ours(args):
             if i >= args.warmup:
                 e2e_t.append(dt)
         pga = None if args.skip_pga else bench_pga(L, nat, torch, args)
+        extras = None if args.skip_extras else bench_extras(L, nat, torch, args, cpu=not args.no_cpu_baseline)
 
     t_step = float(np.sum(step_ms)) / 1e3
     if ws > 1:
@@ -416,6 +417,8 @@ def run_ours(args):
     }
     if pga is not None:
         line["pga"] = pga
+    if extras is not None:
+        line["configs"] = extras
     if rank == 0 and not args.no_cpu_baseline:
         times = cpu_lproduct(1, 1, budget_s=args.cpu_budget)
         info = _cpu_info()
@@ -471,8 +474,99 @@ def bench_pga(L, nat, torch, args):
             "rse_vs_m": float(np.linalg.norm(x - m) ** 2 / max(np.linalg.norm(x) ** 2, 1e-300))}
 
 
+def _run_pga(L, nat, torch, m, mask, spec, precision, iters, **cfg_kw):
+    """Device-resident PGA run through the solver (setup and fetch outside the timed region)."""
+    from paper_2202_02870_b200.completion import PGASolver, pga_schedule
+
+    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=iters, **cfg_kw)
+    m64 = np.asarray(m, dtype=np.float64)
+    mu0 = cfg.nu * L.fro_norm(m64) if cfg.mu0 is None else cfg.mu0
+    mus, ts, betas = pga_schedule(cfg, mu0)
+    solver = PGASolver(m64, mask, spec, precision)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    k = 1
+    while k <= iters:
+        n = min(50, iters - k + 1)
+        recs, _ = solver.run(k, betas[k - 1:k - 1 + n], mus[k - 1:k - 1 + n], cfg.tol)
+        k += len(recs)
+    dt = time.perf_counter() - t0
+    solver.close()
+    return iters / dt
+
+
+def bench_extras(L, nat, torch, args, cpu):
+    """The other BASELINE configs (parity is in tests/test_gpu_configs.py): config 1 PGA (fp64),
+    config 5 svt / t_svd at n = 128, 256, 512, config 4 PGA at full size (2 iterations)."""
+    import torch as _t
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ltensor_oracle as O
+
+    out = {}
+    # ---- config 1: 64x64x16 f64, DCT, mu == 0.01, 100 iterations
+    rng = np.random.default_rng(0)
+    a1 = rng.standard_normal((64, 5, 16))
+    b1 = rng.standard_normal((5, 64, 16))
+    spec1 = L.make_spec("dct", (64, 64, 16))
+    m1 = L.l_product(a1, b1, spec1)
+    mask1 = rng.random(m1.shape) < 0.5
+    kw1 = dict(mu0=0.01, mu_bar_ratio=1.0)
+    _run_pga(L, nat, torch, m1, mask1, spec1, "fp64", 5, **kw1)  # warm-up
+    c1 = {"metric": "PGA completion iters/sec", "value": _run_pga(L, nat, torch, m1, mask1, spec1, "fp64", 100, **kw1),
+          "unit": "it/s", "dtype": "f64", "config": "config1 64x64x16 DCT, tubal rank 5, Bernoulli(0.5), mu=0.01, 100 it"}
+    if cpu:
+        t0 = time.perf_counter()
+        O.pga_complete(m1, mask1, O.ospec("dct", m1.shape), mu0=0.01, mu_bar_ratio=1.0, tol=1e-300, max_iters=20)
+        c1["cpu_baseline"] = {"value": 20 / (time.perf_counter() - t0), "unit": "it/s", "kind": "port",
+                              "cores": _cpu_info()["blas_threads"], "sample": "20 iterations of config 1 (float64)"}
+    out["config1_pga"] = c1
+    # ---- config 5: n x n x 4 x 8 x 16 f32, DCT^3, svt at tau = 0.1 median sv, t_svd
+    c5 = {}
+    for n in (128, 256, 512):
+        rng = np.random.default_rng(0)
+        a5 = rng.standard_normal((n, n, 4, 8, 16), dtype=np.float32)
+        spec5 = L.make_spec("dct", a5.shape)
+        sv = L.linalg._singular_values(a5, spec5)
+        tau = 0.1 * float(np.median(sv))
+        _t.cuda.synchronize()
+        t0 = time.perf_counter()
+        L.svt(a5, tau, spec5)
+        t_svt = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        L.t_svd(a5, spec5)
+        t_tsvd = time.perf_counter() - t0
+        gflop_svd = 512 * 26 * n ** 3 / 1e9
+        entry = {"svt_s": t_svt, "t_svd_s": t_tsvd, "svt_nominal_gflops": (gflop_svd + 512 * 2 * n ** 3 / 1e9) / t_svt,
+                 "t_svd_nominal_gflops": gflop_svd / t_tsvd, "tau": tau,
+                 "note": "numpy in / numpy out through the public API (host copies included)"}
+        if cpu and n == 128:
+            t0 = time.perf_counter()
+            O.svt(a5, tau, O.ospec("dct", a5.shape))
+            entry["cpu_baseline_svt_s"] = time.perf_counter() - t0
+        c5[f"n{n}"] = entry
+    out["config5"] = c5
+    # ---- config 4: 1024x1024x3x64, explicit Q (x) F64 (complex64 transform domain), Bernoulli(0.3)
+    if not args.skip_config4:
+        rng = np.random.default_rng(0)
+        q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+        a4 = rng.standard_normal((1024, 20, 3, 64), dtype=np.float32)
+        b4 = rng.standard_normal((20, 1024, 3, 64), dtype=np.float32)
+        spec4 = L.make_spec("explicit", (1024, 1024, 3, 64), matrices={3: q, 4: L.build_fourier_matrix(64)})
+        m4 = L.l_product(a4.astype(np.float64), b4.astype(np.float64), spec4)
+        mask4 = rng.random(m4.shape) < 0.3
+        out["config4_pga"] = {"metric": "PGA completion iters/sec",
+                              "value": _run_pga(L, nat, torch, m4.astype(np.float32), mask4, spec4, "fp32", 2),
+                              "unit": "it/s", "dtype": "c64",
+                              "config": "config4 1024x1024x3x64 Q(x)DFT64, rank 20, Bernoulli(0.3); 2 of 50 iterations",
+                              "note": "1024^2 complex slices run the global-workspace Jacobi tier"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--skip-extras", action="store_true")
+    ap.add_argument("--skip-config4", action="store_true")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
