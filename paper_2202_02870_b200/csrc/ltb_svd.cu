@@ -39,19 +39,27 @@ template <> struct eps_of<double> {
   static constexpr double value = DBL_EPSILON;
 };
 
-// round-robin pair k of round r for an even number of players np
-__device__ __forceinline__ void rr_pair(int np, int r, int k, int& p, int& q) {
-  const int m1 = np - 1;
-  if (k == 0) {
-    p = m1;
-    q = r;
-  } else {
-    p = (r + k) % m1;
-    q = (r - k + m1) % m1;
-  }
-}
-
 template <typename R> __device__ __forceinline__ R warp_sum_r(R v) { return warp_sum(v); }
+
+// MUFU approximations for the fp32 rotation parameters.  The rotation stays
+// orthogonal to rounding whatever the accuracy of t (c = (1 + t^2)^-1/2 is
+// refined by one Newton step, s = c t); t itself only decides how completely
+// the pair's Gram entry is annihilated.
+__device__ __forceinline__ float sqrt_apx(float x) {
+  float y;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_apx(float x) {
+  float y;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_apx(float x) {
+  float y;
+  asm("rsqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // two consecutive elements, one vector shared-memory access (LDS.64 / LDS.128)
 template <typename T> struct alignas(2 * sizeof(T)) vec2 {
@@ -149,6 +157,27 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
       if (lane == 0) nrm[j] = s2;
     }
     __syncthreads();
+    if (sweep == 0 && o.tau > 0.0 && !o.sv_out && !o.v_out && !WANT_V) {
+      // SVT-only call: sigma_max <= ||A||_F, so ||A||_F <= tau keeps nothing and the
+      // output slice is exactly zero (the recomposition GEMMs see kept == 0)
+      if (warp == 0) {
+        R s = 0;
+        for (int j = lane; j < n; j += 32) s += nrm[j];
+        s = warp_sum_r(s);
+        if (lane == 0) flags[3] = (s <= (R)o.tau * (R)o.tau) ? 1 : 0;
+      }
+      __syncthreads();
+      if (flags[3]) {
+        R* d_out = reinterpret_cast<R*>(o.d_out);
+        if (d_out)
+          for (int j = tid; j < n; j += nth) d_out[b * n + j] = (R)0;
+        if (tid == 0) {
+          if (o.kept_out) o.kept_out[b] = 0;
+          if (o.stats) atomicAdd(&o.stats[0], 1ull);
+        }
+        return;
+      }
+    }
     for (int r = 0; r < npl - 1; ++r) {
       for (int base = warp * TPW; base < npairs; base += nwarps * TPW) {
         const int k = base + team;
@@ -168,6 +197,58 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
         const bool active = k < npairs && p < n && q < n;
         T* wp = W + (size_t)(active ? p : 0) * mp;
         T* wq = W + (size_t)(active ? q : 0) * mp;
+        if constexpr (std::is_same<T, float>::value && MPL > 0) {
+          // fp32: paired-lane FFMA2/FMUL2 on two rows at a time, MUFU rotation parameters
+          float2 X[MPL / 2], Y[MPL / 2];
+          float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int h = 0; h < MPL / 2; ++h) {
+            const int i = 2 * tl + 2 * TS * h;
+            X[h] = *reinterpret_cast<const float2*>(wp + i);
+            Y[h] = *reinterpret_cast<const float2*>(wq + i);
+            acc = __ffma2_rn(X[h], Y[h], acc);
+          }
+          float g = acc.x + acc.y;
+#pragma unroll
+          for (int o = TS / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+          const float al = active ? nrm[p] : 0.f;
+          const float be = active ? nrm[q] : 0.f;
+          const float gabs = fabsf(g);
+          if (!active || !(gabs > tol * sqrt_apx(al) * sqrt_apx(be)) || al == 0.f || be == 0.f) continue;
+          const float zeta = (be - al) * (0.5f * rcp_apx(gabs));
+          const float az = fabsf(zeta);
+          const float den = az < 1e18f ? az + sqrt_apx(fmaf(az, az, 1.f)) : 2.f * az;
+          const float t = copysignf(rcp_apx(den), zeta);
+          const float x1 = fmaf(t, t, 1.f);
+          float c = rsqrt_apx(x1);
+          c = c * fmaf(-0.5f * x1 * c, c, 1.5f);
+          const float s = c * t;
+          const float sg = g >= 0.f ? 1.f : -1.f;
+          const float2 C2 = make_float2(c, c), S2 = make_float2(s, s);
+          const float2 NSQ = make_float2(-s * sg, -s * sg), CQ = make_float2(c * sg, c * sg);
+#pragma unroll
+          for (int h = 0; h < MPL / 2; ++h) {
+            const int i = 2 * tl + 2 * TS * h;
+            *reinterpret_cast<float2*>(wp + i) = __ffma2_rn(C2, X[h], __fmul2_rn(NSQ, Y[h]));
+            *reinterpret_cast<float2*>(wq + i) = __ffma2_rn(S2, X[h], __fmul2_rn(CQ, Y[h]));
+          }
+          if (WANT_V) {
+            T* vp = V + (size_t)p * np_v;
+            T* vq = V + (size_t)q * np_v;
+            for (int i = tl; i < n; i += TS) {
+              const float x = vp[i];
+              const float y = sg * vq[i];
+              vp[i] = c * x - s * y;
+              vq[i] = s * x + c * y;
+            }
+          }
+          if (tl == 0) {
+            nrm[p] = fmaxf(al - t * gabs, 0.f);
+            nrm[q] = be + t * gabs;
+            *rot = 1;
+          }
+          continue;
+        }
         T ga = zero_v<T>();
         T xr[MPL > 0 ? MPL : 1], yr[MPL > 0 ? MPL : 1];
         if constexpr (MPL > 0) {
