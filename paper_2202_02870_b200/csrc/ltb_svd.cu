@@ -41,23 +41,24 @@ template <> struct eps_of<double> {
 
 template <typename R> __device__ __forceinline__ R warp_sum_r(R v) { return warp_sum(v); }
 
-// MUFU approximations for the fp32 rotation parameters.  The rotation stays
-// orthogonal to rounding whatever the accuracy of t (c = (1 + t^2)^-1/2 is
-// refined by one Newton step, s = c t); t itself only decides how completely
-// the pair's Gram entry is annihilated.
+// MUFU approximations (flush-to-zero) for the fp32 rotation parameters.  The
+// rotation stays orthogonal to rounding whatever the accuracy of t (c = (1 +
+// t^2)^-1/2 is refined by one Newton step, s = c t); t itself only decides how
+// completely the pair's Gram entry is annihilated.  Pairs whose norms or Gram
+// entry are below FLT_MIN are left alone (they cannot move an fp32 result).
 __device__ __forceinline__ float sqrt_apx(float x) {
   float y;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 __device__ __forceinline__ float rcp_apx(float x) {
   float y;
-  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 __device__ __forceinline__ float rsqrt_apx(float x) {
   float y;
-  asm("rsqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
           const float al = active ? nrm[p] : 0.f;
           const float be = active ? nrm[q] : 0.f;
           const float gabs = fabsf(g);
-          if (!active || !(gabs > tol * sqrt_apx(al) * sqrt_apx(be)) || al == 0.f || be == 0.f) continue;
+          if (!active || !(gabs > tol * sqrt_apx(al) * sqrt_apx(be)) || !(fminf(fminf(al, be), gabs) >= FLT_MIN)) continue;
           const float zeta = (be - al) * (0.5f * rcp_apx(gabs));
           const float az = fabsf(zeta);
           const float den = az < 1e18f ? az + sqrt_apx(fmaf(az, az, 1.f)) : 2.f * az;
