@@ -73,6 +73,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -157,15 +170,15 @@ struct TcCfg {
   static constexpr int A_BYTES = kBM * kBK * 4;  // 16 KB
   static constexpr int B_BYTES = BN * kBK * 4;
   static constexpr int STAGE_BYTES = (SPLIT == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
-  static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // per-warp 32x33 transpose buffers
-  static constexpr int SMEM = kStages * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */ + EPI_BYTES;
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;  // per epilogue warp: two 32 x 32 fp32 swizzled store boxes
+  static constexpr int SMEM = kStages * STAGE_BYTES + 1024 /* align */ + 1024 /* barriers */ + EPI_BYTES;
   static_assert(2 * BN <= 512, "two accumulators must fit in TMEM");
 };
 
 template <int BN, bool A_MN, bool B_MN, int SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K, int batches,
+                        const __grid_constant__ CUtensorMap tmC, float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K, int batches,
                         uint32_t mn_lbo, uint32_t mn_sbo, int raw_hi, unsigned long long* dbg, int epi_mode) {
   // optional timeline instrumentation (CTA 0, %globaltimer ns) for the launch-cost analysis
   auto stamp = [&](int slot) {
@@ -314,7 +327,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ---------------------------------------------------------------- epilogue
     const int q = warp - 8;  // TMEM lane quarter of this warp (warps 8-11)
-    float* stage = reinterpret_cast<float*>(base + kStages * Cfg::STAGE_BYTES + 256) + q * 32 * 33;
+    // two 4 KB store boxes per warp (1 KB aligned: 128B-swizzle atoms)
+    unsigned char* ebuf = base + kStages * Cfg::STAGE_BYTES + 1024 + q * 2 * 4096;
+    int nbox = 0;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
       int b, m0, n0;
@@ -326,15 +341,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = m0 + 32 * q;
       float* cb = C + (int64_t)b * sc;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = 0; c0 < BN && n0 + c0 < N; c0 += 32) {
         uint32_t r[32];
         const bool tl = (j == 0 && q == 0 && lane == 0 && c0 < 96);
         if (tl) stamp(8 + 2 * (c0 / 32));
         tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
         if (tl) stamp(9 + 2 * (c0 / 32));
-        // mode 1 (default): each thread stores its row segment with 16-byte vector stores
-        // (measured 2x faster than transposing through smem for row-coalesced stores)
-        if (epi_mode == 1) {
+        if (epi_mode == 3) {
+          // registers -> 128B-swizzled smem box (row = lane, 16-byte chunk jj at jj ^ (lane & 7))
+          // -> one TMA tensor store per warp; the TMA unit clips rows / columns past M / N
+          unsigned char* box = ebuf + (nbox & 1) * 4096;
+          if (lane == 0) bulk_wait_read<1>();  // the store that last used this box has read it
+          __syncwarp();
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((jj ^ (lane & 7)) << 4)) =
+                make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                            __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0 && row0 < M) {
+            tma_store_3d(&tmC, box, n0 + c0, row0, b);
+            bulk_commit();
+          }
+          ++nbox;
+        } else if (epi_mode == 1) {
+          // each thread stores its row segment with 16-byte vector stores
           const int row = row0 + lane;
           if (row < M) {
             float* dst = cb + (int64_t)row * ldc + n0 + c0;
@@ -350,25 +382,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (n0 + c0 + jj < N) dst[jj] = __uint_as_float(r[jj]);
             }
           }
-        } else if (epi_mode == 0) {  // transpose through shared memory, row-coalesced stores
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) stage[lane * 33 + jj] = __uint_as_float(r[jj]);
-          __syncwarp();
-          const int col = n0 + c0 + lane;
-          if (col < N) {
-#pragma unroll 8
-            for (int rr = 0; rr < 32; ++rr) {
-              const int row = row0 + rr;
-              if (row < M) cb[(int64_t)row * ldc + col] = stage[rr * 33 + lane];
-            }
-          }
-          __syncwarp();
         }
       }
       tc_fence_before();
       if (j == 0 && q == 0 && lane == 0) stamp(6);
       mbar_arrive(&acce[a]);  // accumulator a may be overwritten
     }
+    if (lane == 0) bulk_wait_all();  // TMA stores complete before the CTA retires
   }
   tc_fence_before();
   __syncthreads();
@@ -386,9 +406,9 @@ uint32_t g_mn_lbo = 4096, g_mn_sbo = 512;
 // truncates fp32 -> tf32); 0: store hi = x with the low 13 bits cleared
 int g_raw_hi = 1;
 unsigned long long* g_dbg = nullptr;
-// epilogue store mode: 1 direct row stores (default), 0 smem-transposed coalesced stores,
-// 2 no stores (diagnostic only)
-int g_epi_mode = 1;
+// epilogue store mode: 3 swizzled smem boxes + TMA tensor stores (default, needs a
+// C tensor map), 1 direct per-thread row stores, 2 no stores (diagnostic only)
+int g_epi_mode = 3;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -461,8 +481,8 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t rows, i
 }
 
 template <int BN, bool A_MN, bool B_MN, int SPLIT>
-int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t ldc, int64_t sc,
-              int64_t batch, int M, int N, int K) {
+int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, bool have_mc,
+              float* C, int64_t ldc, int64_t sc, int64_t batch, int M, int N, int K) {
   using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
   const uint32_t mn_lbo = g_mn_lbo, mn_sbo = g_mn_sbo;
   auto kern = tc_gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT>;
@@ -470,7 +490,9 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, float*
   // persistent: one CTA per SM, tiles strided over the grid
   const int64_t tiles = batch * (int64_t)((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
-  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo, g_raw_hi, g_dbg, g_epi_mode);
+  const int epi = (g_epi_mode == 3 && !have_mc) ? 1 : g_epi_mode;
+  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, mc, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo,
+                                                    g_raw_hi, g_dbg, epi);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -493,17 +515,21 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
   const int BN = 128;
   const bool okB = b_mn ? make_map(&mb, B, N, K, batch, ldb, sb, kBK, true) : make_map(&mb, B, K, N, batch, ldb, sb, BN);
   if (!okA || !okB) return LTB_EUNSUPPORTED;
+  // C: dims {N, M, batch}, box {32, 32, 1}, 128B swizzle (TMA-store epilogue)
+  CUtensorMap mc;
+  const bool okC = make_map(&mc, C, N, M, batch, ldc, sc, 32);
+  if (!okC) std::memset(&mc, 0, sizeof(mc));
   const int m = (int)M, n = (int)N, k = (int)K;
   if (split == 3) {
-    if (!a_mn && !b_mn) return launch_tc<128, false, false, 3>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
-    if (!a_mn && b_mn) return launch_tc<128, false, true, 3>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
-    if (a_mn && !b_mn) return launch_tc<128, true, false, 3>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
-    return launch_tc<128, true, true, 3>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+    if (!a_mn && !b_mn) return launch_tc<128, false, false, 3>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
+    if (!a_mn && b_mn) return launch_tc<128, false, true, 3>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
+    if (a_mn && !b_mn) return launch_tc<128, true, false, 3>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
+    return launch_tc<128, true, true, 3>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
   }
-  if (!a_mn && !b_mn) return launch_tc<128, false, false, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
-  if (!a_mn && b_mn) return launch_tc<128, false, true, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
-  if (a_mn && !b_mn) return launch_tc<128, true, false, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
-  return launch_tc<128, true, true, 1>(ctx, ma, mb, C, ldc, sc, batch, m, n, k);
+  if (!a_mn && !b_mn) return launch_tc<128, false, false, 1>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
+  if (!a_mn && b_mn) return launch_tc<128, false, true, 1>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
+  if (a_mn && !b_mn) return launch_tc<128, true, false, 1>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
+  return launch_tc<128, true, true, 1>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
 }
 
 extern "C" void ltb_tc_debug_set_raw_hi(int v) { g_raw_hi = v; }
