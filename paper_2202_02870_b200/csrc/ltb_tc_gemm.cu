@@ -234,10 +234,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "n"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  if (threadIdx.x == 32) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (epi_mode == 3) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: everything above overlaps the previous kernel's
+  // tail; operands are read (and C written) only after it has completed.  The next
+  // kernel in the stream may start its own prologue as SMs free up.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0) stamp(1);
 
   if (warp == 0) {
@@ -409,6 +419,8 @@ unsigned long long* g_dbg = nullptr;
 // epilogue store mode: 3 swizzled smem boxes + TMA tensor stores (default, needs a
 // C tensor map), 1 direct per-thread row stores, 2 no stores (diagnostic only)
 int g_epi_mode = 3;
+// programmatic dependent launch on (1) / off (0)
+int g_pdl = 1;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -491,8 +503,18 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const 
   const int64_t tiles = batch * (int64_t)((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
   const int epi = (g_epi_mode == 3 && !have_mc) ? 1 : g_epi_mode;
-  kern<<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(ma, mb, mc, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo,
-                                                    g_raw_hi, g_dbg, epi);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo,
+                                       g_raw_hi, g_dbg, epi));
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -534,6 +556,7 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
 
 extern "C" void ltb_tc_debug_set_raw_hi(int v) { g_raw_hi = v; }
 extern "C" void ltb_tc_debug_set_epi_mode(int v) { g_epi_mode = v; }
+extern "C" void ltb_tc_debug_set_pdl(int v) { g_pdl = v; }
 extern "C" void ltb_tc_debug_set_timeline(void* d_buf) { g_dbg = (unsigned long long*)d_buf; }
 
 extern "C" void ltb_tc_debug_set_mn_strides(uint32_t lbo, uint32_t sbo) {

@@ -207,6 +207,10 @@ int dispatch_io(ltb_ctx* ctx, bool ic, bool oc, bool cm, XformParams p, const vo
 
 }  // namespace
 
+// 0: force the CUDA-core tile engine for fp32 real specs (A/B measurements)
+static int g_xform_tc = 1;
+extern "C" void ltb_debug_set_xform_tc(int v) { g_xform_tc = v; }
+
 int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in, int layout_in,
                        const void* d_in, int dtype_out, int layout_out, void* d_out, double* d_sumsq) {
   if (!spec) return ltb_set_error(ctx, LTB_ETRANSFORM, "null spec");
@@ -229,7 +233,7 @@ int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int i
   // fp32 real specs: the transform as one dense Kronecker GEMM on the tensor
   // cores (tcgen05 kind::tf32, 3xTF32 split), with the tube<->slice layout
   // change folded into the operand / output orientation
-  if (!dbl && !ic && !oc && !cm && spec->d_kron[0] && spec->nmodes > 0 &&
+  if (g_xform_tc && !dbl && !ic && !oc && !cm && spec->d_kron[0] && spec->nmodes > 0 &&
       !(layout_in == LTB_SLICE_MAJOR && layout_out == LTB_SLICE_MAJOR)) {
     const int64_t P = spec->P, NT = ntubes;
     const float* K = spec->d_kron[inverse ? 1 : 0];
