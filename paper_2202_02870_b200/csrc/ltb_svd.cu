@@ -21,8 +21,8 @@
 //        out = sum_{sigma_j > tau} (sigma_j - tau) / sigma_j^2 * w_j (w_j^H A)
 //     as two batched GEMMs whose inner dimension is limited per slice to the
 //     number of surviving singular values (ltb_gemm.cu).
-// Slices that do not fit in shared memory run the same kernel with the
-// working columns in an L2-resident global workspace.
+// Slices that do not fit in shared memory run the block-cyclic tier below
+// (column blocks paired through shared memory, one launch per outer round).
 #include <cfloat>
 
 #include "ltb_dispatch.cuh"
@@ -409,21 +409,26 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
 // ---------------------------------------------------------------- t_svd helpers
 // U (m x m, row-major output with leading dim m) from the sorted working
 // columns: u_j = w_j / sigma_j where sigma_j is numerically nonzero, and a
-// deterministic Gram-Schmidt completion (candidate unit vectors e_0, e_1, ...)
-// for the remaining columns (rank-deficient slices, and the m - n extra
-// columns of full_matrices=True).
+// deterministic Gram-Schmidt completion for the remaining columns
+// (rank-deficient slices, and the m - n extra columns of full_matrices=True).
+// The completion candidate for each new column is the unit vector e_i whose
+// residual (1 - |row i of the columns so far|^2) is largest: that residual
+// is >= (m - slot) / m, so every candidate is accepted (no rejection loop).
 template <typename T>
 __global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
                                   const typename scalar_traits<T>::real* __restrict__ sv, T* __restrict__ U) {
   using R = typename scalar_traits<T>::real;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  R* rn = reinterpret_cast<R*>(smem_raw);  // residual row norms, m entries
   const int64_t b = blockIdx.x;
   const T* Wb = w_sorted + b * (int64_t)n * m;
   const R* sb = sv + b * (int64_t)n;
   T* Ub = U + b * (int64_t)m * m;  // Ub[i * m + j] = column j, row i
   __shared__ R red[32];
+  __shared__ int redi[32];
   __shared__ T redc[32];
   __shared__ int good_count;
-  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
   const R smax = n > 0 ? sb[0] : (R)0;
   const R thr = smax * (R)max(m, 1) * eps_of<R>::value;
   // number of leading good columns (sorted descending, so good ones are a prefix)
@@ -439,13 +444,19 @@ __global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
     Ub[(int64_t)i * m + j] = Wb[(int64_t)j * m + i] * ((R)1 / sb[j]);
   }
   __syncthreads();
+  for (int i = tid; i < m; i += nth) {
+    R acc = 0;
+    for (int j = 0; j < g0; ++j) acc += abs2_v(Ub[(int64_t)i * m + j]);
+    rn[i] = (R)1 - acc;
+  }
+  __syncthreads();
   auto block_sum_r = [&](R v) -> R {
     v = warp_sum(v);
     __syncthreads();
     if (lane == 0) red[warp] = v;
     __syncthreads();
     R s = 0;
-    for (int k = 0; k < (nth >> 5); ++k) s += red[k];
+    for (int k = 0; k < nw; ++k) s += red[k];
     return s;
   };
   auto block_sum_t = [&](T v) -> T {
@@ -461,39 +472,59 @@ __global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
     }
     __syncthreads();
     T s = zero_v<T>();
-    for (int k = 0; k < (nth >> 5); ++k) s = s + redc[k];
+    for (int k = 0; k < nw; ++k) s = s + redc[k];
     return s;
   };
-  int cand = 0;
   for (int slot = g0; slot < m; ++slot) {
-    // the slot's column is built in place in U's column `slot`
-    while (cand < m) {
-      for (int i = tid; i < m; i += nth) Ub[(int64_t)i * m + slot] = (i == cand) ? cvt<T>((R)1) : zero_v<T>();
-      __syncthreads();
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int g = 0; g < slot; ++g) {
-          T part = zero_v<T>();
-          for (int i = tid; i < m; i += nth) fma_acc(part, conj_v(Ub[(int64_t)i * m + g]), Ub[(int64_t)i * m + slot]);
-          const T coef = block_sum_t(part);
-          for (int i = tid; i < m; i += nth) {
-            T v = Ub[(int64_t)i * m + slot];
-            v = v - coef * Ub[(int64_t)i * m + g];
-            Ub[(int64_t)i * m + slot] = v;
-          }
-          __syncthreads();
-        }
+    // pivot: the row with the largest residual (lowest index on ties)
+    R best = -(R)1;
+    int bi = m;
+    for (int i = tid; i < m; i += nth)
+      if (rn[i] > best) {
+        best = rn[i];
+        bi = i;
       }
-      R part = 0;
-      for (int i = tid; i < m; i += nth) part += abs2_v(Ub[(int64_t)i * m + slot]);
-      const R nrm = sqrt(block_sum_r(part));
-      ++cand;
-      if (nrm > (R)0.25) {
-        for (int i = tid; i < m; i += nth) Ub[(int64_t)i * m + slot] = Ub[(int64_t)i * m + slot] * ((R)1 / nrm);
-        __syncthreads();
-        break;
+    for (int o = 16; o > 0; o >>= 1) {
+      const R ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
       }
-      __syncthreads();
     }
+    __syncthreads();
+    if (lane == 0) {
+      red[warp] = best;
+      redi[warp] = bi;
+    }
+    __syncthreads();
+    int cand = redi[0];
+    R cb = red[0];
+    for (int k = 1; k < nw; ++k)
+      if (red[k] > cb || (red[k] == cb && redi[k] < cand)) {
+        cb = red[k];
+        cand = redi[k];
+      }
+    for (int i = tid; i < m; i += nth) Ub[(int64_t)i * m + slot] = (i == cand) ? cvt<T>((R)1) : zero_v<T>();
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int g = 0; g < slot; ++g) {
+        T part = zero_v<T>();
+        for (int i = tid; i < m; i += nth) fma_acc(part, conj_v(Ub[(int64_t)i * m + g]), Ub[(int64_t)i * m + slot]);
+        const T coef = block_sum_t(part);
+        for (int i = tid; i < m; i += nth) Ub[(int64_t)i * m + slot] = Ub[(int64_t)i * m + slot] - coef * Ub[(int64_t)i * m + g];
+        __syncthreads();
+      }
+    }
+    R part = 0;
+    for (int i = tid; i < m; i += nth) part += abs2_v(Ub[(int64_t)i * m + slot]);
+    const R inv = (R)1 / sqrt(block_sum_r(part));
+    for (int i = tid; i < m; i += nth) {
+      const T u = Ub[(int64_t)i * m + slot] * inv;
+      Ub[(int64_t)i * m + slot] = u;
+      rn[i] -= abs2_v(u);
+    }
+    __syncthreads();
   }
 }
 
@@ -547,6 +578,309 @@ int launch_smem(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A,
   return launch_smem_variant<T, WANT_V, TS, MPL, 1>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
 }
 
+// ---------------------------------------------------------------- blocked tier
+// Slices whose working columns do not fit in shared memory (config 4's
+// 1024 x 1024 complex slices, config 5 at n >= 256) run a block-cyclic
+// one-sided Jacobi: the n columns are cut into nb blocks of b; each outer
+// round pairs the blocks by the circle method and one CTA per block pair
+// loads its 2b columns into shared memory, orthogonalises every cross pair
+// (on the first round of a sweep also the pairs inside the two blocks) with
+// the same rotation as the resident kernel, and writes the columns back.
+// A sweep is nb - 1 rounds (every column pair met at least once); a slice is
+// converged after a sweep without rotations.  For t_svd, V rides along as n
+// extra rows of every working column (rotated, never dotted).
+struct BlockGeom {
+  int m, n, mp, b, nb;
+};
+
+constexpr size_t kBlockSmem = 200 * 1024;
+int g_force_blocked = 0;  // test hook: route every slice size through the blocked tier
+
+__global__ void fill_int_kernel(int64_t n, int* __restrict__ p, int v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+template <typename T, bool WANT_V>
+__global__ void block_load_kernel(int64_t I1, int64_t I2, const T* __restrict__ A, T* __restrict__ W, BlockGeom g) {
+  using R = typename scalar_traits<T>::real;
+  const int64_t s = blockIdx.y;
+  const bool trans = I1 < I2;
+  const T* Ab = A + s * I1 * I2;
+  T* Ws = W + s * (int64_t)g.n * g.mp;
+  const int64_t total = (int64_t)g.n * g.mp;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(l / g.mp), i = (int)(l - (int64_t)j * g.mp);
+    T v = zero_v<T>();
+    if (i < g.m) {
+      v = trans ? conj_v(Ab[(int64_t)j * g.m + i]) : Ab[(int64_t)i * g.n + j];
+    } else if (WANT_V && i < g.m + g.n && i - g.m == j) {
+      v = cvt<T>((R)1);
+    }
+    Ws[l] = v;
+  }
+}
+
+template <typename T, bool WANT_V>
+__global__ void __launch_bounds__(1024, 1)
+    jacobi_block_kernel(BlockGeom g, int round, int full, T* __restrict__ W, int* __restrict__ rot,
+                        const int* __restrict__ active, const int* __restrict__ skip) {
+  using R = typename scalar_traits<T>::real;
+  constexpr bool CPLX = scalar_traits<T>::is_complex;
+  if (skip && *skip) return;
+  const int64_t s = blockIdx.y;
+  if (!active[s]) return;
+  // block pair of this round (circle method over an even number of block slots)
+  const int nbp = g.nb + (g.nb & 1), m1 = nbp - 1;
+  const int k = blockIdx.x;
+  int P, Q;
+  if (k == 0) {
+    P = m1;
+    Q = round;
+  } else {
+    P = (round + k) % m1;
+    Q = (round - k + m1) % m1;
+  }
+  // with an odd block count one block per round meets the empty slot: it still
+  // needs its internal pairs on the first round of the sweep
+  const bool pv = P < g.nb, qv = Q < g.nb;
+  if (!(pv && qv) && !(full && (pv || qv))) return;
+  const int b = g.b, mp = g.mp, m = g.m;
+  const int cp0 = P * b, cq0 = Q * b;
+  const int np_ = pv ? min(b, g.n - cp0) : 0, nq_ = qv ? min(b, g.n - cq0) : 0;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* C = reinterpret_cast<T*>(smem_raw);
+  R* nrm = reinterpret_cast<R*>(C + (size_t)2 * b * mp);
+  int* flag = reinterpret_cast<int*>(nrm + 2 * b);
+  T* Ws = W + s * (int64_t)g.n * mp;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+  auto gcol = [&](int l) { return l < b ? cp0 + l : cq0 + (l - b); };
+  auto valid = [&](int l) { return l < b ? l < np_ : (l - b) < nq_; };
+  const int vpc = (int)(mp * sizeof(T) / 16);  // 16-byte vectors per column
+  for (int l = warp; l < 2 * b; l += nwarps) {
+    if (!valid(l)) continue;
+    const int4* src = reinterpret_cast<const int4*>(Ws + (int64_t)gcol(l) * mp);
+    int4* dst = reinterpret_cast<int4*>(C + (size_t)l * mp);
+    for (int v = lane; v < vpc; v += 32) dst[v] = src[v];
+  }
+  if (tid == 0) *flag = 0;
+  __syncthreads();
+  for (int l = warp; l < 2 * b; l += nwarps) {
+    R s2 = 0;
+    if (valid(l)) {
+      const T* c = C + (size_t)l * mp;
+      for (int i = lane; i < m; i += 32) s2 += abs2_v(c[i]);
+    }
+    s2 = warp_sum_r(s2);
+    if (lane == 0) nrm[l] = s2;
+  }
+  __syncthreads();
+  const R tol = eps_of<R>::value * sqrt((R)max(m, 1));
+  const int rows = WANT_V ? m + g.n : m;  // rotated rows (padding rows stay zero)
+  const int nrounds = full ? 2 * b - 1 : b;
+  for (int r = 0; r < nrounds; ++r) {
+    for (int pi = warp; pi < b; pi += nwarps) {
+      int p, q;
+      if (full) {  // every pair of the 2b columns: circle method over 2b slots
+        const int mm = 2 * b - 1;
+        if (pi == 0) {
+          p = mm;
+          q = r;
+        } else {
+          p = (r + pi) % mm;
+          q = (r - pi + mm) % mm;
+        }
+      } else {  // cross pairs only: column pi of block P with column (pi + r) mod b of block Q
+        p = pi;
+        q = b + (pi + r) % b;
+      }
+      if (!valid(p) || !valid(q)) continue;
+      T* x = C + (size_t)p * mp;
+      T* y = C + (size_t)q * mp;
+      T ga = zero_v<T>();
+      for (int i = lane; i < m; i += 32) fma_acc(ga, conj_v(x[i]), y[i]);
+      R gre = warp_sum_r(re_v(ga));
+      R gim = CPLX ? warp_sum_r(im_v(ga)) : (R)0;
+      const R al = nrm[p], be = nrm[q];
+      const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
+      if (!(gabs > tol * sqrt(al) * sqrt(be)) || al == (R)0 || be == (R)0) continue;
+      const R zeta = (be - al) / (2 * gabs);
+      const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
+      const R c = (R)1 / sqrt((R)1 + t * t);
+      const R sn = c * t;
+      T ph;
+      if constexpr (CPLX) {
+        ph = T{gre / gabs, -gim / gabs};
+      } else {
+        ph = (gre >= 0) ? (R)1 : (R)-1;
+      }
+      for (int i = lane; i < rows; i += 32) {
+        const T xv = x[i];
+        const T yv = ph * y[i];
+        x[i] = c * xv - sn * yv;
+        y[i] = sn * xv + c * yv;
+      }
+      if (lane == 0) {
+        nrm[p] = fmax(al - t * gabs, (R)0);
+        nrm[q] = be + t * gabs;
+        *flag = 1;
+      }
+    }
+    __syncthreads();
+  }
+  for (int l = warp; l < 2 * b; l += nwarps) {
+    if (!valid(l)) continue;
+    const int4* src = reinterpret_cast<const int4*>(C + (size_t)l * mp);
+    int4* dst = reinterpret_cast<int4*>(Ws + (int64_t)gcol(l) * mp);
+    for (int v = lane; v < vpc; v += 32) dst[v] = src[v];
+  }
+  if (tid == 0 && *flag) rot[s] = 1;
+}
+
+// after a sweep: a slice without rotations is converged; count the rest
+__global__ void block_sweep_update_kernel(int64_t batch, int* __restrict__ rot, int* __restrict__ active,
+                                          int* __restrict__ count, unsigned long long* stats) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int local = 0;
+  for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
+    const int a = active[s];
+    local += a;  // this slice took part in the sweep
+    active[s] = a && rot[s];
+    rot[s] = 0;
+  }
+  atomicAdd(&cnt, local);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (stats) atomicAdd(&stats[1], (unsigned long long)cnt);
+    int c = 0;
+    for (int64_t s = 0; s < batch; ++s) c += active[s];
+    *count = c;
+  }
+}
+
+// singular values, descending stable ranks and the outputs of JacobiOut
+template <typename T, bool WANT_V>
+__global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, JacobiOut o) {
+  using R = typename scalar_traits<T>::real;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  R* sig = reinterpret_cast<R*>(smem_raw);
+  int* rank_sh = reinterpret_cast<int*>(sig + g.n);
+  int* kept_sh = rank_sh + g.n;
+  const int64_t s = blockIdx.x;
+  const int n = g.n, m = g.m, mp = g.mp;
+  const T* Ws = W + s * (int64_t)n * mp;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+  if (tid == 0) *kept_sh = 0;
+  for (int j = warp; j < n; j += nwarps) {
+    R s2 = 0;
+    for (int i = lane; i < m; i += 32) s2 += abs2_v(Ws[(int64_t)j * mp + i]);
+    s2 = warp_sum_r(s2);
+    if (lane == 0) sig[j] = sqrt(s2);
+  }
+  __syncthreads();
+  R* sv_out = reinterpret_cast<R*>(o.sv_out);
+  R* d_out = reinterpret_cast<R*>(o.d_out);
+  int kept_local = 0;
+  for (int j = tid; j < n; j += nth) {
+    const R sj = sig[j];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) {
+      const R si = sig[i];
+      rank += (si > sj) || (si == sj && i < j);
+    }
+    rank_sh[j] = rank;
+    if (sv_out) sv_out[s * n + rank] = sj;
+    const bool keep = sj > (R)o.tau && sj > (R)0;
+    kept_local += keep;
+    if (d_out) d_out[s * n + rank] = keep ? (((sj - (R)o.tau) / sj) / sj) / sj : (R)0;
+  }
+  if (kept_local) atomicAdd(kept_sh, kept_local);
+  __syncthreads();
+  if (o.kept_out && tid == 0) o.kept_out[s] = *kept_sh;
+  if (o.stats && tid == 0) atomicAdd(&o.stats[0], 1ull);
+  if (o.w_out) {
+    T* dst = reinterpret_cast<T*>(o.w_out) + s * (int64_t)n * m;
+    for (int j = warp; j < n; j += nwarps) {
+      T* dj = dst + (int64_t)rank_sh[j] * m;
+      const T* sj = Ws + (int64_t)j * mp;
+      for (int i = lane; i < m; i += 32) dj[i] = sj[i];
+    }
+  }
+  if (WANT_V && o.v_out) {
+    T* dst = reinterpret_cast<T*>(o.v_out) + s * (int64_t)n * n;
+    for (int j = warp; j < n; j += nwarps) {
+      T* dj = dst + (int64_t)rank_sh[j] * n;
+      const T* sj = Ws + (int64_t)j * mp + m;
+      for (int i = lane; i < n; i += 32) dj[i] = sj[i];
+    }
+  }
+}
+
+template <typename T, bool WANT_V>
+int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, const JacobiOut& o,
+                          int max_sweeps) {
+  using R = typename scalar_traits<T>::real;
+  if (batch > 65535) return ltb_set_error(ctx, LTB_ESHAPE, "svd: batch too large for the blocked tier");
+  BlockGeom g;
+  g.m = (int)std::max(I1, I2);
+  g.n = (int)std::min(I1, I2);
+  const int rows = g.m + (WANT_V ? g.n : 0);
+  const int per16 = 16 / (int)std::min<size_t>(sizeof(T), 16);
+  g.mp = (rows + 31) / 32 * 32;
+  g.mp = (g.mp + per16 - 1) / per16 * per16;
+  const size_t colb = (size_t)g.mp * sizeof(T);
+  const size_t fit = (kBlockSmem - 256) / (2 * colb);
+  if (fit < 1) return ltb_set_error(ctx, LTB_EUNSUPPORTED, "svd: slice columns too long for the blocked tier");
+  g.b = (int)std::min<size_t>(std::min<size_t>(32, (size_t)std::max(1, (g.n + 1) / 2)), fit);
+  g.nb = (g.n + g.b - 1) / g.b;
+  const int nbp = g.nb + (g.nb & 1);
+  T* W = nullptr;
+  int* flags = nullptr;
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * (size_t)batch * g.n * g.mp, (void**)&W));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * (size_t)(2 * batch + 4), (void**)&flags));
+  int* rot = flags;
+  int* active = flags + batch;
+  int* count = flags + 2 * batch;
+  LTB_CUDA_TRY(ctx, cudaMemsetAsync(rot, 0, sizeof(int) * batch, ctx->stream));
+  fill_int_kernel<<<grid_for(batch, 256, 1024), 256, 0, ctx->stream>>>(batch, active, 1);
+  LTB_LAUNCH_CHECK(ctx);
+  {
+    dim3 grid((unsigned)std::min<int64_t>(((int64_t)g.n * g.mp + 255) / 256, 256), (unsigned)batch);
+    block_load_kernel<T, WANT_V><<<grid, 256, 0, ctx->stream>>>(I1, I2, A, W, g);
+    LTB_LAUNCH_CHECK(ctx);
+  }
+  const size_t smem = 2 * colb * g.b + 2 * g.b * sizeof(R) + 16;
+  auto kern = jacobi_block_kernel<T, WANT_V>;
+  LTB_TRY(ensure_smem(ctx, kern, smem));
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(ctx->stream, &cap);
+  const dim3 bgrid((unsigned)(nbp / 2), (unsigned)batch);
+  const int threads = 32 * std::min(g.b, 32);
+  if (g.n > 1) {
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+      for (int r = 0; r < nbp - 1; ++r) {
+        kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip);
+        LTB_LAUNCH_CHECK(ctx);
+      }
+      block_sweep_update_kernel<<<1, 256, 0, ctx->stream>>>(batch, rot, active, count, o.stats);
+      LTB_LAUNCH_CHECK(ctx);
+      if (cap != cudaStreamCaptureStatusNone) continue;  // no host read-back inside a capture
+      LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      if (*reinterpret_cast<int*>(ctx->h_scratch) == 0) break;
+    }
+  }
+  const size_t fsmem = (size_t)g.n * (sizeof(R) + sizeof(int)) + 16;
+  auto fin = block_finalize_kernel<T, WANT_V>;
+  LTB_TRY(ensure_smem(ctx, fin, fsmem));
+  fin<<<(unsigned)batch, 512, fsmem, ctx->stream>>>(g, W, o);
+  LTB_LAUNCH_CHECK(ctx);
+  ltb_ws_free(ctx, W);
+  ltb_ws_free(ctx, flags);
+  return LTB_OK;
+}
+
 template <typename T, bool WANT_V>
 int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, JacobiOut o) {
   using R = typename scalar_traits<T>::real;
@@ -555,6 +889,7 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
   if (batch > 0x7fffffff) return ltb_set_error(ctx, LTB_ESHAPE, "svd: batch too large");
   o.stats = ctx->d_stats;
   constexpr bool big = std::is_same<T, cplx<double>>::value;
+  if (g_force_blocked) return launch_jacobi_blocked<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
   auto fits = [&](int mp) { return jacobi_smem_bytes<T>(m, n, WANT_V, mp) <= kSmemLimit; };
   if (m <= 8 && fits(8)) return launch_smem<T, WANT_V, 4, 2>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   if (m <= 32 && fits(32)) return launch_smem<T, WANT_V, 8, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
@@ -567,21 +902,12 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
     if (m <= 128 && fits(128)) return launch_smem<T, WANT_V, 32, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   }
   if (fits(m | 1)) return launch_smem<T, WANT_V, 32, 0>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
-  // global-workspace tier: the working columns live in an L2-resident buffer
-  const int mp = m | 1;
-  const size_t per = (size_t)n * mp + (WANT_V ? (size_t)n * (n | 1) : 0);
-  T* ws = nullptr;
-  LTB_TRY(ltb_ws_alloc(ctx, per * batch * sizeof(T), (void**)&ws));
-  const size_t smem = (n + 1) * sizeof(R) + (n + 8) * sizeof(int) + 16;
-  auto kern = jacobi_kernel<T, WANT_V, true, 32, 0, 1>;
-  LTB_TRY(ensure_smem(ctx, kern, smem));
-  kern<<<(unsigned)batch, 512, smem, ctx->stream>>>(I1, I2, A, ws, o, max_sweeps, mp);
-  LTB_LAUNCH_CHECK(ctx);
-  ltb_ws_free(ctx, ws);
-  return LTB_OK;
+  return launch_jacobi_blocked<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
 }
 
 }  // namespace
+
+extern "C" void ltb_debug_set_svd_blocked(int v) { g_force_blocked = v; }
 
 // SVT of `batch` row-major I1 x I2 slices: out = U (S - tau)_+ V^H
 int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2, const void* d_a, double tau,
@@ -660,7 +986,8 @@ extern "C" int ltb_slice_svd(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1,
     // U of the oriented problem (m x m) and its V (n x n)
     T* u_dst = trans ? (T*)d_v : (T*)d_u;  // m x m
     T* v_dst = trans ? (T*)d_u : (T*)d_v;  // n x n
-    complete_u_kernel<T><<<(unsigned)batch, 256, 0, ctx->stream>>>(m, n, w, (const R*)d_s, u_dst);
+    LTB_TRY(ensure_smem(ctx, complete_u_kernel<T>, (size_t)m * sizeof(R)));
+    complete_u_kernel<T><<<(unsigned)batch, 256, (size_t)m * sizeof(R), ctx->stream>>>(m, n, w, (const R*)d_s, u_dst);
     LTB_LAUNCH_CHECK(ctx);
     cols_to_rowmajor_kernel<T><<<grid_for(batch * n * n, 256, 4096), 256, 0, ctx->stream>>>(batch, n, vcols, v_dst);
     LTB_LAUNCH_CHECK(ctx);

@@ -80,7 +80,7 @@ def test_slice_svt_and_values(dt, shape):
 
 
 @pytest.mark.parametrize("dt", DTYPES)
-@pytest.mark.parametrize("shape", [(6, 4), (4, 6), (5, 5), (3, 1)])
+@pytest.mark.parametrize("shape", [(6, 4), (4, 6), (5, 5), (3, 1), (120, 40), (40, 120)])
 def test_slice_svd_full(dt, shape):
     rng = np.random.default_rng(9)
     batch = 3
@@ -147,3 +147,69 @@ def test_tc_gemm_tf32(split, a_mn, b_mn, mnk):
     ref = np.matmul(a.astype(np.float64), b.astype(np.float64))
     err = np.linalg.norm(dc.numpy() - ref) / np.linalg.norm(ref)
     assert err < (2e-6 if split == 3 else 2e-3), err
+
+
+# ---- blocked (block-cyclic, shared-memory column pairs) tier: slices beyond the resident tier,
+# and small slices forced through it (odd column counts, a single block pair, n = 1)
+BLOCKED_CASES = [(np.float32, (300, 280)), (np.float64, (240, 260)), (np.complex64, (250, 270)),
+                 (np.complex128, (210, 200))]
+
+
+@pytest.fixture
+def force_blocked():
+    nat.lib().ltb_debug_set_svd_blocked(1)
+    yield
+    nat.lib().ltb_debug_set_svd_blocked(0)
+
+
+def _svt_check(dt, shape, batch=2, seed=11):
+    rng = np.random.default_rng(seed)
+    a = rand(rng, (batch,) + shape, dt)
+    u, s, vh = np.linalg.svd(a.astype(np.complex128 if np.iscomplexobj(a) else np.float64), full_matrices=False)
+    tau = float(np.median(s))
+    ref = np.matmul(u * np.maximum(s - tau, 0)[:, None, :], vh)
+    da = nat.DeviceArray.from_numpy(a)
+    out = nat.DeviceArray(a.shape, dt)
+    nat.check(nat.lib().ltb_slice_svt(nat.context(), nat.dtype_code(dt), batch, shape[0], shape[1], da.ptr, tau,
+                                      out.ptr))
+    assert np.linalg.norm(out.numpy() - ref) / max(np.linalg.norm(ref), 1e-30) < 50 * tol(dt)
+    sv = nat.DeviceArray((batch, min(shape)), nat.real_of(dt))
+    nat.check(nat.lib().ltb_slice_singular_values(nat.context(), nat.dtype_code(dt), batch, shape[0], shape[1],
+                                                  da.ptr, sv.ptr))
+    np.testing.assert_allclose(sv.numpy(), s, rtol=50 * tol(dt), atol=50 * tol(dt) * s.max())
+
+
+def _svd_check(dt, shape, batch=2, seed=12):
+    rng = np.random.default_rng(seed)
+    a = rand(rng, (batch,) + shape, dt)
+    m, n = shape
+    da = nat.DeviceArray.from_numpy(a)
+    u = nat.DeviceArray((batch, m, m), dt)
+    v = nat.DeviceArray((batch, n, n), dt)
+    s = nat.DeviceArray((batch, min(m, n)), nat.real_of(dt))
+    nat.check(nat.lib().ltb_slice_svd(nat.context(), nat.dtype_code(dt), batch, m, n, da.ptr, u.ptr, s.ptr, v.ptr))
+    U, S, V = u.numpy(), s.numpy(), v.numpy()
+    k = min(m, n)
+    sig = np.zeros((batch, m, n))
+    sig[:, np.arange(k), np.arange(k)] = S
+    t = 50 * tol(dt)
+    assert np.linalg.norm(U @ sig @ np.conj(np.swapaxes(V, 1, 2)) - a) / np.linalg.norm(a) < t
+    assert np.abs(np.conj(np.swapaxes(V, 1, 2)) @ V - np.eye(n)).max() < t
+    assert np.all(np.diff(S, axis=1) <= 0)
+
+
+@pytest.mark.parametrize("dt,shape", BLOCKED_CASES)
+def test_blocked_tier_svt_and_values(dt, shape):
+    _svt_check(dt, shape)
+
+
+@pytest.mark.parametrize("dt,shape", [(np.float32, (260, 250)), (np.complex64, (240, 260))])
+def test_blocked_tier_svd_full(dt, shape):
+    _svd_check(dt, shape)
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("shape", [(6, 4), (4, 7), (5, 1), (33, 70), (71, 33), (64, 64), (3, 130)])
+def test_blocked_tier_forced_small(dt, shape, force_blocked):
+    _svt_check(dt, shape, batch=3)
+    _svd_check(dt, shape, batch=3)
