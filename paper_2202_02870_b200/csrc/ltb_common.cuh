@@ -150,7 +150,7 @@ struct ltb_spec {
   int64_t mat_total = 0;
   // real specs with P <= kKronMax: the dense Kronecker matrix of L and of L^{-1}
   // (C-order trailing index), fp32, for the tensor-core transform path
-  float* d_kron[2] = {nullptr, nullptr};
+  float* d_kron[2] = {nullptr, nullptr};  // [P*P raw fp32 | P*P 3xTF32 lo part]
 };
 
 constexpr int64_t kKronMax = 512;
@@ -159,7 +159,7 @@ constexpr int64_t kKronMax = 512;
 // alignment cannot take the tcgen05 path
 int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K, bool a_mn, const float* A,
                     int64_t lda, int64_t sa, bool b_mn, const float* B, int64_t ldb, int64_t sb, float* C,
-                    int64_t ldc, int64_t sc, int split);
+                    int64_t ldc, int64_t sc, int split, bool c_trans = false, const float* b_lo = nullptr);
 
 // ------------------------------------------------------------------ errors
 int ltb_set_error(ltb_ctx* ctx, int code, const char* fmt, ...);

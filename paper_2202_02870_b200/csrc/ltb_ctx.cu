@@ -245,7 +245,23 @@ int ltb_spec_create(ltb_ctx* ctx, int ntrail, const int64_t* trail_dims, int nmo
     const int64_t P = s->P;
     std::vector<int> axis_mode(ntrail, -1);
     for (int k = 0; k < nmodes; ++k) axis_mode[axes[k]] = k;
-    std::vector<float> kron((size_t)P * P);
+    // [K | K_lo]: K_lo = round-to-tf32(K - trunc-to-tf32(K)) from the double
+    // values, the precomputed lo operand of the 3xTF32 split (ltb_tc_gemm.cu)
+    std::vector<float> kron((size_t)2 * P * P);
+    auto tf32_trunc = [](float x) {
+      uint32_t u;
+      std::memcpy(&u, &x, 4);
+      u &= 0xFFFFE000u;
+      std::memcpy(&x, &u, 4);
+      return x;
+    };
+    auto tf32_round = [](float x) {
+      uint32_t u;
+      std::memcpy(&u, &x, 4);
+      u = (u + 0x1000u) & 0xFFFFE000u;
+      std::memcpy(&x, &u, 4);
+      return x;
+    };
     std::vector<int> qi(ntrail), qj(ntrail);
     for (int dir = 0; dir < 2; ++dir) {
       const double* src = dir == 0 ? h_fwd : h_inv;
@@ -269,15 +285,17 @@ int ltb_spec_create(ltb_ctx* ctx, int ntrail, const int64_t* trail_dims, int nmo
               v *= src[s->mat_off[k] + (int64_t)qi[a] * n + qj[a]];
             }
           }
-          kron[(size_t)i * P + j] = (float)v;
+          const float f = (float)v;
+          kron[(size_t)i * P + j] = f;
+          kron[(size_t)(P + i) * P + j] = tf32_round((float)(v - (double)tf32_trunc(f)));
         }
       }
-      if (cudaMalloc(&s->d_kron[dir], sizeof(float) * P * P) != cudaSuccess) {
+      if (cudaMalloc(&s->d_kron[dir], sizeof(float) * 2 * P * P) != cudaSuccess) {
         cudaGetLastError();
         s->d_kron[dir] = nullptr;
         break;
       }
-      cudaMemcpy(s->d_kron[dir], kron.data(), sizeof(float) * P * P, cudaMemcpyHostToDevice);
+      cudaMemcpy(s->d_kron[dir], kron.data(), sizeof(float) * 2 * P * P, cudaMemcpyHostToDevice);
     }
     if (!s->d_kron[0] || !s->d_kron[1]) {
       for (int d = 0; d < 2; ++d)

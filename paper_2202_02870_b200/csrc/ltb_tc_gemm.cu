@@ -165,21 +165,33 @@ __device__ __forceinline__ void split_tile(float4* hi, float4* lo, int ct, int r
 }
 
 // ------------------------------------------------------------------ kernel
-template <int BN, bool A_MN, bool B_MN, int SPLIT>
+// RB ("resident B"): B is one constant matrix (a transform's Kronecker matrix)
+// of at most kRbMaxKt K-blocks, loaded once per CTA together with its
+// precomputed lo part, so the pipeline streams and splits only A.
+constexpr int kRbMaxKt = 4;
+
+template <int BN, bool A_MN, bool B_MN, int SPLIT, bool RB>
 struct TcCfg {
   static constexpr int A_BYTES = kBM * kBK * 4;  // 16 KB
   static constexpr int B_BYTES = BN * kBK * 4;
-  static constexpr int STAGE_BYTES = (SPLIT == 3 ? 2 : 1) * (A_BYTES + B_BYTES);
+  static constexpr int NSPLIT = SPLIT == 3 ? 2 : 1;
+  static constexpr int STAGE_BYTES = RB ? NSPLIT * A_BYTES : NSPLIT * (A_BYTES + B_BYTES);
+  static constexpr int RES_BYTES = RB ? kRbMaxKt * NSPLIT * B_BYTES : 0;
   static constexpr int EPI_BYTES = 4 * 2 * 4096;  // per epilogue warp: two 32 x 32 fp32 swizzled store boxes
-  static constexpr int SMEM = kStages * STAGE_BYTES + 1024 /* align */ + 1024 /* barriers */ + EPI_BYTES;
+  static constexpr int SMEM =
+      kStages * STAGE_BYTES + RES_BYTES + 1024 /* align */ + 1024 /* barriers */ + EPI_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   static_assert(2 * BN <= 512, "two accumulators must fit in TMEM");
+  static_assert(B_BYTES % 1024 == 0 && STAGE_BYTES % 1024 == 0, "1 KB swizzle-atom alignment");
+  static_assert(!RB || !B_MN, "resident B is K-major");
 };
 
-template <int BN, bool A_MN, bool B_MN, int SPLIT>
+template <int BN, bool A_MN, bool B_MN, int SPLIT, bool RB>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ CUtensorMap tmC, float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K, int batches,
-                        uint32_t mn_lbo, uint32_t mn_sbo, int raw_hi, unsigned long long* dbg, int epi_mode) {
+                        const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC,
+                        float* __restrict__ C, int64_t ldc, int64_t sc, int M, int N, int K, int batches,
+                        uint32_t mn_lbo, uint32_t mn_sbo, int raw_hi, unsigned long long* dbg, int epi_mode, int ct) {
   // optional timeline instrumentation (CTA 0, %globaltimer ns) for the launch-cost analysis
   auto stamp = [&](int slot) {
     if (dbg && blockIdx.x == 0) {
@@ -189,21 +201,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
   if (threadIdx.x == 0) stamp(0);
-  using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
+  using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT, RB>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // stage s: [A_hi | B_hi | A_lo | B_lo]
+  // stage s: [A_hi | B_hi | A_lo | B_lo]  (RB: [A_hi | A_lo], B resident after the stages)
+  unsigned char* res = base + kStages * Cfg::STAGE_BYTES;
   auto a_hi = [&](int s) { return base + s * Cfg::STAGE_BYTES; };
-  auto b_hi = [&](int s) { return base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES; };
-  auto a_lo = [&](int s) { return base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES + Cfg::B_BYTES; };
-  auto b_lo = [&](int s) { return base + s * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES + Cfg::B_BYTES; };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kStages * Cfg::STAGE_BYTES);
+  auto a_lo = [&](int s) { return base + s * Cfg::STAGE_BYTES + (RB ? Cfg::A_BYTES : Cfg::A_BYTES + Cfg::B_BYTES); };
+  auto b_hi = [&](int s, int kt) {
+    return RB ? res + kt * Cfg::NSPLIT * Cfg::B_BYTES : base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
+  };
+  auto b_lo = [&](int s, int kt) {
+    return RB ? res + kt * Cfg::NSPLIT * Cfg::B_BYTES + Cfg::B_BYTES
+              : base + s * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES + Cfg::B_BYTES;
+  };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(res + Cfg::RES_BYTES);
   uint64_t* full = bars;                  // TMA landed
   uint64_t* conv = bars + kStages;        // split done
   uint64_t* empty = bars + 2 * kStages;   // MMA consumed the stage
   uint64_t* accf = bars + 3 * kStages;    // [2] accumulator ready
   uint64_t* acce = bars + 3 * kStages + 2;  // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 4);
+  uint64_t* bres = bars + 3 * kStages + 4;  // resident B landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 5);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (K + kBK - 1) / kBK;
@@ -227,16 +246,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&accf[a], 1);
       mbar_init(&acce[a], 128);
     }
+    mbar_init(bres, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // TMEM: two BN-column fp32 accumulators (128 lanes)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(2 * BN));
+                 "n"(Cfg::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 32) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (RB && SPLIT == 3) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
     if (epi_mode == 3) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
   }
   tc_fence_before();
@@ -253,6 +274,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
+      if constexpr (RB) {  // the constant B (hi and precomputed lo), once per CTA
+        mbar_expect_tx(bres, ktiles * Cfg::NSPLIT * Cfg::B_BYTES);
+        for (int kt = 0; kt < ktiles; ++kt) {
+          tma_load_3d(b_hi(0, kt), &tmB, bres, kt * kBK, 0, 0);
+          if (SPLIT == 3) tma_load_3d(b_lo(0, kt), &tmBlo, bres, kt * kBK, 0, 0);
+        }
+      }
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int b, m0, n0;
@@ -261,17 +289,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           if (it == 0) stamp(2);
-          mbar_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
+          mbar_expect_tx(&full[s], RB ? Cfg::A_BYTES : Cfg::A_BYTES + Cfg::B_BYTES);
           const int k0 = kt * kBK;
           if (!A_MN) {
             tma_load_3d(a_hi(s), &tmA, &full[s], k0, m0, b);
           } else {
             for (int c = 0; c < kBM / 32; ++c) tma_load_3d(a_hi(s) + c * 4096, &tmA, &full[s], m0 + 32 * c, k0, b);
           }
-          if (!B_MN) {
-            tma_load_3d(b_hi(s), &tmB, &full[s], k0, n0, b);
-          } else {
-            for (int c = 0; c < BN / 32; ++c) tma_load_3d(b_hi(s) + c * 4096, &tmB, &full[s], n0 + 32 * c, k0, b);
+          if constexpr (!RB) {
+            if (!B_MN) {
+              tma_load_3d(b_hi(s, kt), &tmB, &full[s], k0, n0, b);
+            } else {
+              for (int c = 0; c < BN / 32; ++c)
+                tma_load_3d(b_hi(s, kt) + c * 4096, &tmB, &full[s], n0 + 32 * c, k0, b);
+            }
           }
         }
       }
@@ -282,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lboA = A_MN ? mn_lbo : 16u, lboB = B_MN ? mn_lbo : 16u;
     const uint32_t sboA = A_MN ? mn_sbo : 1024u, sboB = B_MN ? mn_sbo : 1024u;
     int it = 0, j = 0;
+    if (RB) mbar_wait(bres, 0);
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
       const int a = j & 1;
       mbar_wait(&acce[a], ((j >> 1) & 1) ^ 1);  // epilogue drained this accumulator
@@ -298,12 +330,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t koff = (A_MN ? 1024u : 32u) * kk;
             const uint32_t kofb = (B_MN ? 1024u : 32u) * kk;
             const uint64_t dah = umma_desc(smem_u32(a_hi(s)) + koff, lboA, sboA, A_MN);
-            const uint64_t dbh = umma_desc(smem_u32(b_hi(s)) + kofb, lboB, sboB, B_MN);
+            const uint64_t dbh = umma_desc(smem_u32(b_hi(s, kt)) + kofb, lboB, sboB, B_MN);
             const uint32_t accum = (kt > 0 || kk > 0) ? 1u : 0u;
             umma_tf32(dacc, dah, dbh, idesc, accum);
             if constexpr (SPLIT == 3) {
               const uint64_t dal = umma_desc(smem_u32(a_lo(s)) + koff, lboA, sboA, A_MN);
-              const uint64_t dbl = umma_desc(smem_u32(b_lo(s)) + kofb, lboB, sboB, B_MN);
+              const uint64_t dbl = umma_desc(smem_u32(b_lo(s, kt)) + kofb, lboB, sboB, B_MN);
               umma_tf32(dacc, dah, dbl, idesc, 1u);
               umma_tf32(dacc, dal, dbh, idesc, 1u);
             }
@@ -318,18 +350,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < 8) {
     // ---------------------------------------------------------------- 3xTF32 split
     if constexpr (SPLIT == 3) {
-      const int ct = threadIdx.x - 64;  // 0 .. kConv-1
+      const int cv = threadIdx.x - 64;  // 0 .. kConv-1
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
-          split_tile<Cfg::A_BYTES / 16>(reinterpret_cast<float4*>(a_hi(s)), reinterpret_cast<float4*>(a_lo(s)), ct,
+          split_tile<Cfg::A_BYTES / 16>(reinterpret_cast<float4*>(a_hi(s)), reinterpret_cast<float4*>(a_lo(s)), cv,
                                         raw_hi);
-          split_tile<Cfg::B_BYTES / 16>(reinterpret_cast<float4*>(b_hi(s)), reinterpret_cast<float4*>(b_lo(s)), ct,
-                                        raw_hi);
+          if constexpr (!RB)
+            split_tile<Cfg::B_BYTES / 16>(reinterpret_cast<float4*>(b_hi(s, kt)),
+                                          reinterpret_cast<float4*>(b_lo(s, kt)), cv, raw_hi);
           fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
-          if (it == 0 && ct == 0) stamp(3);
+          if (it == 0 && cv == 0) stamp(3);
           mbar_arrive(&conv[s]);
         }
       }
@@ -338,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------------------------------------------------------- epilogue
     const int q = warp - 8;  // TMEM lane quarter of this warp (warps 8-11)
     // two 4 KB store boxes per warp (1 KB aligned: 128B-swizzle atoms)
-    unsigned char* ebuf = base + kStages * Cfg::STAGE_BYTES + 1024 + q * 2 * 4096;
+    unsigned char* ebuf = res + Cfg::RES_BYTES + 1024 + q * 2 * 4096;
     int nbox = 0;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
@@ -363,15 +396,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           unsigned char* box = ebuf + (nbox & 1) * 4096;
           if (lane == 0) bulk_wait_read<1>();  // the store that last used this box has read it
           __syncwarp();
+          if (!ct) {
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            *reinterpret_cast<float4*>(box + lane * 128 + ((jj ^ (lane & 7)) << 4)) =
-                make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
-                            __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
+            for (int jj = 0; jj < 8; ++jj)
+              *reinterpret_cast<float4*>(box + lane * 128 + ((jj ^ (lane & 7)) << 4)) =
+                  make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                              __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
+          } else {  // C^T: box row = output column, 32 consecutive M-rows (lanes) per box row
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              *reinterpret_cast<float*>(box + jj * 128 + (((lane >> 2) ^ (jj & 7)) << 4) + ((lane & 3) << 2)) =
+                  __uint_as_float(r[jj]);
+          }
           fence_proxy_async();
           __syncwarp();
           if (lane == 0 && row0 < M) {
-            tma_store_3d(&tmC, box, n0 + c0, row0, b);
+            if (!ct)
+              tma_store_3d(&tmC, box, n0 + c0, row0, b);
+            else
+              tma_store_3d(&tmC, box, row0, n0 + c0, b);
             bulk_commit();
           }
           ++nbox;
@@ -405,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     if (lane == 0) stamp(7);
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
   }
 }
 
@@ -421,6 +464,8 @@ unsigned long long* g_dbg = nullptr;
 int g_epi_mode = 3;
 // programmatic dependent launch on (1) / off (0)
 int g_pdl = 1;
+// resident constant-B variant allowed (1) / off (0)
+int g_rb = 1;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -492,12 +537,13 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t rows, i
   return ok;
 }
 
-template <int BN, bool A_MN, bool B_MN, int SPLIT>
-int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, bool have_mc,
-              float* C, int64_t ldc, int64_t sc, int64_t batch, int M, int N, int K) {
-  using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT>;
+template <int BN, bool A_MN, bool B_MN, int SPLIT, bool RB>
+int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mblo,
+              const CUtensorMap& mc, bool have_mc, int ct, float* C, int64_t ldc, int64_t sc, int64_t batch, int M,
+              int N, int K) {
+  using Cfg = TcCfg<BN, A_MN, B_MN, SPLIT, RB>;
   const uint32_t mn_lbo = g_mn_lbo, mn_sbo = g_mn_sbo;
-  auto kern = tc_gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT>;
+  auto kern = tc_gemm_tf32_kernel<BN, A_MN, B_MN, SPLIT, RB>;
   LTB_TRY(ensure_smem(ctx, kern, Cfg::SMEM));
   // persistent: one CTA per SM, tiles strided over the grid
   const int64_t tiles = batch * (int64_t)((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
@@ -513,8 +559,8 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const 
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo,
-                                       g_raw_hi, g_dbg, epi));
+  LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, mc, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo,
+                                       g_raw_hi, g_dbg, epi, ct));
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -523,40 +569,56 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const 
 
 // C[b] = op(A[b]) op(B[b]) in fp32 on tcgen05 (3xTF32 when split == 3).
 // a_mn: A stored K x M (else M x K); b_mn: B stored K x N (else N x K).
+// c_trans: write C^T (C stored N x M with leading dimension ldc) instead of C.
+// b_lo: optional precomputed lo part of a constant K-major B (batch 1): with
+// N <= 96 and K <= 128 B then stays resident in shared memory for the whole
+// launch (the transform's Kronecker matrix) and only A is split on the fly.
 // Returns LTB_EUNSUPPORTED (no error text) when the shape / alignment / driver
 // cannot use the tensor-core path; the caller then falls back.
 int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K, bool a_mn, const float* A,
                     int64_t lda, int64_t sa, bool b_mn, const float* B, int64_t ldb, int64_t sb, float* C,
-                    int64_t ldc, int64_t sc, int split) {
+                    int64_t ldc, int64_t sc, int split, bool c_trans, const float* b_lo) {
   if (batch < 1 || M < 1 || N < 1 || K < 1 || batch > 65535) return LTB_EUNSUPPORTED;
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return LTB_EUNSUPPORTED;
   if ((M + kBM - 1) / kBM > 65535) return LTB_EUNSUPPORTED;
-  CUtensorMap ma, mb;
+  const bool rb = b_lo && g_rb && split == 3 && !b_mn && (batch == 1 || sb == 0) && N <= 96 &&
+                  K <= kRbMaxKt * kBK;
+  const int BN = rb ? 96 : 128;
+  CUtensorMap ma, mb, mblo;
   // A: K-major -> dims {K, M}, box {32, 128};  MN-major -> dims {M, K}, box {32 (M), 32 (K)}
   const bool okA = a_mn ? make_map(&ma, A, M, K, batch, lda, sa, kBK, true) : make_map(&ma, A, K, M, batch, lda, sa, kBM);
-  const int BN = 128;
   const bool okB = b_mn ? make_map(&mb, B, N, K, batch, ldb, sb, kBK, true) : make_map(&mb, B, K, N, batch, ldb, sb, BN);
-  if (!okA || !okB) return LTB_EUNSUPPORTED;
-  // C: dims {N, M, batch}, box {32, 32, 1}, 128B swizzle (TMA-store epilogue)
+  const bool okBlo = rb ? make_map(&mblo, b_lo, K, N, 1, ldb, 0, BN) : true;
+  if (!rb) std::memset(&mblo, 0, sizeof(mblo));
+  if (!okA || !okB || !okBlo) return LTB_EUNSUPPORTED;
+  // C: dims {N, M, batch} (C^T: {M, N, batch}), box {32, 32, 1}, 128B swizzle (TMA-store epilogue)
   CUtensorMap mc;
-  const bool okC = make_map(&mc, C, N, M, batch, ldc, sc, 32);
-  if (!okC) std::memset(&mc, 0, sizeof(mc));
-  const int m = (int)M, n = (int)N, k = (int)K;
-  if (split == 3) {
-    if (!a_mn && !b_mn) return launch_tc<128, false, false, 3>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
-    if (!a_mn && b_mn) return launch_tc<128, false, true, 3>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
-    if (a_mn && !b_mn) return launch_tc<128, true, false, 3>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
-    return launch_tc<128, true, true, 3>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
+  const bool okC = c_trans ? make_map(&mc, C, M, N, batch, ldc, sc, 32) : make_map(&mc, C, N, M, batch, ldc, sc, 32);
+  if (!okC) {
+    if (c_trans) return LTB_EUNSUPPORTED;  // the transposed store needs the TMA epilogue
+    std::memset(&mc, 0, sizeof(mc));
   }
-  if (!a_mn && !b_mn) return launch_tc<128, false, false, 1>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
-  if (!a_mn && b_mn) return launch_tc<128, false, true, 1>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
-  if (a_mn && !b_mn) return launch_tc<128, true, false, 1>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
-  return launch_tc<128, true, true, 1>(ctx, ma, mb, mc, okC, C, ldc, sc, batch, m, n, k);
+  const int m = (int)M, n = (int)N, k = (int)K, ct = c_trans ? 1 : 0;
+#define LTB_TC(BNv, AM, BM_, SP, RBv) \
+  launch_tc<BNv, AM, BM_, SP, RBv>(ctx, ma, mb, mblo, mc, okC, ct, C, ldc, sc, batch, m, n, k)
+  if (rb) return a_mn ? LTB_TC(96, true, false, 3, true) : LTB_TC(96, false, false, 3, true);
+  if (split == 3) {
+    if (!a_mn && !b_mn) return LTB_TC(128, false, false, 3, false);
+    if (!a_mn && b_mn) return LTB_TC(128, false, true, 3, false);
+    if (a_mn && !b_mn) return LTB_TC(128, true, false, 3, false);
+    return LTB_TC(128, true, true, 3, false);
+  }
+  if (!a_mn && !b_mn) return LTB_TC(128, false, false, 1, false);
+  if (!a_mn && b_mn) return LTB_TC(128, false, true, 1, false);
+  if (a_mn && !b_mn) return LTB_TC(128, true, false, 1, false);
+  return LTB_TC(128, true, true, 1, false);
+#undef LTB_TC
 }
 
 extern "C" void ltb_tc_debug_set_raw_hi(int v) { g_raw_hi = v; }
 extern "C" void ltb_tc_debug_set_epi_mode(int v) { g_epi_mode = v; }
 extern "C" void ltb_tc_debug_set_pdl(int v) { g_pdl = v; }
+extern "C" void ltb_tc_debug_set_rb(int v) { g_rb = v; }
 extern "C" void ltb_tc_debug_set_timeline(void* d_buf) { g_dbg = (unsigned long long*)d_buf; }
 
 extern "C" void ltb_tc_debug_set_mn_strides(uint32_t lbo, uint32_t sbo) {
@@ -569,7 +631,7 @@ extern "C" int ltb_tc_gemm(ltb_ctx* ctx, int64_t batch, int64_t m, int64_t n, in
                            int64_t lda, int64_t sa, int b_mn, const void* d_b, int64_t ldb, int64_t sb, void* d_c,
                            int64_t ldc, int64_t sc, int split) {
   int st = ltb_tc_gemm_f32(ctx, batch, m, n, k, a_mn != 0, (const float*)d_a, lda, sa, b_mn != 0, (const float*)d_b,
-                           ldb, sb, (float*)d_c, ldc, sc, split);
+                           ldb, sb, (float*)d_c, ldc, sc, split, false, nullptr);
   if (st == LTB_EUNSUPPORTED) return ltb_set_error(ctx, LTB_EUNSUPPORTED, "tc_gemm: shape/alignment unsupported");
   return st;
 }

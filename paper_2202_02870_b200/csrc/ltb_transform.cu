@@ -237,15 +237,18 @@ int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int i
       !(layout_in == LTB_SLICE_MAJOR && layout_out == LTB_SLICE_MAJOR)) {
     const int64_t P = spec->P, NT = ntubes;
     const float* K = spec->d_kron[inverse ? 1 : 0];
+    const float* Klo = K + P * P;  // precomputed 3xTF32 lo part (ltb_ctx.cu)
     const float* X = (const float*)d_in;
     float* Y = (float*)d_out;
     int st;
-    if (layout_in == LTB_TUBE_MAJOR && layout_out == LTB_SLICE_MAJOR)  // Y(P x NT) = K * X^T
-      st = ltb_tc_gemm_f32(ctx, 1, P, NT, P, false, K, P, 0, false, X, P, 0, Y, NT, 0, 3);
-    else if (layout_in == LTB_SLICE_MAJOR)  // Y(NT x P) = X^T(NT x P) * K^T, X stored P x NT
-      st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, true, X, NT, 0, false, K, P, 0, Y, P, 0, 3);
-    else  // tube -> tube: Y(NT x P) = X * K^T
-      st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, false, X, P, 0, false, K, P, 0, Y, P, 0, 3);
+    // every orientation is D(NT x P) = X(NT x P) * K^T with tubes on the 128-row MMA side
+    // and K (constant, pre-split) resident in shared memory when P <= 96
+    if (layout_in == LTB_TUBE_MAJOR && layout_out == LTB_SLICE_MAJOR)  // Y(P x NT) = D^T
+      st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, false, X, P, 0, false, K, P, 0, Y, NT, 0, 3, true, Klo);
+    else if (layout_in == LTB_SLICE_MAJOR)  // X stored P x NT (MN-major A), Y(NT x P) = D
+      st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, true, X, NT, 0, false, K, P, 0, Y, P, 0, 3, false, Klo);
+    else  // tube -> tube: Y(NT x P) = D
+      st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, false, X, P, 0, false, K, P, 0, Y, P, 0, 3, false, Klo);
     if (st != LTB_EUNSUPPORTED) {
       if (st == LTB_OK && d_sumsq) LTB_CUDA_TRY(ctx, cudaMemsetAsync(d_sumsq, 0, 2 * sizeof(double), ctx->stream));
       return st;

@@ -213,3 +213,30 @@ def test_blocked_tier_svd_full(dt, shape):
 def test_blocked_tier_forced_small(dt, shape, force_blocked):
     _svt_check(dt, shape, batch=3)
     _svd_check(dt, shape, batch=3)
+
+
+# ---- the tensor-core transform (dense Kronecker GEMM, resident pre-split K when P <= 96) in every
+# layout orientation, against the CPU oracle's mode products (fp32 tolerance 1e-4 rel. Frobenius)
+@pytest.mark.parametrize("trail", [(3, 2), (5, 8), (3, 32), (4, 25)])
+@pytest.mark.parametrize("nt", [1, 130, 1000])
+def test_tc_transform_layouts(trail, nt):
+    import ltensor_oracle as O
+    from paper_2202_02870_b200 import transforms as TR
+    import paper_2202_02870_b200 as L
+
+    rng = np.random.default_rng(len(trail) * 1000 + nt)
+    shape = (nt, 1) + trail
+    x = rng.standard_normal(shape).astype(np.float32)
+    spec = L.make_spec("dct", shape)
+    ref = O.forward(x.astype(np.float64), O.ospec("dct", shape)).reshape(nt, -1)  # tube-major (t, q)
+    P = ref.shape[1]
+    handle = TR.device_spec(spec, trail)
+    dx = nat.DeviceArray.from_numpy(x.reshape(nt, P))
+    for lo, shp, want in ((nat.TUBE_MAJOR, (nt, P), ref), (nat.SLICE_MAJOR, (P, nt), ref.T)):
+        out, _ = TR.transform_device(dx, handle, nt, False, nat.TUBE_MAJOR, np.float32, lo, shp)
+        got = out.numpy()
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-5
+    # inverse from slice-major input back to tube-major
+    hat = nat.DeviceArray.from_numpy(np.ascontiguousarray(ref.T.astype(np.float32)))
+    back, _ = TR.transform_device(hat, handle, nt, True, nat.SLICE_MAJOR, np.float32, nat.TUBE_MAJOR, (nt, P))
+    assert np.linalg.norm(back.numpy() - x.reshape(nt, P)) / np.linalg.norm(x) < 1e-5
