@@ -309,7 +309,6 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-    phase_ms = np.zeros(4)
     step_ms = []
     # the step (K1(A), K1(B), K2, K1') is captured once as ONE CUDA graph and
     # replayed (no per-kernel host enqueue cost; kernels run back to back); each
@@ -323,18 +322,32 @@ def run_ours(args):
     with torch.cuda.graph(full, stream=stream):
         plan.run(a, b, c)
     launches_per_step = nat.launch_count() - l0
+    # per-phase graphs (K1 of A and B is one launch when the plan pairs them)
+    E_a, E_b, E_c = 256 * 128 * 96, 128 * 256 * 96, 256 * 256 * 96
+    phase_defs = {0: ("transform_fwd_A", 8 * E_a, 70 * E_a, "one f32 read + one write of A"),
+                  1: ("transform_fwd_B", 8 * E_b, 70 * E_b, "one f32 read + one write of B"),
+                  2: ("slice_gemm", 4 * (E_a + E_b + E_c), 2 * 256 * 128 * 256 * 96,
+                      "f32 reads of A-hat, B-hat and the write of C-hat"),
+                  3: ("transform_inv_C", 8 * E_c, 70 * E_c, "one f32 read + one write of C")}
+    if plan.paired:
+        phase_defs[0] = ("transform_fwd_AB", 8 * (E_a + E_b), 70 * (E_a + E_b),
+                         "one f32 read + one write of A and of B (one launch)")
+        del phase_defs[1]
+    phase_ids = sorted(phase_defs)
     graphs = []
-    for ph in range(4):
+    for ph in phase_ids:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             plan.run(a, b, c, phases=(ph,))
         graphs.append(g)
+    nph = len(graphs)
+    phase_ms = np.zeros(nph)
 
     def phases(marks):
-        for ph, g in enumerate(graphs):
-            marks(ph)
+        for i, g in enumerate(graphs):
+            marks(i)
             g.replay()
-        marks(4)
+        marks(nph)
 
     with ClockSampler(local) as clocks:
         for _ in range(args.warmup):
@@ -352,8 +365,8 @@ def run_ours(args):
         for _ in range(args.steps):
             flush.zero_()
             phases(lambda i: ev[i].record(stream))
-            ev[4].synchronize()
-            phase_ms += [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
+            ev[nph].synchronize()
+            phase_ms += [ev[i].elapsed_time(ev[i + 1]) for i in range(nph)]
         launches = launches_per_step * args.steps
         # e2e: public numpy-in/numpy-out API, host copies inside the timed region
         e2e_t = []
@@ -381,14 +394,12 @@ def run_ours(args):
     e2e_value = ws * GFLOP_CFG2 * len(e2e_t) / e2e_total / 1e9
 
     # roofline of the dominant kernel of the step (per-phase CUDA events on the launching stream)
-    names = ["transform_fwd_A", "transform_fwd_B", "slice_gemm", "transform_inv_C"]
+    names = [phase_defs[i][0] for i in phase_ids]
+    alg_bytes = [phase_defs[i][1] for i in phase_ids]
+    alg_flops = [phase_defs[i][2] for i in phase_ids]
+    alg_desc = [phase_defs[i][3] for i in phase_ids]
     phase_avg = phase_ms / args.steps
     dom = int(np.argmax(phase_avg))
-    E_a, E_b, E_c = 256 * 128 * 96, 128 * 256 * 96, 256 * 256 * 96
-    alg_bytes = [8 * E_a, 8 * E_b, 4 * (E_a + E_b + E_c), 8 * E_c]
-    alg_flops = [70 * E_a, 70 * E_b, 2 * 256 * 128 * 256 * 96, 70 * E_c]
-    alg_desc = ["one f32 read + one write of A", "one f32 read + one write of B",
-                "f32 reads of A-hat, B-hat and the write of C-hat", "one f32 read + one write of C"]
     # each phase's roofline is the binding resource at its arithmetic intensity:
     # t_min = max(flop / tensor peak, bytes / HBM peak)
     t_flop = alg_flops[dom] / (tf_peak * 1e12)

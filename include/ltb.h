@@ -112,6 +112,15 @@ int ltb_transform(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int invers
                   int dtype_in, int layout_in, const void* d_in,
                   int dtype_out, int layout_out, void* d_out, double* h_sumsq);
 
+/* K1 of both l_product operands (linalg.py:34-43: apply_l(a), apply_l(b)) in one
+ * call: two tensors with the same tube count and dtypes, each transformed as by
+ * ltb_transform (no real-output check).  On the tensor-core path the pair is
+ * one launch (batch of two), so the fixed launch / pipeline-fill cost is paid
+ * once. */
+int ltb_transform_pair(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse,
+                       int dtype_in, int layout_in, const void* d_in0, const void* d_in1,
+                       int dtype_out, int layout_out, void* d_out0, void* d_out1);
+
 /* mode_n_product (core.py:110-122) on a C-order view (outer, nin, inner):
  * y[o, i, l] = sum_j mat[i, j] x[o, j, l], mat nout x nin row-major (dtype_mat). */
 int ltb_mode_product(ltb_ctx* ctx, int64_t outer, int64_t nin, int64_t inner, int64_t nout,

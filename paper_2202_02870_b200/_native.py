@@ -55,6 +55,7 @@ _SIGNATURES = {
     "ltb_spec_create": ([_vp, _int, C.POINTER(_i64), _int, _ip, _int, _dp, _dp, C.POINTER(_vp)], _int),
     "ltb_spec_destroy": ([_vp], None),
     "ltb_transform": ([_vp, _vp, _i64, _int, _int, _int, _vp, _int, _int, _vp, _dp], _int),
+    "ltb_transform_pair": ([_vp, _vp, _i64, _int, _int, _int, _vp, _vp, _int, _int, _vp, _vp], _int),
     "ltb_mode_product": ([_vp, _i64, _i64, _i64, _i64, _int, _vp, _int, _vp, _int, _vp], _int),
     "ltb_slice_gemm": ([_vp, _int, _i64, _i64, _i64, _i64, _int, _vp, _i64, _i64, _int, _vp, _i64, _i64,
                         _vp, _i64, _i64], _int),

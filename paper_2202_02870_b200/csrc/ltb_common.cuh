@@ -220,6 +220,9 @@ void ltb_ws_free(ltb_ctx* ctx, void* p);
 int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,
                        int layout_in, const void* d_in, int dtype_out, int layout_out, void* d_out,
                        double* d_sumsq /* device, 2 doubles, may be null */);
+int ltb_transform_pair_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,
+                            int layout_in, const void* d_in0, const void* d_in1, int dtype_out, int layout_out,
+                            void* d_out0, void* d_out1);
 int ltb_reduce_sumsq_dev(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y,
                          double* d_out /* 2 doubles */);
 int ltb_gemm_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int op_a,

@@ -336,6 +336,13 @@ int ltb_transform(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int invers
   return LTB_OK;
 }
 
+int ltb_transform_pair(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in, int layout_in,
+                       const void* d_in0, const void* d_in1, int dtype_out, int layout_out, void* d_out0,
+                       void* d_out1) {
+  return ltb_transform_pair_impl(ctx, spec, ntubes, inverse, dtype_in, layout_in, d_in0, d_in1, dtype_out,
+                                 layout_out, d_out0, d_out1);
+}
+
 int ltb_slice_gemm(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int op_a,
                    const void* d_a, int64_t lda, int64_t stride_a, int op_b, const void* d_b, int64_t ldb,
                    int64_t stride_b, void* d_c, int64_t ldc, int64_t stride_c) {

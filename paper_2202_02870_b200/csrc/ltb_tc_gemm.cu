@@ -452,6 +452,308 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ 3xTF32 with A in TMEM
+// The split operands of A never touch shared memory twice: four converter
+// warps (one per TMEM lane quarter) read their rows of the raw TMA tile once,
+// and write hi = trunc(x) and lo = round(x - hi) straight into tensor memory
+// with tcgen05.st; the three MMAs per K=8 step then take A from TMEM
+// (tcgen05.mma ... [a_tmem], b_desc), so shared memory carries only the TMA
+// writes, one converter read of A, and the B operand reads.  For a K-major A
+// the TMA tile keeps the 128B swizzle (conflict-free row reads); an MN-major A
+// (slice-major transform input) is fetched unswizzled as [k][32 rows] boxes,
+// read down the rows.  B is split in shared memory by two more warps, or is a
+// resident constant with a precomputed lo part (RB).
+constexpr int kSt3 = 4;                   // pipeline stages
+constexpr int kConvA = 128, kConvB = 64;  // converter threads (warps 2-5 for A, 6-7 for B)
+
+template <int BN, bool A_MN, bool B_MN, bool RB>
+struct Tc3Cfg {
+  static constexpr int A_BYTES = kBM * kBK * 4;  // 16 KB raw A tile
+  static constexpr int B_BYTES = BN * kBK * 4;
+  static constexpr int STAGE_BYTES = RB ? A_BYTES : A_BYTES + 2 * B_BYTES;  // [A | B_hi | B_lo]
+  static constexpr int RES_BYTES = RB ? kRbMaxKt * 2 * B_BYTES : 0;
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;
+  static constexpr int SMEM = kSt3 * STAGE_BYTES + RES_BYTES + 1024 + 1024 + EPI_BYTES;
+  static constexpr int ACOL = 2 * BN;  // TMEM column of the first A stage (after two accumulators)
+  static_assert(ACOL + kSt3 * 64 <= 512, "accumulators + A stages must fit in TMEM");
+  static_assert(B_BYTES % 1024 == 0 && STAGE_BYTES % 1024 == 0, "1 KB swizzle-atom alignment");
+  static_assert(!RB || !B_MN, "resident B is K-major");
+};
+
+__device__ __forceinline__ void umma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+template <int BN, bool A_MN, bool B_MN, bool RB>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC, int M, int N,
+               int K, int batches, uint32_t mn_lbo, uint32_t mn_sbo, int ct) {
+  using Cfg = Tc3Cfg<BN, A_MN, B_MN, RB>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* res = base + kSt3 * Cfg::STAGE_BYTES;
+  auto a_raw = [&](int s) { return base + s * Cfg::STAGE_BYTES; };
+  auto b_hi = [&](int s, int kt) {
+    return RB ? res + kt * 2 * Cfg::B_BYTES : base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
+  };
+  auto b_lo = [&](int s, int kt) {
+    return RB ? res + kt * 2 * Cfg::B_BYTES + Cfg::B_BYTES : base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES + Cfg::B_BYTES;
+  };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(res + Cfg::RES_BYTES);
+  uint64_t* full = bars;               // TMA landed
+  uint64_t* conv = bars + kSt3;        // A in TMEM (and B split) for the stage
+  uint64_t* empty = bars + 2 * kSt3;   // MMAs of the stage completed
+  uint64_t* accf = bars + 3 * kSt3;    // [2] accumulator ready
+  uint64_t* acce = bars + 3 * kSt3 + 2;
+  uint64_t* bres = bars + 3 * kSt3 + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kSt3 + 5);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ktiles = (K + kBK - 1) / kBK;
+  const int num_n = (N + BN - 1) / BN, num_m = (M + kBM - 1) / kBM;
+  const int total = batches * num_m * num_n;
+  auto decode = [&](int t, int& b, int& m0, int& n0) {
+    const int nb = t % num_n;
+    const int r = t / num_n;
+    m0 = (r % num_m) * kBM;
+    b = r / num_m;
+    n0 = nb * BN;
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSt3; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], kConvA + (RB ? 0 : kConvB));
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&accf[a], 1);
+      mbar_init(&acce[a], 128);
+    }
+    mbar_init(bres, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 32) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (RB) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      if constexpr (RB) {
+        mbar_expect_tx(bres, ktiles * 2 * Cfg::B_BYTES);
+        for (int kt = 0; kt < ktiles; ++kt) {
+          tma_load_3d(b_hi(0, kt), &tmB, bres, kt * kBK, 0, 0);
+          tma_load_3d(b_lo(0, kt), &tmBlo, bres, kt * kBK, 0, 0);
+        }
+      }
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int b, m0, n0;
+        decode(t, b, m0, n0);
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % kSt3;
+          mbar_wait(&empty[s], ((it / kSt3) & 1) ^ 1);
+          mbar_expect_tx(&full[s], RB ? Cfg::A_BYTES : Cfg::A_BYTES + Cfg::B_BYTES);
+          const int k0 = kt * kBK;
+          if (!A_MN) {
+            tma_load_3d(a_raw(s), &tmA, &full[s], k0, m0, b);
+          } else {
+            for (int c = 0; c < kBM / 32; ++c) tma_load_3d(a_raw(s) + c * 4096, &tmA, &full[s], m0 + 32 * c, k0, b);
+          }
+          if constexpr (!RB) {
+            if (!B_MN) {
+              tma_load_3d(b_hi(s, kt), &tmB, &full[s], k0, n0, b);
+            } else {
+              for (int c = 0; c < BN / 32; ++c)
+                tma_load_3d(b_hi(s, kt) + c * 4096, &tmB, &full[s], n0 + 32 * c, k0, b);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = idesc_tf32(BN, false, B_MN);
+    const uint32_t lboB = B_MN ? mn_lbo : 16u, sboB = B_MN ? mn_sbo : 1024u;
+    int it = 0, j = 0;
+    if (RB) mbar_wait(bres, 0);
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      const int a = j & 1;
+      mbar_wait(&acce[a], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dacc = tmem + (uint32_t)(a * BN);
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int s = it % kSt3;
+        mbar_wait(&conv[s], (it / kSt3) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ahi = tmem + (uint32_t)(Cfg::ACOL + 64 * s), alo = ahi + 32;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            const uint32_t kofb = (B_MN ? 1024u : 32u) * kk;
+            const uint64_t dbh = umma_desc(smem_u32(b_hi(s, kt)) + kofb, lboB, sboB, B_MN);
+            const uint64_t dbl = umma_desc(smem_u32(b_lo(s, kt)) + kofb, lboB, sboB, B_MN);
+            umma_tf32_ta(dacc, ahi + 8 * kk, dbh, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+            umma_tf32_ta(dacc, ahi + 8 * kk, dbl, idesc, 1u);
+            umma_tf32_ta(dacc, alo + 8 * kk, dbh, idesc, 1u);
+          }
+          umma_commit(&empty[s]);
+          if (kt == ktiles - 1) umma_commit(&accf[a]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------------------------------------------------------- A -> TMEM (hi, lo)
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int row = 32 * q + lane;   // tile row of this thread
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int s = it % kSt3;
+        mbar_wait(&full[s], (it / kSt3) & 1);
+        uint32_t hi[32], lo[32];
+        const unsigned char* ab = a_raw(s);
+        if (!A_MN) {  // 128B-swizzled rows: 16-byte chunk c of row r sits at c ^ (r & 7)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(ab + row * 128 + ((c ^ (row & 7)) << 4));
+            const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float h = tf32_trunc(x[e]);
+              hi[4 * c + e] = __float_as_uint(h);
+              lo[4 * c + e] = __float_as_uint(tf32_round(x[e] - h));
+            }
+          }
+        } else {  // unswizzled [k][32 rows] boxes, one per 32-row chunk
+          const float* cb = reinterpret_cast<const float*>(ab + (row >> 5) * 4096) + (row & 31);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float x = cb[32 * k];
+            const float h = tf32_trunc(x);
+            hi[k] = __float_as_uint(h);
+            lo[k] = __float_as_uint(tf32_round(x - h));
+          }
+        }
+        const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(Cfg::ACOL + 64 * s);
+        tmem_st32(tq, hi);
+        tmem_st32(tq + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&conv[s]);
+      }
+    }
+  } else if (warp < 8) {
+    // ---------------------------------------------------------------- B split in shared memory
+    if constexpr (!RB) {
+      const int cv = threadIdx.x - 192;  // 0 .. kConvB-1
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % kSt3;
+          mbar_wait(&full[s], (it / kSt3) & 1);
+          float4* bh = reinterpret_cast<float4*>(b_hi(s, kt));
+          float4* bl = reinterpret_cast<float4*>(b_lo(s, kt));
+#pragma unroll 4
+          for (int i = cv; i < Cfg::B_BYTES / 16; i += kConvB) {
+            const float4 x = bh[i];
+            const float4 h = make_float4(tf32_trunc(x.x), tf32_trunc(x.y), tf32_trunc(x.z), tf32_trunc(x.w));
+            bl[i] = make_float4(tf32_round(x.x - h.x), tf32_round(x.y - h.y), tf32_round(x.z - h.z),
+                                tf32_round(x.w - h.w));
+          }
+          fence_proxy_async();
+          mbar_arrive(&conv[s]);
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (TMA tensor stores)
+    const int q = warp - 8;
+    unsigned char* ebuf = res + Cfg::RES_BYTES + 1024 + q * 2 * 4096;
+    int nbox = 0, j = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      int b, m0, n0;
+      decode(t, b, m0, n0);
+      const int a = j & 1;
+      mbar_wait(&accf[a], (j >> 1) & 1);
+      tc_fence_after();
+      const int row0 = m0 + 32 * q;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN && n0 + c0 < N; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
+        unsigned char* box = ebuf + (nbox & 1) * 4096;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        if (!ct) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((jj ^ (lane & 7)) << 4)) =
+                make_float4(__uint_as_float(r[4 * jj]), __uint_as_float(r[4 * jj + 1]),
+                            __uint_as_float(r[4 * jj + 2]), __uint_as_float(r[4 * jj + 3]));
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            *reinterpret_cast<float*>(box + jj * 128 + (((lane >> 2) ^ (jj & 7)) << 4) + ((lane & 3) << 2)) =
+                __uint_as_float(r[jj]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && row0 < M) {
+          if (!ct)
+            tma_store_3d(&tmC, box, n0 + c0, row0, b);
+          else
+            tma_store_3d(&tmC, box, row0, n0 + c0, b);
+          bulk_commit();
+        }
+        ++nbox;
+      }
+      tc_fence_before();
+      mbar_arrive(&acce[a]);
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 // ------------------------------------------------------------------ host: tensor maps
 // MN-major 128B-swizzle descriptor strides (bytes): LBO = MN-chunk stride, SBO = 8-row K-group stride
 uint32_t g_mn_lbo = 4096, g_mn_sbo = 512;
@@ -466,6 +768,8 @@ int g_epi_mode = 3;
 int g_pdl = 1;
 // resident constant-B variant allowed (1) / off (0)
 int g_rb = 1;
+// 3xTF32 with A staged in TMEM (tc3_kernel) (1) / split in shared memory (0)
+int g_tc3 = 1;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -494,10 +798,10 @@ struct MapKey {
   const float* ptr;
   int64_t inner, rows, batch, ld, bstride;
   int box_rows;
-  bool mn32;
+  int swz;
   bool operator==(const MapKey& o) const {
     return ptr == o.ptr && inner == o.inner && rows == o.rows && batch == o.batch && ld == o.ld &&
-           bstride == o.bstride && box_rows == o.box_rows && mn32 == o.mn32;
+           bstride == o.bstride && box_rows == o.box_rows && swz == o.swz;
   }
 };
 struct MapEntry {
@@ -509,11 +813,11 @@ MapEntry g_map_cache[32];
 int g_map_next = 0;
 
 bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t rows, int64_t batch, int64_t ld,
-              int64_t bstride, int box_rows, bool mn32 = false) {
+              int64_t bstride, int box_rows, int swz = 0) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 4) % 16 || (bstride * 4) % 16) return false;
-  const MapKey key{ptr, inner, rows, batch, ld, bstride, box_rows, mn32};
+  const MapKey key{ptr, inner, rows, batch, ld, bstride, box_rows, swz};
   for (auto& e : g_map_cache)
     if (e.valid && e.key == key) {
       *map = e.map;
@@ -525,7 +829,9 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t rows, i
   cuuint32_t estr[3] = {1u, 1u, 1u};
   const bool ok = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      mn32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                      swz == 1   ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                      : swz == 2 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                 : CU_TENSOR_MAP_SWIZZLE_128B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   if (ok) {
     MapEntry& e = g_map_cache[g_map_next];
@@ -565,6 +871,29 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const 
   return LTB_OK;
 }
 
+template <int BN, bool A_MN, bool B_MN, bool RB>
+int launch_tc3(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mblo,
+               const CUtensorMap& mc, int ct, int64_t batch, int M, int N, int K) {
+  using Cfg = Tc3Cfg<BN, A_MN, B_MN, RB>;
+  auto kern = tc3_kernel<BN, A_MN, B_MN, RB>;
+  LTB_TRY(ensure_smem(ctx, kern, Cfg::SMEM));
+  const int64_t tiles = batch * (int64_t)((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
+  const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, mc, M, N, K, (int)batch, g_mn_lbo, g_mn_sbo, ct));
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
+
 }  // namespace
 
 // C[b] = op(A[b]) op(B[b]) in fp32 on tcgen05 (3xTF32 when split == 3).
@@ -599,6 +928,20 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
     std::memset(&mc, 0, sizeof(mc));
   }
   const int m = (int)M, n = (int)N, k = (int)K, ct = c_trans ? 1 : 0;
+  if (split == 3 && g_tc3 && okC) {
+    // A staged in TMEM (tc3_kernel): an MN-major A is fetched unswizzled
+    CUtensorMap ma3;
+    const bool ok3 = a_mn ? make_map(&ma3, A, M, K, batch, lda, sa, kBK, 2) : (ma3 = ma, true);
+    if (ok3) {
+#define LTB_TC3(BNv, AM, BM_, RBv) launch_tc3<BNv, AM, BM_, RBv>(ctx, ma3, mb, mblo, mc, ct, batch, m, n, k)
+      if (rb) return a_mn ? LTB_TC3(96, true, false, true) : LTB_TC3(96, false, false, true);
+      if (!a_mn && !b_mn) return LTB_TC3(128, false, false, false);
+      if (!a_mn && b_mn) return LTB_TC3(128, false, true, false);
+      if (a_mn && !b_mn) return LTB_TC3(128, true, false, false);
+      return LTB_TC3(128, true, true, false);
+#undef LTB_TC3
+    }
+  }
 #define LTB_TC(BNv, AM, BM_, SP, RBv) \
   launch_tc<BNv, AM, BM_, SP, RBv>(ctx, ma, mb, mblo, mc, okC, ct, C, ldc, sc, batch, m, n, k)
   if (rb) return a_mn ? LTB_TC(96, true, false, 3, true) : LTB_TC(96, false, false, 3, true);
@@ -619,6 +962,7 @@ extern "C" void ltb_tc_debug_set_raw_hi(int v) { g_raw_hi = v; }
 extern "C" void ltb_tc_debug_set_epi_mode(int v) { g_epi_mode = v; }
 extern "C" void ltb_tc_debug_set_pdl(int v) { g_pdl = v; }
 extern "C" void ltb_tc_debug_set_rb(int v) { g_rb = v; }
+extern "C" void ltb_tc_debug_set_tc3(int v) { g_tc3 = v; }
 extern "C" void ltb_tc_debug_set_timeline(void* d_buf) { g_dbg = (unsigned long long*)d_buf; }
 
 extern "C" void ltb_tc_debug_set_mn_strides(uint32_t lbo, uint32_t sbo) {

@@ -258,6 +258,41 @@ int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int i
   return dispatch_io<float>(ctx, ic, oc, cm, p, d_in, layout_in, d_out, layout_out, mats, d_sumsq);
 }
 
+// K1 of two tensors with equal tube counts: one batched tensor-core launch when
+// the pair can be addressed as a batch of two (same sign of the input and
+// output pointer offsets, 16-byte multiples); otherwise two launches.
+int ltb_transform_pair_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,
+                            int layout_in, const void* d_in0, const void* d_in1, int dtype_out, int layout_out,
+                            void* d_out0, void* d_out1) {
+  if (!spec) return ltb_set_error(ctx, LTB_ETRANSFORM, "null spec");
+  const bool real32 = dtype_in == LTB_F32 && dtype_out == LTB_F32 && !spec->is_complex;
+  if (g_xform_tc && real32 && spec->d_kron[0] && spec->nmodes > 0 && ntubes > 0 && spec->P <= 96 &&
+      layout_in == LTB_TUBE_MAJOR && layout_out == LTB_SLICE_MAJOR) {
+    int64_t din = (const char*)d_in1 - (const char*)d_in0;
+    int64_t dout = (const char*)d_out1 - (const char*)d_out0;
+    const float* X = (const float*)d_in0;
+    float* Y = (float*)d_out0;
+    if (din < 0 && dout < 0) {  // address the pair from the lower pointers
+      din = -din;
+      dout = -dout;
+      X = (const float*)d_in1;
+      Y = (float*)d_out1;
+    }
+    const int64_t P = spec->P, NT = ntubes;
+    if (din > 0 && dout > 0 && din % 16 == 0 && dout % 16 == 0 && din < (int64_t(1) << 40) &&
+        dout < (int64_t(1) << 40) && din / 4 >= NT * P && dout / 4 >= NT * P) {
+      const float* K = spec->d_kron[inverse ? 1 : 0];
+      const int st =
+          ltb_tc_gemm_f32(ctx, 2, NT, P, P, false, X, P, din / 4, false, K, P, 0, Y, NT, dout / 4, 3, true, K + P * P);
+      if (st != LTB_EUNSUPPORTED) return st;
+    }
+  }
+  LTB_TRY(ltb_transform_impl(ctx, spec, ntubes, inverse, dtype_in, layout_in, d_in0, dtype_out, layout_out, d_out0,
+                             nullptr));
+  return ltb_transform_impl(ctx, spec, ntubes, inverse, dtype_in, layout_in, d_in1, dtype_out, layout_out, d_out1,
+                            nullptr);
+}
+
 extern "C" int ltb_mode_product(ltb_ctx* ctx, int64_t outer, int64_t nin, int64_t inner, int64_t nout, int dtype_in,
                                 const void* d_in, int dtype_mat, const void* d_mat, int dtype_out, void* d_out) {
   if (!dtype_valid(dtype_in) || !dtype_valid(dtype_mat) || !dtype_valid(dtype_out))

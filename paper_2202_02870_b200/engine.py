@@ -37,6 +37,8 @@ class LProductPlan:
         self.hc = nat.DeviceArray((self.P, self.m, self.n), self.hat_dtype)
         self.c_shape = (self.m, self.n) + self.trailing
         self._sums = (C.c_double * 2)()
+        # K1(A) and K1(B) as one call (one tensor-core launch) when the tube counts match
+        self.paired = self.m * self.k == self.k * self.n
 
     def flops(self) -> int:
         """Algorithmic flop count: slice GEMM + separable real transforms."""
@@ -52,18 +54,22 @@ class LProductPlan:
     def run(self, a: nat.DeviceArray, b: nat.DeviceArray, c: nat.DeviceArray, marks=None, check_real=False,
             phases=(0, 1, 2, 3)):
         """Enqueue the phases K1(A)=0, K1(B)=1, K2=2, K1'=3 (all by default); `marks(i)`
-        is called before phase i and after the last one (i = 4)."""
+        is called before phase i and after the last one (i = 4).  When `paired`, phase 0
+        transforms A and B together and phase 1 enqueues nothing."""
         lib, ctx = nat.lib(), nat.context()
         h = self.handle.ptr
         mark = marks or (lambda i: None)
         m, k, n, P = self.m, self.k, self.n, self.P
         sums = None
         mark(0)
-        if 0 in phases:
+        if 0 in phases and self.paired:  # phase 0 transforms both operands, phase 1 is empty
+            nat.check(lib.ltb_transform_pair(ctx, h, m * k, 0, a.code, nat.TUBE_MAJOR, a.ptr, b.ptr, self.ha.code,
+                                             nat.SLICE_MAJOR, self.ha.ptr, self.hb.ptr))
+        elif 0 in phases:
             nat.check(lib.ltb_transform(ctx, h, m * k, 0, a.code, nat.TUBE_MAJOR, a.ptr, self.ha.code,
                                         nat.SLICE_MAJOR, self.ha.ptr, None))
         mark(1)
-        if 1 in phases:
+        if 1 in phases and not self.paired:
             nat.check(lib.ltb_transform(ctx, h, k * n, 0, b.code, nat.TUBE_MAJOR, b.ptr, self.hb.code,
                                         nat.SLICE_MAJOR, self.hb.ptr, None))
         mark(2)
