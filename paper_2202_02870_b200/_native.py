@@ -243,8 +243,12 @@ class DeviceArray:
         check(lib().ltb_convert(context(), self.size, self.code, self.ptr, out.code, out.ptr))
         return out
 
-    def numpy(self) -> np.ndarray:
-        out = np.empty(self.shape, dtype=self.dtype)
+    def numpy(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Download; `out` (C-contiguous, same shape and dtype, e.g. pinned host memory) is filled in place."""
+        if out is None:
+            out = np.empty(self.shape, dtype=self.dtype)
+        elif out.shape != self.shape or out.dtype != self.dtype or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous {self.dtype} array of shape {self.shape}")
         if self.nbytes:
             check(lib().ltb_memcpy_d2h(context(), out.ctypes.data_as(_vp), self.ptr, self.nbytes))
         return out

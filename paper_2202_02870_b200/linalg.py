@@ -43,7 +43,8 @@ def _hat_stack(x: np.ndarray, spec: TransformSpec, hat_dtype=None) -> nat.Device
     return out
 
 
-def _from_hat_stack(stack: nat.DeviceArray, lead, trailing, spec: TransformSpec, assume_real: bool) -> np.ndarray:
+def _from_hat_stack(stack: nat.DeviceArray, lead, trailing, spec: TransformSpec, assume_real: bool,
+                    out: np.ndarray | None = None) -> np.ndarray:
     """L^{-1} of a device slice stack back to an (I1, I2, trailing) numpy tensor (linalg.py:26-27)."""
     full = forward_dtype(stack.dtype, spec)
     want_real = assume_real and np.issubdtype(full, np.complexfloating)
@@ -52,11 +53,11 @@ def _from_hat_stack(stack: nat.DeviceArray, lead, trailing, spec: TransformSpec,
     src_dtype = nat.complex_of(full) if np.issubdtype(stack.dtype, np.complexfloating) else nat.real_of(full)
     src = stack.astype(src_dtype)
     shape = tuple(lead) + tuple(trailing)
-    out, sums = transform_device(src, device_spec(spec, trailing), lead[0] * lead[1], True, nat.SLICE_MAJOR,
+    res, sums = transform_device(src, device_spec(spec, trailing), lead[0] * lead[1], True, nat.SLICE_MAJOR,
                                  out_dtype, nat.TUBE_MAJOR, shape, residual=want_real)
     if want_real:
         check_real_residual(sums, out_dtype)
-    return out.numpy()
+    return res.numpy(out)
 
 
 def _real_inputs(*tensors) -> bool:
@@ -80,8 +81,11 @@ def _singular_values(a: np.ndarray, spec: TransformSpec) -> np.ndarray:
 
 
 # ----------------------------------------------------------------- public API
-def l_product(a, b, spec: TransformSpec) -> np.ndarray:
-    """a *_L b = L^{-1}(L(a) facewise L(b)) (linalg.py:34-43)."""
+def l_product(a, b, spec: TransformSpec, *, out: np.ndarray | None = None) -> np.ndarray:
+    """a *_L b = L^{-1}(L(a) facewise L(b)) (linalg.py:34-43).
+
+    `out` (optional, not in the reference signature): a C-contiguous host array of
+    the result's shape and dtype (e.g. pinned memory) that receives the product."""
     a = np.asarray(a)
     b = np.asarray(b)
     if a.shape[2:] != b.shape[2:]:
@@ -94,10 +98,21 @@ def l_product(a, b, spec: TransformSpec) -> np.ndarray:
     m, k, n = a.shape[0], a.shape[1], b.shape[1]
     trailing = a.shape[2:]
     P = num_rep(a.shape)
-    ha = _hat_stack(a, spec, hat_dtype)
-    hb = _hat_stack(b, spec, hat_dtype)
+    if a.dtype == b.dtype and np.isrealobj(a) and m * k == k * n and spec.modes:
+        # K1 of both operands in one call (one tensor-core launch on the fp32 path)
+        src_dtype = nat.real_of(hat_dtype)
+        sa = nat.DeviceArray.from_numpy(a, src_dtype)
+        sb = nat.DeviceArray.from_numpy(b, src_dtype)
+        ha = nat.DeviceArray((P, m, k), hat_dtype)
+        hb = nat.DeviceArray((P, k, n), hat_dtype)
+        nat.check(nat.lib().ltb_transform_pair(nat.context(), device_spec(spec, trailing).ptr, m * k, 0, sa.code,
+                                               nat.TUBE_MAJOR, sa.ptr, sb.ptr, ha.code, nat.SLICE_MAJOR, ha.ptr,
+                                               hb.ptr))
+    else:
+        ha = _hat_stack(a, spec, hat_dtype)
+        hb = _hat_stack(b, spec, hat_dtype)
     hc = slice_gemm(ha, hb, P, m, k, n)
-    return _from_hat_stack(hc, (m, n), trailing, spec, _real_inputs(a, b))
+    return _from_hat_stack(hc, (m, n), trailing, spec, _real_inputs(a, b), out=out)
 
 
 def identity_tensor(n: int, trailing_dims, spec: TransformSpec) -> np.ndarray:
