@@ -157,6 +157,13 @@ int ltb_tc_gemm(ltb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t k, in
  */
 int ltb_slice_svt(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,
                   const void* d_a, double tau, void* d_out);
+
+/* svt (linalg.py:168-181) on the transform-domain stack of a REAL tensor under
+ * `spec` (batch == spec P): when the spec's modes are real or exactly
+ * Hermitian-rowed (the DFT), slices q and its conjugate partner are solved once
+ * and mirrored; otherwise identical to ltb_slice_svt. */
+int ltb_spec_slice_svt(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1, int64_t I2,
+                       const void* d_a, double tau, void* d_out);
 int ltb_slice_svd(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,
                   const void* d_a, void* d_u, void* d_s, void* d_v);
 int ltb_slice_singular_values(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,

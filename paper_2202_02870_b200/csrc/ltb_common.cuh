@@ -151,6 +151,12 @@ struct ltb_spec {
   // real specs with P <= kKronMax: the dense Kronecker matrix of L and of L^{-1}
   // (C-order trailing index), fp32, for the tensor-core transform path
   float* d_kron[2] = {nullptr, nullptr};  // [P*P raw fp32 | P*P 3xTF32 lo part]
+  // complex specs whose modes are real or have exactly Hermitian rows (the
+  // DFT): slice q of a REAL tensor's transform is the conjugate of slice
+  // partner[q]; uniq lists one slice of every pair (q <= partner[q])
+  int64_t n_unique = 0;
+  int* d_uniq = nullptr;
+  int* d_partner = nullptr;
 };
 
 constexpr int64_t kKronMax = 512;
@@ -220,6 +226,8 @@ void ltb_ws_free(ltb_ctx* ctx, void* p);
 int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,
                        int layout_in, const void* d_in, int dtype_out, int layout_out, void* d_out,
                        double* d_sumsq /* device, 2 doubles, may be null */);
+int ltb_svt_mirror_impl(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1, int64_t I2,
+                        const void* d_a, double tau, void* d_out, const int* d_skip);
 int ltb_transform_pair_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,
                             int layout_in, const void* d_in0, const void* d_in1, int dtype_out, int layout_out,
                             void* d_out0, void* d_out1);

@@ -239,6 +239,63 @@ int ltb_spec_create(ltb_ctx* ctx, int ntrail, const int64_t* trail_dims, int nmo
     s->d_mats[0][dir] = d32;
     s->d_mats[1][dir] = d64;
   }
+  // conjugate-slice pairing for real input data (complex specs): every transformed
+  // mode is real (partner index j) or has exactly Hermitian rows (partner (n - j) mod n)
+  if (is_complex && nmodes > 0) {
+    std::vector<int> herm(ntrail, 0);
+    bool ok = true, any = false;
+    for (int k = 0; k < nmodes && ok; ++k) {
+      const int n = s->sizes[k];
+      const double* M = h_fwd + 2 * s->mat_off[k];
+      bool real = true, hrow = true;
+      for (int i = 0; i < n && (real || hrow); ++i)
+        for (int j = 0; j < n; ++j) {
+          const double re = M[2 * ((int64_t)i * n + j)], im = M[2 * ((int64_t)i * n + j) + 1];
+          if (im != 0.0) real = false;
+          const int ip = (n - i) % n;
+          const double re2 = M[2 * ((int64_t)ip * n + j)], im2 = M[2 * ((int64_t)ip * n + j) + 1];
+          if (re2 != re || im2 != -im) hrow = false;
+        }
+      if (real) continue;
+      if (hrow) {
+        herm[axes[k]] = 1;
+        any = true;
+      } else {
+        ok = false;
+      }
+    }
+    if (ok && any && s->P < (int64_t(1) << 31)) {
+      const int64_t P = s->P;
+      std::vector<int> partner((size_t)P), uniq;
+      std::vector<int64_t> idx(ntrail);
+      for (int64_t q = 0; q < P; ++q) {
+        int64_t r = q;
+        for (int a = ntrail - 1; a >= 0; --a) {
+          idx[a] = r % trail_dims[a];
+          r /= trail_dims[a];
+        }
+        int64_t qp = 0;
+        for (int a = 0; a < ntrail; ++a) {
+          const int64_t j = herm[a] ? (trail_dims[a] - idx[a]) % trail_dims[a] : idx[a];
+          qp = qp * trail_dims[a] + j;
+        }
+        partner[(size_t)q] = (int)qp;
+        if (q <= qp) uniq.push_back((int)q);
+      }
+      if ((int64_t)uniq.size() < P && cudaMalloc(&s->d_partner, sizeof(int) * P) == cudaSuccess &&
+          cudaMalloc(&s->d_uniq, sizeof(int) * uniq.size()) == cudaSuccess) {
+        cudaMemcpy(s->d_partner, partner.data(), sizeof(int) * P, cudaMemcpyHostToDevice);
+        cudaMemcpy(s->d_uniq, uniq.data(), sizeof(int) * uniq.size(), cudaMemcpyHostToDevice);
+        s->n_unique = (int64_t)uniq.size();
+      } else {
+        cudaGetLastError();
+        if (s->d_partner) cudaFree(s->d_partner);
+        s->d_partner = nullptr;
+        s->d_uniq = nullptr;
+        s->n_unique = 0;
+      }
+    }
+  }
   // dense Kronecker matrices K[q][q'] = prod_a F_a[k_a][k'_a] (F_a = M_a on
   // transformed axes, I elsewhere; C-order q) for the tensor-core path
   if (!is_complex && s->P <= kKronMax) {
@@ -319,6 +376,8 @@ void ltb_spec_destroy(ltb_spec* s) {
       if (s->d_mats[p][d]) cudaFree(s->d_mats[p][d]);
   for (int d = 0; d < 2; ++d)
     if (s->d_kron[d]) cudaFree(s->d_kron[d]);
+  if (s->d_uniq) cudaFree(s->d_uniq);
+  if (s->d_partner) cudaFree(s->d_partner);
   delete s;
 }
 

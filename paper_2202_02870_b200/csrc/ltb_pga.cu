@@ -224,7 +224,8 @@ int pga_transforms(ltb_pga* g, int k, double beta, double mu, double tol, double
     LTB_TRY((launch_xform_tile<Tc, Tm>(ctx, p, ld, st, (const Tm*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
   }
   // slice SVT with tau = mu_k
-  LTB_TRY(ltb_svt_impl(ctx, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, nullptr, g->hat_b, skip));
+  // (conjugate slice pairs of the real iterate are solved once)
+  LTB_TRY(ltb_svt_mirror_impl(ctx, g->spec, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, g->hat_b, skip));
   // inverse with the fused norms epilogue
   if (!pga_plan<Tc, Tm>(g->spec, g->NT, 1, p, &smem))
     return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");

@@ -955,6 +955,73 @@ int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2,
   });
 }
 
+namespace {
+template <typename T>
+__global__ void slice_gather_kernel(int64_t nu, int64_t S, const int* __restrict__ uniq, const T* __restrict__ src,
+                                    T* __restrict__ dst, const int* skip) {
+  if (skip && *skip) return;
+  const int64_t total = nu * S;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = l / S;
+    dst[l] = src[(int64_t)uniq[u] * S + (l - u * S)];
+  }
+}
+
+template <typename T>
+__global__ void slice_mirror_scatter_kernel(int64_t nu, int64_t S, const int* __restrict__ uniq,
+                                            const int* __restrict__ partner, const T* __restrict__ src,
+                                            T* __restrict__ dst, const int* skip) {
+  if (skip && *skip) return;
+  const int64_t total = nu * S;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = l / S, r = l - u * S;
+    const int q = uniq[u], p = partner[q];
+    const T v = src[l];
+    dst[(int64_t)q * S + r] = v;
+    if (p != q) dst[(int64_t)p * S + r] = conj_v(v);
+  }
+}
+}  // namespace
+
+// SVT of the transform-domain stack of a REAL tensor under `spec`: slices q
+// and partner[q] are exact conjugates (SVT(conj A) = conj SVT(A), and the
+// Jacobi kernel is conjugation-equivariant), so only one slice of every pair
+// is solved and its conjugate mirrored -- P_u = 99 of 192 slices for config 4.
+int ltb_svt_mirror_impl(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1, int64_t I2,
+                        const void* d_a, double tau, void* d_out, const int* d_skip) {
+  if (!spec || !spec->d_uniq || spec->P != batch || !dtype_is_complex(dtype) || batch == 0 || I1 == 0 || I2 == 0)
+    return ltb_svt_impl(ctx, dtype, batch, I1, I2, d_a, tau, nullptr, d_out, d_skip);
+  return dispatch_dtype(dtype, [&](auto tg) -> int {
+    using T = typename decltype(tg)::type;
+    if constexpr (!scalar_traits<T>::is_complex) {
+      return ltb_svt_impl(ctx, dtype, batch, I1, I2, d_a, tau, nullptr, d_out, d_skip);
+    } else {
+      const int64_t nu = spec->n_unique, S = I1 * I2;
+      T* cin = nullptr;
+      T* cout = nullptr;
+      LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * nu * S, (void**)&cin));
+      LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * nu * S, (void**)&cout));
+      const unsigned grid = grid_for(nu * S, 256, ctx->num_sms * 8);
+      slice_gather_kernel<T><<<grid, 256, 0, ctx->stream>>>(nu, S, spec->d_uniq, (const T*)d_a, cin, d_skip);
+      LTB_LAUNCH_CHECK(ctx);
+      LTB_TRY(ltb_svt_impl(ctx, dtype, nu, I1, I2, cin, tau, nullptr, cout, d_skip));
+      slice_mirror_scatter_kernel<T><<<grid, 256, 0, ctx->stream>>>(nu, S, spec->d_uniq, spec->d_partner, cout,
+                                                                    (T*)d_out, d_skip);
+      LTB_LAUNCH_CHECK(ctx);
+      ltb_ws_free(ctx, cin);
+      ltb_ws_free(ctx, cout);
+      return LTB_OK;
+    }
+  });
+}
+
+extern "C" int ltb_spec_slice_svt(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1,
+                                  int64_t I2, const void* d_a, double tau, void* d_out) {
+  if (!dtype_valid(dtype)) return ltb_set_error(ctx, LTB_EPARAM, "svt: bad dtype");
+  if (batch < 0 || I1 < 0 || I2 < 0) return ltb_set_error(ctx, LTB_ESHAPE, "svt: negative dimension");
+  return ltb_svt_mirror_impl(ctx, spec, dtype, batch, I1, I2, d_a, tau, d_out, nullptr);
+}
+
 extern "C" int ltb_slice_singular_values(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2,
                                          const void* d_a, void* d_s) {
   if (!dtype_valid(dtype)) return ltb_set_error(ctx, LTB_EPARAM, "svd: bad dtype");

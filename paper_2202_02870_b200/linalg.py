@@ -239,5 +239,9 @@ def svt(a, tau: float, spec: TransformSpec) -> np.ndarray:
     hat = _hat_stack(a, spec)
     P, i1, i2 = hat.shape
     out = nat.DeviceArray((P, i1, i2), hat.dtype)
-    nat.check(nat.lib().ltb_slice_svt(nat.context(), hat.code, P, i1, i2, hat.ptr, float(tau), out.ptr))
+    if np.isrealobj(a):  # conjugate slice pairs of a real tensor's transform are solved once
+        nat.check(nat.lib().ltb_spec_slice_svt(nat.context(), device_spec(spec, a.shape[2:]).ptr, hat.code, P, i1,
+                                               i2, hat.ptr, float(tau), out.ptr))
+    else:
+        nat.check(nat.lib().ltb_slice_svt(nat.context(), hat.code, P, i1, i2, hat.ptr, float(tau), out.ptr))
     return _from_hat_stack(out, (i1, i2), a.shape[2:], spec, _real_inputs(a))

@@ -240,3 +240,25 @@ def test_tc_transform_layouts(trail, nt):
     hat = nat.DeviceArray.from_numpy(np.ascontiguousarray(ref.T.astype(np.float32)))
     back, _ = TR.transform_device(hat, handle, nt, True, nat.SLICE_MAJOR, np.float32, nat.TUBE_MAJOR, (nt, P))
     assert np.linalg.norm(back.numpy() - x.reshape(nt, P)) / np.linalg.norm(x) < 1e-5
+
+
+# ---- conjugate-pair SVT: for a real tensor under a DFT-type spec, solving one slice of every
+# conjugate pair and mirroring must equal solving every slice (the Jacobi kernel is conjugation-
+# equivariant), bit for bit
+@pytest.mark.parametrize("kind,shape", [("fft", (20, 16, 6)), ("fft", (12, 30, 4, 5)), ("dct", (10, 9, 4))])
+def test_spec_svt_mirror_matches_full(kind, shape):
+    import paper_2202_02870_b200 as L
+    from paper_2202_02870_b200 import linalg, transforms as TR
+
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal(shape)
+    spec = L.make_spec(kind, shape)
+    hat = linalg._hat_stack(x, spec)
+    P, i1, i2 = hat.shape
+    tau = 0.7
+    full = nat.DeviceArray(hat.shape, hat.dtype)
+    mirr = nat.DeviceArray(hat.shape, hat.dtype)
+    nat.check(nat.lib().ltb_slice_svt(nat.context(), hat.code, P, i1, i2, hat.ptr, tau, full.ptr))
+    nat.check(nat.lib().ltb_spec_slice_svt(nat.context(), TR.device_spec(spec, shape[2:]).ptr, hat.code, P, i1, i2,
+                                           hat.ptr, tau, mirr.ptr))
+    np.testing.assert_array_equal(mirr.numpy(), full.numpy())
