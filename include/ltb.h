@@ -85,6 +85,10 @@ int ltb_memcpy_d2d(ltb_ctx* ctx, void* d_dst, const void* d_src, int64_t bytes);
 int ltb_memset_zero(ltb_ctx* ctx, void* d_dst, int64_t bytes);
 /* elementwise dtype conversion (real<->complex, single<->double); complex->real keeps .re */
 int ltb_convert(ltb_ctx* ctx, int64_t n, int dtype_in, const void* d_in, int dtype_out, void* d_out);
+/* TLT1 container payload (io.py:1-10, read_container io.py:54-83): reorder a
+ * generalized column-major (Fortran) payload of `ndim` dims to C order on the
+ * device; elem_bytes 1 (bool mask), 4 (float32), 8 (float64), 16 (complex128). */
+int ltb_fortran_to_c(ltb_ctx* ctx, int ndim, const int64_t* dims, int elem_bytes, const void* d_src, void* d_dst);
 
 /* ---------------------------------------------------------------- spec
  * Replaces TransformSpec.mode_matrix / mode_inverse (transforms.py:87-100)

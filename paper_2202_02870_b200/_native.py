@@ -52,6 +52,7 @@ _SIGNATURES = {
     "ltb_memcpy_d2d": ([_vp, _vp, _vp, _i64], _int),
     "ltb_memset_zero": ([_vp, _vp, _i64], _int),
     "ltb_convert": ([_vp, _i64, _int, _vp, _int, _vp], _int),
+    "ltb_fortran_to_c": ([_vp, _int, _vp, _int, _vp, _vp], _int),
     "ltb_spec_create": ([_vp, _int, C.POINTER(_i64), _int, _ip, _int, _dp, _dp, C.POINTER(_vp)], _int),
     "ltb_spec_destroy": ([_vp], None),
     "ltb_transform": ([_vp, _vp, _i64, _int, _int, _int, _vp, _int, _int, _vp, _dp], _int),

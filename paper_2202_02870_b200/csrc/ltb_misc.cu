@@ -102,7 +102,65 @@ __global__ void pga_gradient_kernel(int64_t n, const R* __restrict__ xc, const R
 __global__ void finalize_partials_kernel(const double* __restrict__ partials, int64_t nblocks, int nacc,
                                          unsigned maxmask, double* __restrict__ out);
 
+// TLT1 payloads are generalized column-major (io.py:1-10): the device copy is
+// reordered to C order, dst[c-index(i)] = src[f-index(i)], for element sizes
+// 1, 4, 8, 16 bytes.  Each thread owns one destination element (coalesced
+// writes; the source gather is strided).
+struct FDims {
+  int nd;
+  int64_t d[8];
+};
+
+template <typename E>
+__global__ void fortran_to_c_kernel(int64_t total, FDims g, const E* __restrict__ src, E* __restrict__ dst) {
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = l, f = 0, stride = 1;
+    int64_t idx[8];
+    for (int a = g.nd - 1; a >= 0; --a) {  // C-order decode
+      idx[a] = r % g.d[a];
+      r /= g.d[a];
+    }
+    for (int a = 0; a < g.nd; ++a) {  // Fortran-order encode
+      f += idx[a] * stride;
+      stride *= g.d[a];
+    }
+    dst[l] = src[f];
+  }
+}
+
 extern "C" {
+
+int ltb_fortran_to_c(ltb_ctx* ctx, int ndim, const int64_t* dims, int elem_bytes, const void* d_src, void* d_dst) {
+  if (ndim < 1 || ndim > 8) return ltb_set_error(ctx, LTB_ESHAPE, "fortran_to_c: order %d outside 1..8", ndim);
+  FDims g{};
+  g.nd = ndim;
+  int64_t total = 1;
+  for (int a = 0; a < ndim; ++a) {
+    if (dims[a] < 0) return ltb_set_error(ctx, LTB_ESHAPE, "fortran_to_c: negative dim");
+    g.d[a] = dims[a];
+    total *= dims[a];
+  }
+  if (total == 0) return LTB_OK;
+  const unsigned grid = grid_for(total, 256, ctx->num_sms * 16);
+  switch (elem_bytes) {
+    case 1:
+      fortran_to_c_kernel<uint8_t><<<grid, 256, 0, ctx->stream>>>(total, g, (const uint8_t*)d_src, (uint8_t*)d_dst);
+      break;
+    case 4:
+      fortran_to_c_kernel<float><<<grid, 256, 0, ctx->stream>>>(total, g, (const float*)d_src, (float*)d_dst);
+      break;
+    case 8:
+      fortran_to_c_kernel<double><<<grid, 256, 0, ctx->stream>>>(total, g, (const double*)d_src, (double*)d_dst);
+      break;
+    case 16:
+      fortran_to_c_kernel<double2><<<grid, 256, 0, ctx->stream>>>(total, g, (const double2*)d_src, (double2*)d_dst);
+      break;
+    default:
+      return ltb_set_error(ctx, LTB_EPARAM, "fortran_to_c: element size %d not in {1, 4, 8, 16}", elem_bytes);
+  }
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
 
 int ltb_embed_diag(ltb_ctx* ctx, int dtype_out, int64_t batch, int64_t m, int64_t n, const void* d_vals,
                    void* d_out) {

@@ -122,3 +122,14 @@ def completion_cases(lp):
 def mask_cases():
     return {"m_a": ((4, 5, 3), 0.5, 0), "m_b": ((6, 6, 4), 0.3, 42), "m_c": ((8, 8, 3), 0.3, 3),
             "m_d": ((3, 3, 2), 1.0, 0), "m_e": ((3, 3, 2), 0.0, 0)}
+
+
+def btph_cases():
+    """Small cprod products checked against the reference's btph construction (btph.py:140-149)."""
+    r = np.random.default_rng(314)
+    c = {}
+    for name, (sa, sb) in {"b_cprod3": ((3, 4, 5), (4, 2, 5)), "b_cprod4": ((2, 3, 3, 4), (3, 2, 3, 4)),
+                           "b_cprod_tube": ((1, 1, 6), (1, 1, 6))}.items():
+        c[name] = dict(kind="cprod", a=r.standard_normal(sa), b=r.standard_normal(sb),
+                       spec_shape=(sa[0], sb[1]) + tuple(sa[2:]))
+    return c

@@ -60,6 +60,15 @@ def main():
         out[f"{name}/a"] = case["a"]
         out[f"{name}/b"] = case["b"]
         out[f"{name}/c"] = ref.l_product(case["a"], case["b"], spec_of(case))
+    # the generalized c-product through the reference's block-Toeplitz-plus-Hankel
+    # construction (btph.py:140-149), the paper's independent characterisation of cprod
+    from ltensor.btph import cproduct_via_btph
+
+    for name, case in cases.btph_cases().items():
+        put_meta(out, name, case)
+        out[f"{name}/a"] = case["a"]
+        out[f"{name}/b"] = case["b"]
+        out[f"{name}/c"] = cproduct_via_btph(case["a"], case["b"])
     for name, case in cases.svd_cases().items():
         spec = spec_of(case)
         put_meta(out, name, case, tau=case["tau"])
@@ -98,6 +107,21 @@ def main():
     for name, (dims, sr, seed) in cases.mask_cases().items():
         out[f"{name}/meta"] = np.array(json.dumps({"dims": list(dims), "sr": sr, "seed": seed}))
         out[f"{name}/mask"] = ref.sample_mask(dims, sr, seed)
+    # TLT1 container bytes written by the reference (io.py:39-51) for a few dtypes / orders
+    import tempfile
+
+    from ltensor.io import write_container
+
+    r = np.random.default_rng(2718)
+    io_cases = {"io_f64": r.standard_normal((3, 4, 2, 5)), "io_f32": r.standard_normal((2, 3, 4)).astype(np.float32),
+                "io_c128": r.standard_normal((2, 2, 3)) + 1j * r.standard_normal((2, 2, 3)),
+                "io_mask": r.random((5, 4, 3, 2)) < 0.37}
+    with tempfile.TemporaryDirectory() as td:
+        for name, x in io_cases.items():
+            path = Path(td) / f"{name}.tlt"
+            write_container(path, x)
+            out[f"{name}/x"] = x
+            out[f"{name}/bytes"] = np.frombuffer(path.read_bytes(), dtype=np.uint8)
     np.savez_compressed(HERE / "golden.npz", **out)
     total = sum(np.asarray(v).nbytes for v in out.values())
     print(f"wrote {len(out)} arrays, {total / 1e6:.2f} MB raw -> {HERE / 'golden.npz'}")

@@ -143,3 +143,12 @@ def test_deterministic_bitwise(golden):
     a, _ = L.pga_complete(m, mask, cfg)
     b, _ = L.pga_complete(m, mask, cfg)
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", case_names("b_"))
+def test_cprod_product_matches_btph(golden, name):
+    """The CUDA l_product under the non-unitary cprod transform equals the reference's
+    block-Toeplitz-plus-Hankel matrix product (btph.py:140-149) on the same inputs."""
+    spec = build_spec(L, golden, name)
+    c = L.l_product(golden[f"{name}/a"], golden[f"{name}/b"], spec)
+    assert rel_err(c, golden[f"{name}/c"]) < 1e-10

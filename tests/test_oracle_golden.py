@@ -78,3 +78,11 @@ def test_pinned_completion_rse(golden):
 def test_sample_mask(golden, name):
     md = meta(golden, name)
     np.testing.assert_array_equal(O.sample_mask(md["dims"], md["sr"], md["seed"]), golden[f"{name}/mask"])
+
+
+@pytest.mark.parametrize("name", case_names("b_"))
+def test_oracle_cprod_equals_btph(golden, name):
+    """the oracle's cprod l_product equals the reference's btph construction."""
+    spec = build_spec(O, golden, name)
+    c = O.l_product(golden[f"{name}/a"], golden[f"{name}/b"], spec)
+    assert rel_err(c, golden[f"{name}/c"]) < 1e-12
