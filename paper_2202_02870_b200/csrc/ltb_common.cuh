@@ -165,7 +165,9 @@ constexpr int64_t kKronMax = 512;
 // alignment cannot take the tcgen05 path
 int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K, bool a_mn, const float* A,
                     int64_t lda, int64_t sa, bool b_mn, const float* B, int64_t ldb, int64_t sb, float* C,
-                    int64_t ldc, int64_t sc, int split, bool c_trans = false, const float* b_lo = nullptr);
+                    int64_t ldc, int64_t sc, int split, bool c_trans = false, const float* b_lo = nullptr,
+                    const int* klim = nullptr, const float* rscale = nullptr, const float* cscale = nullptr,
+                    const int* skip = nullptr);
 
 // ------------------------------------------------------------------ errors
 int ltb_set_error(ltb_ctx* ctx, int code, const char* fmt, ...);

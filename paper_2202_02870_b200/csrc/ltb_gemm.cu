@@ -150,14 +150,16 @@ int ltb_gemm_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, 
       LTB_LAUNCH_CHECK(ctx);
       return LTB_OK;
     }
-    // fp32 without per-slice limits / scaling: tcgen05 kind::tf32 with the 3xTF32 split
+    // fp32 without m / n limits: tcgen05 kind::tf32 with the 3xTF32 split (per-slice K
+    // limits, row / column scaling and the skip flag are handled by the tensor-core kernel)
     if constexpr (std::is_same<T, float>::value) {
-      if (!d_mlim && !d_nlim && !d_klim && !d_row_scale && !d_col_scale && !d_skip && m >= 32 && n >= 32 &&
-          k >= 8) {
+      if (!d_mlim && !d_nlim && m >= 32 && n >= 32 && k >= 8) {
         // op N: A stored m x k (K-major); op T: stored k x m (MN-major).  B: op N stored k x n (MN-major).
         const bool a_mn = (op_a == LTB_OP_T || op_a == LTB_OP_H);
         const bool b_mn = (op_b == LTB_OP_N || op_b == LTB_OP_C);
-        const int st = ltb_tc_gemm_f32(ctx, batch, m, n, k, a_mn, a, lda, sa, b_mn, b, ldb, sb, c, ldc, sc, 3);
+        const int st = ltb_tc_gemm_f32(ctx, batch, m, n, k, a_mn, a, lda, sa, b_mn, b, ldb, sb, c, ldc, sc, 3,
+                                       false, nullptr, d_klim, (const float*)d_row_scale,
+                                       (const float*)d_col_scale, d_skip);
         if (st != LTB_EUNSUPPORTED) return st;
       }
     }

@@ -932,17 +932,20 @@ int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2,
     LTB_TRY((launch_jacobi<T, false>(ctx, batch, I1, I2, (const T*)d_a, o)));
     const T* A = (const T*)d_a;
     T* out = (T*)d_out;
+    // fp32 runs the full-size first GEMM on the tensor cores (d = 0 past the kept
+    // count zeroes those rows / columns); the CUDA-core path skips them instead
+    const int* lim = std::is_same<T, float>::value ? nullptr : kept;
     if (!trans) {
       // Z = D W^H A   (n x I2, rows limited to the kept count)
       LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, n, I2, m, LTB_OP_C, w, m, n * m, LTB_OP_N, A, I2, I1 * I2, z, I2,
-                            n * I2, kept, nullptr, nullptr, d, nullptr, d_skip));
+                            n * I2, lim, nullptr, nullptr, d, nullptr, d_skip));
       // out = W Z     (I1 x I2, inner dimension limited to the kept count)
       LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, I1, I2, n, LTB_OP_T, w, m, n * m, LTB_OP_N, z, I2, n * I2, out, I2,
                             I1 * I2, nullptr, nullptr, kept, nullptr, nullptr, d_skip));
     } else {
       // Y = A W D     (I1 x n, columns limited to the kept count)
       LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, I1, n, m, LTB_OP_N, A, I2, I1 * I2, LTB_OP_T, w, m, n * m, z, n,
-                            I1 * n, nullptr, kept, nullptr, nullptr, d, d_skip));
+                            I1 * n, nullptr, lim, nullptr, nullptr, d, d_skip));
       // out = Y W^H
       LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, I1, I2, n, LTB_OP_N, z, n, I1 * n, LTB_OP_C, w, m, n * m, out, I2,
                             I1 * I2, nullptr, nullptr, kept, nullptr, nullptr, d_skip));

@@ -502,11 +502,20 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 
+// optional per-batch extras (the SVT recomposition, ltb_svd.cu): K limited to the
+// kept count (a tile with no K blocks stores zeros), output rows / columns scaled
+struct Tc3Extras {
+  const int* klim;       // batch, or null
+  const float* rscale;   // batch x M, or null
+  const float* cscale;   // batch x N, or null
+  const int* skip;       // device flag, or null
+};
+
 template <int BN, bool A_MN, bool B_MN, bool RB>
 __global__ void __launch_bounds__(kThreads, 1)
     tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC, int M, int N,
-               int K, int batches, uint32_t mn_lbo, uint32_t mn_sbo, int ct) {
+               int K, int batches, uint32_t mn_lbo, uint32_t mn_sbo, int ct, Tc3Extras ex) {
   using Cfg = Tc3Cfg<BN, A_MN, B_MN, RB>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -530,13 +539,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (K + kBK - 1) / kBK;
   const int num_n = (N + BN - 1) / BN, num_m = (M + kBM - 1) / kBM;
-  const int total = batches * num_m * num_n;
+  int total = batches * num_m * num_n;
   auto decode = [&](int t, int& b, int& m0, int& n0) {
     const int nb = t % num_n;
     const int r = t / num_n;
     m0 = (r % num_m) * kBM;
     b = r / num_m;
     n0 = nb * BN;
+  };
+  auto ktiles_of = [&](int b) {  // K blocks of batch b (all of them without a limit)
+    if (!ex.klim) return ktiles;
+    const int kb = min(K, max(ex.klim[b], 0));
+    return (kb + kBK - 1) / kBK;
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSt3; ++s) {
@@ -567,11 +581,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // device-side stop flag (PGA), read after the dependency wait: no tiles at all
+  if (ex.skip && *ex.skip) total = 0;
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
-      if constexpr (RB) {
+      if (RB && total > 0) {
         mbar_expect_tx(bres, ktiles * 2 * Cfg::B_BYTES);
         for (int kt = 0; kt < ktiles; ++kt) {
           tma_load_3d(b_hi(0, kt), &tmB, bres, kt * kBK, 0, 0);
@@ -582,7 +598,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int b, m0, n0;
         decode(t, b, m0, n0);
-        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int kt_b = ktiles_of(b);
+        for (int kt = 0; kt < kt_b; ++kt, ++it) {
           const int s = it % kSt3;
           mbar_wait(&empty[s], ((it / kSt3) & 1) ^ 1);
           mbar_expect_tx(&full[s], RB ? Cfg::A_BYTES : Cfg::A_BYTES + Cfg::B_BYTES);
@@ -608,13 +625,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc = idesc_tf32(BN, false, B_MN);
     const uint32_t lboB = B_MN ? mn_lbo : 16u, sboB = B_MN ? mn_sbo : 1024u;
     int it = 0, j = 0;
-    if (RB) mbar_wait(bres, 0);
+    if (RB && total > 0) mbar_wait(bres, 0);
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
       const int a = j & 1;
+      int b, m0, n0;
+      decode(t, b, m0, n0);
+      const int kt_b = ktiles_of(b);
       mbar_wait(&acce[a], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t dacc = tmem + (uint32_t)(a * BN);
-      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+      if (kt_b == 0) {  // nothing to accumulate: the epilogue stores zeros
+        if (lane == 0) mbar_arrive(&accf[a]);
+        __syncwarp();
+        continue;
+      }
+      for (int kt = 0; kt < kt_b; ++kt, ++it) {
         const int s = it % kSt3;
         mbar_wait(&conv[s], (it / kSt3) & 1);
         tc_fence_after();
@@ -630,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_tf32_ta(dacc, alo + 8 * kk, dbh, idesc, 1u);
           }
           umma_commit(&empty[s]);
-          if (kt == ktiles - 1) umma_commit(&accf[a]);
+          if (kt == kt_b - 1) umma_commit(&accf[a]);
         }
         __syncwarp();
       }
@@ -641,7 +666,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = 32 * q + lane;   // tile row of this thread
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+      int b, m0, n0;
+      decode(t, b, m0, n0);
+      const int kt_b = ktiles_of(b);
+      for (int kt = 0; kt < kt_b; ++kt, ++it) {
         const int s = it % kSt3;
         mbar_wait(&full[s], (it / kSt3) & 1);
         uint32_t hi[32], lo[32];
@@ -682,7 +710,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cv = threadIdx.x - 192;  // 0 .. kConvB-1
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        int b, m0, n0;
+        decode(t, b, m0, n0);
+        const int kt_b = ktiles_of(b);
+        for (int kt = 0; kt < kt_b; ++kt, ++it) {
           const int s = it % kSt3;
           mbar_wait(&full[s], (it / kSt3) & 1);
           float4* bh = reinterpret_cast<float4*>(b_hi(s, kt));
@@ -711,10 +742,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&accf[a], (j >> 1) & 1);
       tc_fence_after();
       const int row0 = m0 + 32 * q;
+      const bool zero = ktiles_of(b) == 0;
+      const float rs = (ex.rscale && row0 + lane < M) ? ex.rscale[(int64_t)b * M + row0 + lane] : 1.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN && n0 + c0 < N; c0 += 32) {
         uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
+        if (!zero) {
+          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) r[jj] = 0u;
+        }
+        if (ex.rscale || ex.cscale) {
+          const float* cs = ex.cscale ? ex.cscale + (int64_t)b * N + n0 + c0 : nullptr;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const float c = (cs && n0 + c0 + jj < N) ? cs[jj] : 1.f;
+            r[jj] = __float_as_uint(__uint_as_float(r[jj]) * rs * c);
+          }
+        }
         unsigned char* box = ebuf + (nbox & 1) * 4096;
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
@@ -873,7 +919,7 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const 
 
 template <int BN, bool A_MN, bool B_MN, bool RB>
 int launch_tc3(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mblo,
-               const CUtensorMap& mc, int ct, int64_t batch, int M, int N, int K) {
+               const CUtensorMap& mc, int ct, int64_t batch, int M, int N, int K, const Tc3Extras& ex) {
   using Cfg = Tc3Cfg<BN, A_MN, B_MN, RB>;
   auto kern = tc3_kernel<BN, A_MN, B_MN, RB>;
   LTB_TRY(ensure_smem(ctx, kern, Cfg::SMEM));
@@ -889,7 +935,7 @@ int launch_tc3(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, mc, M, N, K, (int)batch, g_mn_lbo, g_mn_sbo, ct));
+  LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, mc, M, N, K, (int)batch, g_mn_lbo, g_mn_sbo, ct, ex));
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -906,7 +952,10 @@ int launch_tc3(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const
 // cannot use the tensor-core path; the caller then falls back.
 int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K, bool a_mn, const float* A,
                     int64_t lda, int64_t sa, bool b_mn, const float* B, int64_t ldb, int64_t sb, float* C,
-                    int64_t ldc, int64_t sc, int split, bool c_trans, const float* b_lo) {
+                    int64_t ldc, int64_t sc, int split, bool c_trans, const float* b_lo, const int* klim,
+                    const float* rscale, const float* cscale, const int* skip) {
+  const Tc3Extras ex{klim, rscale, cscale, skip};
+  const bool extras = klim || rscale || cscale || skip;
   if (batch < 1 || M < 1 || N < 1 || K < 1 || batch > 65535) return LTB_EUNSUPPORTED;
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return LTB_EUNSUPPORTED;
   if ((M + kBM - 1) / kBM > 65535) return LTB_EUNSUPPORTED;
@@ -928,12 +977,13 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
     std::memset(&mc, 0, sizeof(mc));
   }
   const int m = (int)M, n = (int)N, k = (int)K, ct = c_trans ? 1 : 0;
+  if (extras && !(split == 3 && g_tc3 && okC)) return LTB_EUNSUPPORTED;  // extras live in tc3_kernel only
   if (split == 3 && g_tc3 && okC) {
     // A staged in TMEM (tc3_kernel): an MN-major A is fetched unswizzled
     CUtensorMap ma3;
     const bool ok3 = a_mn ? make_map(&ma3, A, M, K, batch, lda, sa, kBK, 2) : (ma3 = ma, true);
     if (ok3) {
-#define LTB_TC3(BNv, AM, BM_, RBv) launch_tc3<BNv, AM, BM_, RBv>(ctx, ma3, mb, mblo, mc, ct, batch, m, n, k)
+#define LTB_TC3(BNv, AM, BM_, RBv) launch_tc3<BNv, AM, BM_, RBv>(ctx, ma3, mb, mblo, mc, ct, batch, m, n, k, ex)
       if (rb) return a_mn ? LTB_TC3(96, true, false, true) : LTB_TC3(96, false, false, true);
       if (!a_mn && !b_mn) return LTB_TC3(128, false, false, false);
       if (!a_mn && b_mn) return LTB_TC3(128, false, true, false);
