@@ -620,8 +620,10 @@ __global__ void block_load_kernel(int64_t I1, int64_t I2, const T* __restrict__ 
   }
 }
 
-template <typename T, bool WANT_V>
-__global__ void __launch_bounds__(1024, 1)
+// MPL > 0: each lane holds rows lane + 32 e (e < MPL) of the pair in registers
+// between the dot product and the rotation (mp == 32 MPL); MPL == 0 loops.
+template <typename T, bool WANT_V, int MPL, int NTMAX>
+__global__ void __launch_bounds__(NTMAX, 1)
     jacobi_block_kernel(BlockGeom g, int round, int full, T* __restrict__ W, int* __restrict__ rot,
                         const int* __restrict__ active, const int* __restrict__ skip) {
   using R = typename scalar_traits<T>::real;
@@ -697,7 +699,17 @@ __global__ void __launch_bounds__(1024, 1)
       T* x = C + (size_t)p * mp;
       T* y = C + (size_t)q * mp;
       T ga = zero_v<T>();
-      for (int i = lane; i < m; i += 32) fma_acc(ga, conj_v(x[i]), y[i]);
+      T xr[MPL > 0 ? MPL : 1], yr[MPL > 0 ? MPL : 1];
+      if constexpr (MPL > 0) {  // rows past m are zero padding
+#pragma unroll
+        for (int e = 0; e < MPL; ++e) {
+          xr[e] = x[lane + 32 * e];
+          yr[e] = y[lane + 32 * e];
+          fma_acc(ga, conj_v(xr[e]), yr[e]);
+        }
+      } else {
+        for (int i = lane; i < m; i += 32) fma_acc(ga, conj_v(x[i]), y[i]);
+      }
       R gre = warp_sum_r(re_v(ga));
       R gim = CPLX ? warp_sum_r(im_v(ga)) : (R)0;
       const R al = nrm[p], be = nrm[q];
@@ -713,11 +725,20 @@ __global__ void __launch_bounds__(1024, 1)
       } else {
         ph = (gre >= 0) ? (R)1 : (R)-1;
       }
-      for (int i = lane; i < rows; i += 32) {
-        const T xv = x[i];
-        const T yv = ph * y[i];
-        x[i] = c * xv - sn * yv;
-        y[i] = sn * xv + c * yv;
+      if constexpr (MPL > 0) {
+#pragma unroll
+        for (int e = 0; e < MPL; ++e) {
+          const T yv = ph * yr[e];
+          x[lane + 32 * e] = c * xr[e] - sn * yv;
+          y[lane + 32 * e] = sn * xr[e] + c * yv;
+        }
+      } else {
+        for (int i = lane; i < rows; i += 32) {
+          const T xv = x[i];
+          const T yv = ph * y[i];
+          x[i] = c * xv - sn * yv;
+          y[i] = sn * xv + c * yv;
+        }
       }
       if (lane == 0) {
         nrm[p] = fmax(al - t * gabs, (R)0);
@@ -817,6 +838,34 @@ __global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, Jaco
   }
 }
 
+// the sweep loop of the blocked tier for one kernel variant
+template <typename T, bool WANT_V, int MPL, int NTMAX>
+int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int* rot, int* active, int* count,
+                     const JacobiOut& o, int max_sweeps) {
+  using R = typename scalar_traits<T>::real;
+  const int nbp = g.nb + (g.nb & 1);
+  const size_t smem = 2 * (size_t)g.mp * sizeof(T) * g.b + 2 * g.b * sizeof(R) + 16;
+  auto kern = jacobi_block_kernel<T, WANT_V, MPL, NTMAX>;
+  LTB_TRY(ensure_smem(ctx, kern, smem));
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(ctx->stream, &cap);
+  const dim3 bgrid((unsigned)(nbp / 2), (unsigned)batch);
+  const int threads = 32 * std::min(g.b, NTMAX / 32);
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int r = 0; r < nbp - 1; ++r) {
+      kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip);
+      LTB_LAUNCH_CHECK(ctx);
+    }
+    block_sweep_update_kernel<<<1, 256, 0, ctx->stream>>>(batch, rot, active, count, o.stats);
+    LTB_LAUNCH_CHECK(ctx);
+    if (cap != cudaStreamCaptureStatusNone) continue;  // no host read-back inside a capture
+    LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (*reinterpret_cast<int*>(ctx->h_scratch) == 0) break;
+  }
+  return LTB_OK;
+}
+
 template <typename T, bool WANT_V>
 int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, const JacobiOut& o,
                           int max_sweeps) {
@@ -826,15 +875,30 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   g.m = (int)std::max(I1, I2);
   g.n = (int)std::min(I1, I2);
   const int rows = g.m + (WANT_V ? g.n : 0);
+  // register-tile variants (fp32 / complex64 SVT): rows padded to 32 * MPL, block size capped
+  // by the variant's thread count (registers per thread)
+  constexpr bool f32 = std::is_same<T, float>::value, c32 = std::is_same<T, cplx<float>>::value;
+  int mpl = 0, ntmax = 1024;
+  if constexpr (!WANT_V && (f32 || c32)) {
+    const int need = (rows + 31) / 32;
+    if (need <= 8) {
+      mpl = 8;
+    } else if (need <= 16) {
+      mpl = 16;
+      ntmax = f32 ? 1024 : 512;
+    } else if (need <= 32) {
+      mpl = 32;
+      ntmax = f32 ? 512 : 384;
+    }
+  }
   const int per16 = 16 / (int)std::min<size_t>(sizeof(T), 16);
-  g.mp = (rows + 31) / 32 * 32;
+  g.mp = mpl > 0 ? 32 * mpl : (rows + 31) / 32 * 32;
   g.mp = (g.mp + per16 - 1) / per16 * per16;
   const size_t colb = (size_t)g.mp * sizeof(T);
   const size_t fit = (kBlockSmem - 256) / (2 * colb);
   if (fit < 1) return ltb_set_error(ctx, LTB_EUNSUPPORTED, "svd: slice columns too long for the blocked tier");
-  g.b = (int)std::min<size_t>(std::min<size_t>(32, (size_t)std::max(1, (g.n + 1) / 2)), fit);
+  g.b = (int)std::min<size_t>(std::min<size_t>((size_t)ntmax / 32, (size_t)std::max(1, (g.n + 1) / 2)), fit);
   g.nb = (g.n + g.b - 1) / g.b;
-  const int nbp = g.nb + (g.nb & 1);
   T* W = nullptr;
   int* flags = nullptr;
   LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * (size_t)batch * g.n * g.mp, (void**)&W));
@@ -850,26 +914,19 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
     block_load_kernel<T, WANT_V><<<grid, 256, 0, ctx->stream>>>(I1, I2, A, W, g);
     LTB_LAUNCH_CHECK(ctx);
   }
-  const size_t smem = 2 * colb * g.b + 2 * g.b * sizeof(R) + 16;
-  auto kern = jacobi_block_kernel<T, WANT_V>;
-  LTB_TRY(ensure_smem(ctx, kern, smem));
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(ctx->stream, &cap);
-  const dim3 bgrid((unsigned)(nbp / 2), (unsigned)batch);
-  const int threads = 32 * std::min(g.b, 32);
   if (g.n > 1) {
-    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-      for (int r = 0; r < nbp - 1; ++r) {
-        kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip);
-        LTB_LAUNCH_CHECK(ctx);
-      }
-      block_sweep_update_kernel<<<1, 256, 0, ctx->stream>>>(batch, rot, active, count, o.stats);
-      LTB_LAUNCH_CHECK(ctx);
-      if (cap != cudaStreamCaptureStatusNone) continue;  // no host read-back inside a capture
-      LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-      if (*reinterpret_cast<int*>(ctx->h_scratch) == 0) break;
+    int st = LTB_OK;
+    if constexpr (!WANT_V && (f32 || c32)) {
+      if (mpl == 8) st = run_block_sweeps<T, WANT_V, 8, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
+      else if (mpl == 16 && f32) st = run_block_sweeps<T, WANT_V, 16, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
+      else if (mpl == 16) st = run_block_sweeps<T, WANT_V, 16, 512>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
+      else if (mpl == 32 && f32) st = run_block_sweeps<T, WANT_V, 32, 512>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
+      else if (mpl == 32) st = run_block_sweeps<T, WANT_V, 32, 384>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
+      else st = run_block_sweeps<T, WANT_V, 0, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
+    } else {
+      st = run_block_sweeps<T, WANT_V, 0, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
     }
+    LTB_TRY(st);
   }
   const size_t fsmem = (size_t)g.n * (sizeof(R) + sizeof(int)) + 16;
   auto fin = block_finalize_kernel<T, WANT_V>;
