@@ -168,7 +168,7 @@ __device__ __forceinline__ void split_tile(float4* hi, float4* lo, int ct, int r
 // RB ("resident B"): B is one constant matrix (a transform's Kronecker matrix)
 // of at most kRbMaxKt K-blocks, loaded once per CTA together with its
 // precomputed lo part, so the pipeline streams and splits only A.
-constexpr int kRbMaxKt = 4;
+constexpr int kRbMaxKt = 3;
 
 template <int BN, bool A_MN, bool B_MN, int SPLIT, bool RB>
 struct TcCfg {
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // (slice-major transform input) is fetched unswizzled as [k][32 rows] boxes,
 // read down the rows.  B is split in shared memory by two more warps, or is a
 // resident constant with a precomputed lo part (RB).
-constexpr int kSt3 = 4;                   // pipeline stages
+constexpr int kTm3 = 4;                   // TMEM A stages (hi + lo, 64 columns each)
 constexpr int kConvA = 128, kConvB = 64;  // converter threads (warps 2-5 for A, 6-7 for B)
 
 template <int BN, bool A_MN, bool B_MN, bool RB>
@@ -471,11 +471,16 @@ struct Tc3Cfg {
   static constexpr int A_BYTES = kBM * kBK * 4;  // 16 KB raw A tile
   static constexpr int B_BYTES = BN * kBK * 4;
   static constexpr int STAGE_BYTES = RB ? A_BYTES : A_BYTES + 2 * B_BYTES;  // [A | B_hi | B_lo]
+  // shared-memory ring: with a resident B a stage holds only the raw A tile and is
+  // released as soon as the converters have read it, so a deeper ring keeps more
+  // HBM reads in flight; otherwise B lives in the stage until its MMAs complete
+  static constexpr int SMS = RB ? 7 : 4;
   static constexpr int RES_BYTES = RB ? kRbMaxKt * 2 * B_BYTES : 0;
   static constexpr int EPI_BYTES = 4 * 2 * 4096;
-  static constexpr int SMEM = kSt3 * STAGE_BYTES + RES_BYTES + 1024 + 1024 + EPI_BYTES;
+  static constexpr int SMEM = SMS * STAGE_BYTES + RES_BYTES + 1024 + 1024 + EPI_BYTES;
   static constexpr int ACOL = 2 * BN;  // TMEM column of the first A stage (after two accumulators)
-  static_assert(ACOL + kSt3 * 64 <= 512, "accumulators + A stages must fit in TMEM");
+  static_assert(ACOL + kTm3 * 64 <= 512, "accumulators + A stages must fit in TMEM");
+  static_assert(RB || SMS == kTm3, "without a resident B the shared-memory and TMEM rings advance together");
   static_assert(B_BYTES % 1024 == 0 && STAGE_BYTES % 1024 == 0, "1 KB swizzle-atom alignment");
   static_assert(!RB || !B_MN, "resident B is K-major");
 };
@@ -509,17 +514,30 @@ struct Tc3Extras {
   const float* rscale;   // batch x M, or null
   const float* cscale;   // batch x N, or null
   const int* skip;       // device flag, or null
+  float* c_direct;       // C^T output written with coalesced per-column stores (lanes = rows), or null
+  int64_t ldc, sc;
 };
 
 template <int BN, bool A_MN, bool B_MN, bool RB>
 __global__ void __launch_bounds__(kThreads, 1)
     tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC, int M, int N,
-               int K, int batches, uint32_t mn_lbo, uint32_t mn_sbo, int ct, Tc3Extras ex) {
+               int K, int batches, uint32_t mn_lbo, uint32_t mn_sbo, int ct, Tc3Extras ex,
+               unsigned long long* dbg) {
   using Cfg = Tc3Cfg<BN, A_MN, B_MN, RB>;
+  // optional timeline (CTA 0, %globaltimer ns): same slots as tc_gemm_tf32_kernel
+  auto stamp = [&](int slot) {
+    if (dbg && blockIdx.x == 0) {
+      unsigned long long tns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+      dbg[slot] = tns;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* res = base + kSt3 * Cfg::STAGE_BYTES;
+  constexpr int SMS = Cfg::SMS;
+  unsigned char* res = base + SMS * Cfg::STAGE_BYTES;
   auto a_raw = [&](int s) { return base + s * Cfg::STAGE_BYTES; };
   auto b_hi = [&](int s, int kt) {
     return RB ? res + kt * 2 * Cfg::B_BYTES : base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES;
@@ -528,13 +546,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     return RB ? res + kt * 2 * Cfg::B_BYTES + Cfg::B_BYTES : base + s * Cfg::STAGE_BYTES + Cfg::A_BYTES + Cfg::B_BYTES;
   };
   uint64_t* bars = reinterpret_cast<uint64_t*>(res + Cfg::RES_BYTES);
-  uint64_t* full = bars;               // TMA landed
-  uint64_t* conv = bars + kSt3;        // A in TMEM (and B split) for the stage
-  uint64_t* empty = bars + 2 * kSt3;   // MMAs of the stage completed
-  uint64_t* accf = bars + 3 * kSt3;    // [2] accumulator ready
-  uint64_t* acce = bars + 3 * kSt3 + 2;
-  uint64_t* bres = bars + 3 * kSt3 + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kSt3 + 5);
+  uint64_t* full = bars;                  // [SMS] TMA landed
+  uint64_t* sfree = bars + SMS;           // [SMS] smem stage reusable
+  uint64_t* tfull = bars + 2 * SMS;       // [kTm3] A in TMEM (and B split) for the k-block
+  uint64_t* tfree = tfull + kTm3;         // [kTm3] MMAs reading the TMEM stage completed
+  uint64_t* accf = tfree + kTm3;          // [2] accumulator ready
+  uint64_t* acce = accf + 2;              // [2] accumulator drained
+  uint64_t* bres = acce + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktiles = (K + kBK - 1) / kBK;
@@ -553,10 +572,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     return (kb + kBK - 1) / kBK;
   };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kSt3; ++s) {
+    for (int s = 0; s < SMS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], kConvA + (RB ? 0 : kConvB));
-      mbar_init(&empty[s], 1);
+      mbar_init(&sfree[s], RB ? kConvA : 1);
+    }
+    for (int s = 0; s < kTm3; ++s) {
+      mbar_init(&tfull[s], kConvA + (RB ? 0 : kConvB));
+      mbar_init(&tfree[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&accf[a], 1);
@@ -581,6 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0) stamp(1);
   // device-side stop flag (PGA), read after the dependency wait: no tiles at all
   if (ex.skip && *ex.skip) total = 0;
 
@@ -600,8 +623,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode(t, b, m0, n0);
         const int kt_b = ktiles_of(b);
         for (int kt = 0; kt < kt_b; ++kt, ++it) {
-          const int s = it % kSt3;
-          mbar_wait(&empty[s], ((it / kSt3) & 1) ^ 1);
+          const int s = it % SMS;
+          mbar_wait(&sfree[s], ((it / SMS) & 1) ^ 1);
+          if (it == 0) stamp(2);
           mbar_expect_tx(&full[s], RB ? Cfg::A_BYTES : Cfg::A_BYTES + Cfg::B_BYTES);
           const int k0 = kt * kBK;
           if (!A_MN) {
@@ -640,11 +664,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       for (int kt = 0; kt < kt_b; ++kt, ++it) {
-        const int s = it % kSt3;
-        mbar_wait(&conv[s], (it / kSt3) & 1);
+        const int s = it % SMS, ts = it % kTm3;
+        mbar_wait(&tfull[ts], (it / kTm3) & 1);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t ahi = tmem + (uint32_t)(Cfg::ACOL + 64 * s), alo = ahi + 32;
+          const uint32_t ahi = tmem + (uint32_t)(Cfg::ACOL + 64 * ts), alo = ahi + 32;
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
             const uint32_t kofb = (B_MN ? 1024u : 32u) * kk;
@@ -654,7 +678,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_tf32_ta(dacc, ahi + 8 * kk, dbl, idesc, 1u);
             umma_tf32_ta(dacc, alo + 8 * kk, dbh, idesc, 1u);
           }
-          umma_commit(&empty[s]);
+          if (it == 0) stamp(4);
+          umma_commit(&tfree[ts]);
+          if (!RB) umma_commit(&sfree[s]);  // B of this smem stage has been read
           if (kt == kt_b - 1) umma_commit(&accf[a]);
         }
         __syncwarp();
@@ -670,8 +696,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode(t, b, m0, n0);
       const int kt_b = ktiles_of(b);
       for (int kt = 0; kt < kt_b; ++kt, ++it) {
-        const int s = it % kSt3;
-        mbar_wait(&full[s], (it / kSt3) & 1);
+        const int s = it % SMS, ts = it % kTm3;
+        mbar_wait(&full[s], (it / SMS) & 1);
         uint32_t hi[32], lo[32];
         const unsigned char* ab = a_raw(s);
         if (!A_MN) {  // 128B-swizzled rows: 16-byte chunk c of row r sits at c ^ (r & 7)
@@ -696,12 +722,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             lo[k] = __float_as_uint(tf32_round(x - h));
           }
         }
-        const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(Cfg::ACOL + 64 * s);
+        if (RB) mbar_arrive(&sfree[s]);  // the raw tile is in registers: the TMA may refill the stage
+        mbar_wait(&tfree[ts], ((it / kTm3) & 1) ^ 1);  // MMAs of the TMEM stage's previous k-block done
+        tc_fence_after();
+        const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(Cfg::ACOL + 64 * ts);
         tmem_st32(tq, hi);
         tmem_st32(tq + 32, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
-        mbar_arrive(&conv[s]);
+        if (it == 0 && threadIdx.x == 64) stamp(3);
+        mbar_arrive(&tfull[ts]);
       }
     }
   } else if (warp < 8) {
@@ -714,8 +744,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode(t, b, m0, n0);
         const int kt_b = ktiles_of(b);
         for (int kt = 0; kt < kt_b; ++kt, ++it) {
-          const int s = it % kSt3;
-          mbar_wait(&full[s], (it / kSt3) & 1);
+          const int s = it % SMS;
+          mbar_wait(&full[s], (it / SMS) & 1);
           float4* bh = reinterpret_cast<float4*>(b_hi(s, kt));
           float4* bl = reinterpret_cast<float4*>(b_lo(s, kt));
 #pragma unroll 4
@@ -726,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 tf32_round(x.w - h.w));
           }
           fence_proxy_async();
-          mbar_arrive(&conv[s]);
+          mbar_arrive(&tfull[s]);  // SMS == kTm3 here
         }
       }
     }
@@ -740,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode(t, b, m0, n0);
       const int a = j & 1;
       mbar_wait(&accf[a], (j >> 1) & 1);
+      if (j == 0 && q == 0 && lane == 0) stamp(5);
       tc_fence_after();
       const int row0 = m0 + 32 * q;
       const bool zero = ktiles_of(b) == 0;
@@ -760,6 +791,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float c = (cs && n0 + c0 + jj < N) ? cs[jj] : 1.f;
             r[jj] = __float_as_uint(__uint_as_float(r[jj]) * rs * c);
           }
+        }
+        if (ct && ex.c_direct) {
+          // C^T: for each output column the 32 lanes hold 32 consecutive rows -> one 128-byte store
+          const int row = row0 + lane;
+          if (row < M) {
+            float* cb = ex.c_direct + (int64_t)b * ex.sc + row;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj)
+              if (n0 + c0 + jj < N) cb[(int64_t)(n0 + c0 + jj) * ex.ldc] = __uint_as_float(r[jj]);
+          }
+          continue;
         }
         unsigned char* box = ebuf + (nbox & 1) * 4096;
         if (lane == 0) bulk_wait_read<1>();
@@ -788,6 +830,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++nbox;
       }
       tc_fence_before();
+      if (j == 0 && q == 0 && lane == 0) stamp(6);
       mbar_arrive(&acce[a]);
     }
     if (lane == 0) bulk_wait_all();
@@ -796,6 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
+    if (lane == 0) stamp(7);
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
@@ -816,6 +860,8 @@ int g_pdl = 1;
 int g_rb = 1;
 // 3xTF32 with A staged in TMEM (tc3_kernel) (1) / split in shared memory (0)
 int g_tc3 = 1;
+// transposed outputs: coalesced direct stores (1) / smem box + TMA store (0)
+int g_ct_direct = 0;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -935,7 +981,8 @@ int launch_tc3(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, mc, M, N, K, (int)batch, g_mn_lbo, g_mn_sbo, ct, ex));
+  LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, mc, M, N, K, (int)batch, g_mn_lbo, g_mn_sbo, ct, ex,
+                                       g_dbg));
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -954,7 +1001,7 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
                     int64_t lda, int64_t sa, bool b_mn, const float* B, int64_t ldb, int64_t sb, float* C,
                     int64_t ldc, int64_t sc, int split, bool c_trans, const float* b_lo, const int* klim,
                     const float* rscale, const float* cscale, const int* skip) {
-  const Tc3Extras ex{klim, rscale, cscale, skip};
+  const Tc3Extras ex{klim, rscale, cscale, skip, (c_trans && g_ct_direct) ? C : nullptr, ldc, sc};
   const bool extras = klim || rscale || cscale || skip;
   if (batch < 1 || M < 1 || N < 1 || K < 1 || batch > 65535) return LTB_EUNSUPPORTED;
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return LTB_EUNSUPPORTED;
@@ -1013,6 +1060,7 @@ extern "C" void ltb_tc_debug_set_epi_mode(int v) { g_epi_mode = v; }
 extern "C" void ltb_tc_debug_set_pdl(int v) { g_pdl = v; }
 extern "C" void ltb_tc_debug_set_rb(int v) { g_rb = v; }
 extern "C" void ltb_tc_debug_set_tc3(int v) { g_tc3 = v; }
+extern "C" void ltb_tc_debug_set_ct_direct(int v) { g_ct_direct = v; }
 extern "C" void ltb_tc_debug_set_timeline(void* d_buf) { g_dbg = (unsigned long long*)d_buf; }
 
 extern "C" void ltb_tc_debug_set_mn_strides(uint32_t lbo, uint32_t sbo) {

@@ -26,7 +26,7 @@ buf = torch.zeros(16, dtype=torch.int64, device="cuda")
 names = ["start", "setup done", "first TMA issued", "first split done", "first MMA commit", "epilogue start",
          "tile stored", "before dealloc", "c0 ld start", "c0 ld done", "c1 ld start", "c1 ld done", "c2 ld start",
          "c2 ld done"]
-for ph, label in ((0, "forward A"), (2, "slice GEMM"), (3, "inverse C")):
+for ph, label in ((0, "forward A (+B when paired)"), (2, "slice GEMM"), (3, "inverse C")):
     for rep in range(3):
         plan.run(a, b, c)
         flush.zero_()
