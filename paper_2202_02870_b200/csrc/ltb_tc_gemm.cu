@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // read down the rows.  B is split in shared memory by two more warps, or is a
 // resident constant with a precomputed lo part (RB).
 constexpr int kTm3 = 4;                   // TMEM A stages (hi + lo, 64 columns each)
+constexpr int kThreads3 = 512;            // 16 warps: TMA, MMA, 4 A converters, 2 B converters, 8 epilogue
 constexpr int kConvA = 128, kConvB = 64;  // converter threads (warps 2-5 for A, 6-7 for B)
 
 template <int BN, bool A_MN, bool B_MN, bool RB>
@@ -474,9 +475,12 @@ struct Tc3Cfg {
   // shared-memory ring: with a resident B a stage holds only the raw A tile and is
   // released as soon as the converters have read it, so a deeper ring keeps more
   // HBM reads in flight; otherwise B lives in the stage until its MMAs complete
-  static constexpr int SMS = RB ? 7 : 4;
+  static constexpr int SMS = RB ? 5 : 4;
   static constexpr int RES_BYTES = RB ? kRbMaxKt * 2 * B_BYTES : 0;
-  static constexpr int EPI_BYTES = 4 * 2 * 4096;
+  // epilogue warps: 8 (two per TMEM lane quarter, alternate 32-column chunks) with a
+  // resident B; 4 otherwise (shared memory is taken by the B stages)
+  static constexpr int EPW = RB ? 8 : 4;
+  static constexpr int EPI_BYTES = EPW * 2 * 4096;
   static constexpr int SMEM = SMS * STAGE_BYTES + RES_BYTES + 1024 + 1024 + EPI_BYTES;
   static constexpr int ACOL = 2 * BN;  // TMEM column of the first A stage (after two accumulators)
   static_assert(ACOL + kTm3 * 64 <= 512, "accumulators + A stages must fit in TMEM");
@@ -519,7 +523,7 @@ struct Tc3Extras {
 };
 
 template <int BN, bool A_MN, bool B_MN, bool RB>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads3, 1)
     tc3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmC, int M, int N,
                int K, int batches, uint32_t mn_lbo, uint32_t mn_sbo, int ct, Tc3Extras ex,
@@ -582,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&accf[a], 1);
-      mbar_init(&acce[a], 128);
+      mbar_init(&acce[a], 32 * Cfg::EPW);
     }
     mbar_init(bres, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -760,10 +764,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 8 + Cfg::EPW) {
     // ---------------------------------------------------------------- epilogue (TMA tensor stores)
-    const int q = warp - 8;
-    unsigned char* ebuf = res + Cfg::RES_BYTES + 1024 + q * 2 * 4096;
+    const int q = warp & 3;                         // TMEM lane quarter
+    const int half = (warp - 8) >> 2;               // chunk parity (EPW == 8) or 0
+    constexpr int CSTEP = 32 * (Cfg::EPW / 4);      // column stride between this warp's chunks
+    unsigned char* ebuf = res + Cfg::RES_BYTES + 1024 + (warp - 8) * 2 * 4096;
     int nbox = 0, j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
       int b, m0, n0;
@@ -776,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool zero = ktiles_of(b) == 0;
       const float rs = (ex.rscale && row0 + lane < M) ? ex.rscale[(int64_t)b * M + row0 + lane] : 1.f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN && n0 + c0 < N; c0 += 32) {
+      for (int c0 = 32 * half; c0 < BN && n0 + c0 < N; c0 += CSTEP) {
         uint32_t r[32];
         if (!zero) {
           tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
@@ -973,7 +979,7 @@ int launch_tc3(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const
   const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kThreads3);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
