@@ -962,9 +962,295 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
   return launch_jacobi_blocked<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
 }
 
+// ---------------------------------------------------------------- QR-preconditioned fp32 SVT
+// For an fp32 SVT the oriented slice W (m x n, m >= n) is first reduced by a
+// Householder QR in shared memory, W = Q R, and the one-sided Jacobi runs on
+// the n columns of X = R^T (Drmac-Veselic preconditioning): X J = V Sigma, the
+// Jacobi columns y_j = sigma_j v_j are W's right singular vectors scaled by
+// sigma.  The slice shrinks from m to n rows and the sweep count drops (13 ->
+// 9-10 on config-3 iterates, tools/ sweep study); Q is never formed:
+//   svt(W) = W V diag((s - tau)_+ / s) V^T = W (Y~ Y~^T),  y~_j = y_j sqrt((s_j - tau)_+ / s_j) / s_j,
+// so the kernel emits Y~ (sorted, scaled) and two tensor-core GEMMs finish:
+// Z = Y~ Y~^T, then out = A Z (I1 >= I2) or Z A (I1 < I2).
+template <int TS, int MPL, int MINB>
+__global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
+    jacobi_qr_kernel(int64_t I1, int64_t I2, const float* __restrict__ A, JacobiOut o, int max_sweeps, int pitch) {
+  if (o.skip && *o.skip) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const bool trans = I1 < I2;
+  const int m = (int)(trans ? I2 : I1);
+  const int n = (int)(trans ? I1 : I2);
+  const int64_t b = blockIdx.x;
+  const float* Ab = A + b * I1 * I2;
+  float* W = reinterpret_cast<float*>(smem_raw);  // n columns, pitch >= max(m, TS * MPL), even
+  float* vhead = W + (size_t)n * pitch;           // v_k[0] of the reflectors
+  float* beta = vhead + n;
+  float* nrm = beta + n;                          // n + 1
+  int* flags = reinterpret_cast<int*>(nrm + n + 1);
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+  constexpr int TR = TS * MPL;  // register-tile rows of X (rows n..TR-1 are zero)
+
+  if (!trans) {
+    for (int l = tid; l < m * n; l += nth) {
+      const int i = l / n, j = l - i * n;
+      W[(size_t)j * pitch + i] = Ab[l];
+    }
+  } else {
+    for (int l = tid; l < m * n; l += nth) {
+      const int j = l / m, i = l - j * m;
+      W[(size_t)j * pitch + i] = Ab[l];
+    }
+  }
+  if (tid < 4) flags[tid] = 0;
+  __syncthreads();
+  // ||A||_F <= tau: nothing survives the threshold (sigma_max <= ||A||_F)
+  if (warp == 0) {
+    float s2 = 0.f;
+    for (int l = lane; l < m * n; l += 32) {
+      const int j = l / m, i = l - j * m;
+      const float v = W[(size_t)j * pitch + i];
+      s2 += v * v;
+    }
+    s2 = warp_sum(s2);
+    if (lane == 0) flags[3] = (o.tau > 0.0 && (double)s2 <= o.tau * o.tau) ? 1 : 0;
+  }
+  __syncthreads();
+  if (flags[3]) {
+    if (tid == 0) {
+      if (o.kept_out) o.kept_out[b] = 0;
+      if (o.stats) atomicAdd(&o.stats[0], 1ull);
+    }
+    return;
+  }
+
+  // ---- Householder QR: R on and above the diagonal, v_k below it (v_k[0] in vhead)
+  for (int k = 0; k < n; ++k) {
+    float* wk = W + (size_t)k * pitch;
+    if (warp == 0) {
+      float s2 = 0.f;
+      for (int i = k + 1 + lane; i < m; i += 32) s2 += wk[i] * wk[i];
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        const float x0 = wk[k];
+        const float nx = sqrtf(x0 * x0 + s2);
+        const float alpha = x0 >= 0.f ? -nx : nx;
+        const float v0 = x0 - alpha;
+        const float vv = v0 * v0 + s2;
+        // a numerically zero column (vv below FLT_MIN: 2 / vv would overflow) is left alone
+        const bool refl = vv >= FLT_MIN;
+        beta[k] = refl ? 2.f / vv : 0.f;
+        vhead[k] = v0;
+        if (refl) wk[k] = alpha;
+      }
+    }
+    __syncthreads();
+    const float bk = beta[k], v0 = vhead[k];
+    if (bk != 0.f) {
+      for (int j = k + 1 + warp; j < n; j += nwarps) {
+        float* wj = W + (size_t)j * pitch;
+        float dot = (lane == 0) ? v0 * wj[k] : 0.f;
+        for (int i = k + 1 + lane; i < m; i += 32) dot += wk[i] * wj[i];
+        dot = warp_sum(dot) * bk;
+        if (lane == 0) wj[k] -= dot * v0;
+        for (int i = k + 1 + lane; i < m; i += 32) wj[i] -= dot * wk[i];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- X = R^T in place: R[i][j] (row i < column j, upper triangle) moves to column i,
+  // row j (below the diagonal, where the reflector lived); then clear the upper triangle
+  // and the rows n .. TR-1
+  for (int l = tid; l < n * n; l += nth) {
+    const int i = l / n, j = l - i * n;
+    if (j > i) W[(size_t)i * pitch + j] = W[(size_t)j * pitch + i];
+  }
+  __syncthreads();
+  for (int l = tid; l < n * TR; l += nth) {
+    const int i = l / TR, j = l - i * TR;
+    if (j < i || j >= n) W[(size_t)i * pitch + j] = 0.f;
+  }
+  __syncthreads();
+
+  // ---- one-sided Jacobi on the n columns of X (n rows), as jacobi_kernel's fp32 path
+  const float tol = FLT_EPSILON * sqrtf((float)max(n, 1));
+  const int npl = n + (n & 1);
+  const int npairs = npl / 2;
+  constexpr int TPW = 32 / TS;
+  const int tl = lane % TS;
+  const int team = lane / TS;
+  int sweeps_done = 0;
+  for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
+    int* rot = &flags[sweep & 1];
+    for (int j = warp; j < n; j += nwarps) {
+      const float* wj = W + (size_t)j * pitch;
+      float s2 = 0.f;
+      for (int i = lane; i < n; i += 32) s2 += wj[i] * wj[i];
+      s2 = warp_sum(s2);
+      if (lane == 0) nrm[j] = s2;
+    }
+    __syncthreads();
+    for (int r = 0; r < npl - 1; ++r) {
+      for (int base = warp * TPW; base < npairs; base += nwarps * TPW) {
+        const int k = base + team;
+        int p = 0, q = 0;
+        if (k < npairs) {
+          const int m1 = npl - 1;
+          if (k == 0) {
+            p = m1;
+            q = r;
+          } else {
+            p = r + k;
+            p -= (p >= m1) ? m1 : 0;
+            q = r - k;
+            q += (q < 0) ? m1 : 0;
+          }
+        }
+        const bool active = k < npairs && p < n && q < n;
+        float* wp = W + (size_t)(active ? p : 0) * pitch;
+        float* wq = W + (size_t)(active ? q : 0) * pitch;
+        float2 X2[MPL / 2], Y2[MPL / 2];
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int h = 0; h < MPL / 2; ++h) {
+          const int i = 2 * tl + 2 * TS * h;
+          X2[h] = *reinterpret_cast<const float2*>(wp + i);
+          Y2[h] = *reinterpret_cast<const float2*>(wq + i);
+          acc = __ffma2_rn(X2[h], Y2[h], acc);
+        }
+        float g = acc.x + acc.y;
+#pragma unroll
+        for (int off = TS / 2; off > 0; off >>= 1) g += __shfl_xor_sync(0xffffffffu, g, off);
+        const float al = active ? nrm[p] : 0.f;
+        const float be = active ? nrm[q] : 0.f;
+        const float gabs = fabsf(g);
+        if (!active || !(gabs > tol * sqrt_apx(al) * sqrt_apx(be)) || !(fminf(fminf(al, be), gabs) >= FLT_MIN)) continue;
+        const float zeta = (be - al) * (0.5f * rcp_apx(gabs));
+        const float az = fabsf(zeta);
+        const float den = az < 1e18f ? az + sqrt_apx(fmaf(az, az, 1.f)) : 2.f * az;
+        const float t = copysignf(rcp_apx(den), zeta);
+        const float x1 = fmaf(t, t, 1.f);
+        float c = rsqrt_apx(x1);
+        c = c * fmaf(-0.5f * x1 * c, c, 1.5f);
+        const float sn = c * t;
+        const float sg = g >= 0.f ? 1.f : -1.f;
+        const float2 C2 = make_float2(c, c), S2 = make_float2(sn, sn);
+        const float2 NSQ = make_float2(-sn * sg, -sn * sg), CQ = make_float2(c * sg, c * sg);
+#pragma unroll
+        for (int h = 0; h < MPL / 2; ++h) {
+          const int i = 2 * tl + 2 * TS * h;
+          *reinterpret_cast<float2*>(wp + i) = __ffma2_rn(C2, X2[h], __fmul2_rn(NSQ, Y2[h]));
+          *reinterpret_cast<float2*>(wq + i) = __ffma2_rn(S2, X2[h], __fmul2_rn(CQ, Y2[h]));
+        }
+        if (tl == 0) {
+          nrm[p] = fmaxf(al - t * gabs, 0.f);
+          nrm[q] = be + t * gabs;
+          *rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int any = *rot;
+    __syncthreads();
+    if (tid == 0) flags[(sweep + 1) & 1] = 0;
+    __syncthreads();
+    sweeps_done = sweep + 1;
+    if (!any) break;
+  }
+  if (o.stats && tid == 0) {
+    atomicAdd(&o.stats[0], 1ull);
+    atomicAdd(&o.stats[1], (unsigned long long)sweeps_done);
+  }
+  // ---- singular values, descending ranks, scaled columns y~_j
+  float* sig = nrm;
+  for (int j = warp; j < n; j += nwarps) {
+    const float* wj = W + (size_t)j * pitch;
+    float s2 = 0.f;
+    for (int i = lane; i < n; i += 32) s2 += wj[i] * wj[i];
+    s2 = warp_sum(s2);
+    if (lane == 0) sig[j] = sqrtf(s2);
+  }
+  if (tid == 0) flags[2] = 0;
+  __syncthreads();
+  int* rank_sh = flags + 4;
+  float* scale = beta;  // reuse: per-column output scale
+  int kept_local = 0;
+  for (int j = tid; j < n; j += nth) {
+    const float sj = sig[j];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) {
+      const float si = sig[i];
+      rank += (si > sj) || (si == sj && i < j);
+    }
+    rank_sh[j] = rank;
+    const bool keep = sj > (float)o.tau && sj > 0.f;
+    kept_local += keep;
+    scale[j] = keep ? sqrtf((sj - (float)o.tau) / sj) / sj : 0.f;
+  }
+  if (kept_local) atomicAdd(&flags[2], kept_local);
+  __syncthreads();
+  if (o.kept_out && tid == 0) o.kept_out[b] = flags[2];
+  float* dst = reinterpret_cast<float*>(o.w_out) + b * (int64_t)n * n;
+  for (int l = tid; l < n * n; l += nth) {
+    const int j = l / n, i = l - j * n;
+    dst[(int64_t)rank_sh[j] * n + i] = W[(size_t)j * pitch + i] * scale[j];
+  }
+}
+
+size_t jacobi_qr_smem(int n, int pitch) { return ((size_t)n * pitch + 4 * (size_t)n + 1) * 4 + (n + 8) * 4 + 16; }
+
+template <int TS, int MPL, int MINB>
+int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o,
+                      int max_sweeps, int n, int pitch) {
+  const size_t smem = jacobi_qr_smem(n, pitch);
+  const int pairs = std::max(1, (n + 1) / 2);
+  const int maxw = MINB == 2 ? 18 : 32;
+  const int teams = std::max(1, (pairs * TS + 31) / 32);
+  const int per_warp = (teams + maxw - 1) / maxw;
+  const int nwarps = std::max(1, (teams + per_warp - 1) / per_warp);
+  auto kern = jacobi_qr_kernel<TS, MPL, MINB>;
+  LTB_TRY(ensure_smem(ctx, kern, smem, true));
+  kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, o, max_sweeps, pitch);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
+
+// 1 when the QR-preconditioned resident kernel takes this fp32 SVT; 0 to use the others
+int g_svt_qr = 1;
+
+// LTB_EUNSUPPORTED when the shape does not fit the QR-preconditioned kernel
+int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o) {
+  const int m = (int)std::max(I1, I2), n = (int)std::min(I1, I2);
+  if (!g_svt_qr || g_force_blocked || n < 32 || batch > 0x7fffffff) return LTB_EUNSUPPORTED;
+  int TSv = 16, MPLv = 0;
+  if (n <= 64) MPLv = 4;
+  else if (n <= 128) MPLv = 8;
+  else if (n <= 160) MPLv = 10;
+  else if (n <= 192) MPLv = 12;
+  else if (n <= 256) { TSv = 32; MPLv = 8; }
+  else return LTB_EUNSUPPORTED;
+  int pitch = std::max(m, TSv * MPLv);
+  pitch += pitch & 1;
+  const size_t smem = jacobi_qr_smem(n, pitch);
+  if (smem > kSmemLimit) return LTB_EUNSUPPORTED;
+  const bool two = 2 * (smem + 1024) <= 228 * 1024;
+  const int ms = 40;
+#define LTB_QR(TS_, MPL_) \
+  return two ? launch_qr_variant<TS_, MPL_, 2>(ctx, batch, I1, I2, A, o, ms, n, pitch) \
+             : launch_qr_variant<TS_, MPL_, 1>(ctx, batch, I1, I2, A, o, ms, n, pitch)
+  if (TSv == 32) { LTB_QR(32, 8); }
+  switch (MPLv) {
+    case 4: LTB_QR(16, 4);
+    case 8: LTB_QR(16, 8);
+    case 10: LTB_QR(16, 10);
+    default: LTB_QR(16, 12);
+  }
+#undef LTB_QR
+}
+
 }  // namespace
 
 extern "C" void ltb_debug_set_svd_blocked(int v) { g_force_blocked = v; }
+extern "C" void ltb_debug_set_svt_qr(int v) { g_svt_qr = v; }
 
 // SVT of `batch` row-major I1 x I2 slices: out = U (S - tau)_+ V^H
 int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2, const void* d_a, double tau,
@@ -977,6 +1263,34 @@ int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2,
     using R = typename scalar_traits<T>::real;
     const bool trans = I1 < I2;
     const int64_t m = trans ? I2 : I1, n = trans ? I1 : I2;
+    if constexpr (std::is_same<T, float>::value) {
+      // QR-preconditioned Jacobi: Y~ (n x n per slice), then Z = Y~ Y~^T and out = A Z | Z A
+      float* y = nullptr;
+      float* z = nullptr;
+      int* kept = nullptr;
+      LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * n * n, (void**)&y));
+      LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * n * n, (void**)&z));
+      LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * batch, (void**)&kept));
+      JacobiOut o{y, nullptr, nullptr, kept, nullptr, tau, d_skip};
+      o.stats = ctx->d_stats;
+      const int st = launch_jacobi_qr(ctx, batch, I1, I2, (const float*)d_a, o);
+      if (st == LTB_OK) {
+        const float* A = (const float*)d_a;
+        // Z = Y~ Y~^T: y stores the columns of Y~ as rows (K = rank index, limited to the kept count)
+        LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, n, n, n, LTB_OP_T, y, n, n * n, LTB_OP_N, y, n, n * n, z, n, n * n,
+                              nullptr, nullptr, kept, nullptr, nullptr, d_skip));
+        if (!trans)  // out = A Z  (I1 x n)
+          LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, I1, n, n, LTB_OP_N, A, I2, I1 * I2, LTB_OP_N, z, n, n * n,
+                                (float*)d_out, I2, I1 * I2, nullptr, nullptr, nullptr, nullptr, nullptr, d_skip));
+        else  // out = Z A  (n x I2)
+          LTB_TRY(ltb_gemm_impl(ctx, dtype, batch, n, I2, n, LTB_OP_N, z, n, n * n, LTB_OP_N, A, I2, I1 * I2,
+                                (float*)d_out, I2, I1 * I2, nullptr, nullptr, nullptr, nullptr, nullptr, d_skip));
+      }
+      ltb_ws_free(ctx, y);
+      ltb_ws_free(ctx, z);
+      ltb_ws_free(ctx, kept);
+      if (st != LTB_EUNSUPPORTED) return st;
+    }
     T* w = nullptr;
     T* z = nullptr;
     R* d = nullptr;

@@ -262,3 +262,28 @@ def test_spec_svt_mirror_matches_full(kind, shape):
     nat.check(nat.lib().ltb_spec_slice_svt(nat.context(), TR.device_spec(spec, shape[2:]).ptr, hat.code, P, i1, i2,
                                            hat.ptr, tau, mirr.ptr))
     np.testing.assert_array_equal(mirr.numpy(), full.numpy())
+
+
+# ---- fp32 SVT through the QR-preconditioned kernel: rank-deficient, zero and duplicated-column
+# slices (Householder steps with vanishing columns), both orientations
+@pytest.mark.parametrize("shape", [(40, 50), (50, 40), (64, 64), (150, 170)])
+def test_svt_qr_rank_deficient(shape):
+    rng = np.random.default_rng(31)
+    m, n = shape
+    batch = 4
+    a = np.zeros((batch, m, n), np.float32)
+    a[0] = (rng.standard_normal((m, 5)) @ rng.standard_normal((5, n))).astype(np.float32)  # rank 5
+    a[1] = 0.0                                                                              # zero slice
+    col = rng.standard_normal((m, 1))
+    a[2] = np.repeat(col, n, axis=1).astype(np.float32)                                     # rank 1, equal columns
+    a[3] = rng.standard_normal((m, n)).astype(np.float32)                                   # full rank
+    u, s, vh = np.linalg.svd(a.astype(np.float64), full_matrices=False)
+    tau = 0.5
+    ref = np.matmul(u * np.maximum(s - tau, 0)[:, None, :], vh)
+    da = nat.DeviceArray.from_numpy(a)
+    out = nat.DeviceArray(a.shape, np.float32)
+    nat.check(nat.lib().ltb_slice_svt(nat.context(), nat.dtype_code(np.float32), batch, m, n, da.ptr, tau, out.ptr))
+    got = out.numpy()
+    for i in range(batch):
+        den = max(np.linalg.norm(ref[i]), 1e-30)
+        assert np.linalg.norm(got[i] - ref[i]) / den < 1e-4 or np.linalg.norm(got[i]) < 1e-6
