@@ -1182,6 +1182,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
       rank += (si > sj) || (si == sj && i < j);
     }
     rank_sh[j] = rank;
+    if (o.sv_out) reinterpret_cast<float*>(o.sv_out)[b * n + rank] = sj;
     const bool keep = sj > (float)o.tau && sj > 0.f;
     kept_local += keep;
     scale[j] = keep ? sqrtf((sj - (float)o.tau) / sj) / sj : 0.f;
@@ -1189,6 +1190,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   if (kept_local) atomicAdd(&flags[2], kept_local);
   __syncthreads();
   if (o.kept_out && tid == 0) o.kept_out[b] = flags[2];
+  if (!o.w_out) return;
   float* dst = reinterpret_cast<float*>(o.w_out) + b * (int64_t)n * n;
   for (int l = tid; l < n * n; l += nth) {
     const int j = l / n, i = l - j * n;
@@ -1404,6 +1406,11 @@ extern "C" int ltb_slice_singular_values(ltb_ctx* ctx, int dtype, int64_t batch,
   return dispatch_dtype(dtype, [&](auto tg) -> int {
     using T = typename decltype(tg)::type;
     JacobiOut o{nullptr, d_s, nullptr, nullptr, nullptr, 0.0, nullptr};
+    if constexpr (std::is_same<T, float>::value) {  // sigma only: QR-preconditioned kernel when it fits
+      o.stats = ctx->d_stats;
+      const int st = launch_jacobi_qr(ctx, batch, I1, I2, (const float*)d_a, o);
+      if (st != LTB_EUNSUPPORTED) return st;
+    }
     return launch_jacobi<T, false>(ctx, batch, I1, I2, (const T*)d_a, o);
   });
 }
