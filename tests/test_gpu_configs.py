@@ -97,7 +97,7 @@ def test_config5_svt_and_tsvd(n):
     f = L.t_svd(a, spec)
     # singular values (device slice order -> reference p-order) and the factor-independent S
     sv = L.linalg._singular_values(a, spec)[core.slice_order_permutation(a.shape[2:])]
-    assert rel_err(sv, sv_ref) < 1e-5
+    assert rel_err(sv, sv_ref) < 1e-4  # north_star fp32 tolerance (QR-preconditioned sigma: normwise accurate)
     assert rel_err(np.sort(f.tube_norms)[::-1], f.tube_norms) == 0.0
     assert abs(float((f.tube_norms ** 2).sum()) - float((a.astype(np.float64) ** 2).sum())) \
         < 1e-4 * float((a.astype(np.float64) ** 2).sum())
