@@ -497,8 +497,32 @@ def bench_pga(L, nat, torch, args):
     slices, sweeps = nat.jacobi_stats(reset=True)
     x = solver.fetch(False)
     solver.close()
+    # K3 alone on a late-iteration-sized problem: the config-3 transform-domain stack of the
+    # observed data at tau = mu_150, timed on the device (nominal SVD flops)
+    hat = L.linalg._hat_stack(np.where(mask, m, 0).astype(np.float32), spec)
+    P3, i1, i2 = hat.shape
+    hout = nat.DeviceArray(hat.shape, hat.dtype)
+    tau = float(mus[min(149, len(mus) - 1)])
+    for _ in range(2):
+        nat.check(nat.lib().ltb_slice_svt(nat.context(), hat.code, P3, i1, i2, hat.ptr, tau, hout.ptr))
+    nat.sync()
+    t0 = time.perf_counter()
+    nat.check(nat.lib().ltb_slice_svt(nat.context(), hat.code, P3, i1, i2, hat.ptr, tau, hout.ptr))
+    nat.sync()
+    t_k3 = time.perf_counter() - t0
+    mm, nn = max(i1, i2), min(i1, i2)
+    k3_flop = P3 * (6 * mm * nn * nn + 20 * nn ** 3 + 2 * mm * nn * nn)
+    fp32_peak = 74.4
+    roof = {"kernel": "K3 SVT (QR-preconditioned one-sided Jacobi + recomposition)", "bound": "fp32",
+            "achieved": k3_flop / t_k3 / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": k3_flop / t_k3 / 1e12 / fp32_peak, "traffic": None,
+            "alg_per_launch": f"{k3_flop} flop nominal (300 slices x (6mn^2 + 20n^3 + 2mn^2))",
+            "peak_source": "FP32 FFMA nominal 148 SM x 128 x 2 x 1.965 GHz (SURVEY.md §8(d))",
+            "k3_ms": t_k3 * 1e3,
+            "iteration_ceiling_it_s": 2466, "iteration_frac": (n_done / dt) / 2466,
+            "ceiling_source": "SURVEY.md §8(d): max(HBM 305.1 MB, 26.67 GFLOP) per iteration"}
     return {"metric": "PGA completion iters/sec", "value": n_done / dt, "unit": "it/s", "iterations": n_done,
-            "seconds": dt, "dtype": "f32", "jacobi_sweeps_per_slice": sweeps / max(slices, 1),
+            "seconds": dt, "dtype": "f32", "jacobi_sweeps_per_slice": sweeps / max(slices, 1), "roofline": roof,
             "config": {"workload": "config3 144x176x3x100 rank-10 DCT(modes 3,4), Bernoulli(0.2), tol 1e-300",
                        "data": "synthetic stand-in for the paper's colour videos (not in this container)"},
             "rse_vs_m": float(np.linalg.norm(x - m) ** 2 / max(np.linalg.norm(x) ** 2, 1e-300))}
