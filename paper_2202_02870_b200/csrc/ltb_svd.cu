@@ -1079,6 +1079,13 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   const int tl = lane % TS;
   const int team = lane / TS;
   int sweeps_done = 0;
+  // circle-method slots of this thread's team: slot t handles pair k = base_t + team; the
+  // pair of round r is p = (r + k) mod m1, q = (r - k) mod m1 (k = 0: p = m1, q = r), so
+  // both advance by one per round and no index arithmetic is redone per pass
+  const int m1 = npl - 1;
+  const int stride = nwarps * TPW;
+  const int nslot = (npairs + stride - 1) / stride;  // <= 4 for every launched shape
+  const float* const Wc = W + 2 * tl;
   for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
     int* rot = &flags[sweep & 1];
     for (int j = warp; j < n; j += nwarps) {
@@ -1089,32 +1096,30 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
       if (lane == 0) nrm[j] = s2;
     }
     __syncthreads();
-    for (int r = 0; r < npl - 1; ++r) {
-      for (int base = warp * TPW; base < npairs; base += nwarps * TPW) {
-        const int k = base + team;
-        int p = 0, q = 0;
-        if (k < npairs) {
-          const int m1 = npl - 1;
-          if (k == 0) {
-            p = m1;
-            q = r;
-          } else {
-            p = r + k;
-            p -= (p >= m1) ? m1 : 0;
-            q = r - k;
-            q += (q < 0) ? m1 : 0;
-          }
-        }
+    int ps[4], qs[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int k = warp * TPW + t * stride + team;
+      ps[t] = (k == 0) ? m1 : k;
+      qs[t] = (k == 0) ? 0 : m1 - k;
+    }
+    for (int r = 0; r < m1; ++r) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (t >= nslot) break;
+        const int k = warp * TPW + t * stride + team;
+        const int p = ps[t], q = qs[t];
+        ps[t] = (k == 0) ? m1 : (p + 1 == m1 ? 0 : p + 1);
+        qs[t] = (q + 1 == m1) ? 0 : q + 1;
         const bool active = k < npairs && p < n && q < n;
-        float* wp = W + (size_t)(active ? p : 0) * pitch;
-        float* wq = W + (size_t)(active ? q : 0) * pitch;
+        float* wp = const_cast<float*>(Wc) + (size_t)(active ? p : 0) * pitch;
+        float* wq = const_cast<float*>(Wc) + (size_t)(active ? q : 0) * pitch;
         float2 X2[MPL / 2], Y2[MPL / 2];
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
         for (int h = 0; h < MPL / 2; ++h) {
-          const int i = 2 * tl + 2 * TS * h;
-          X2[h] = *reinterpret_cast<const float2*>(wp + i);
-          Y2[h] = *reinterpret_cast<const float2*>(wq + i);
+          X2[h] = *reinterpret_cast<const float2*>(wp + 2 * TS * h);
+          Y2[h] = *reinterpret_cast<const float2*>(wq + 2 * TS * h);
           acc = __ffma2_rn(X2[h], Y2[h], acc);
         }
         float g = acc.x + acc.y;
@@ -1127,23 +1132,22 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
         const float zeta = (be - al) * (0.5f * rcp_apx(gabs));
         const float az = fabsf(zeta);
         const float den = az < 1e18f ? az + sqrt_apx(fmaf(az, az, 1.f)) : 2.f * az;
-        const float t = copysignf(rcp_apx(den), zeta);
-        const float x1 = fmaf(t, t, 1.f);
+        const float tt = copysignf(rcp_apx(den), zeta);
+        const float x1 = fmaf(tt, tt, 1.f);
         float c = rsqrt_apx(x1);
         c = c * fmaf(-0.5f * x1 * c, c, 1.5f);
-        const float sn = c * t;
+        const float sn = c * tt;
         const float sg = g >= 0.f ? 1.f : -1.f;
         const float2 C2 = make_float2(c, c), S2 = make_float2(sn, sn);
         const float2 NSQ = make_float2(-sn * sg, -sn * sg), CQ = make_float2(c * sg, c * sg);
 #pragma unroll
         for (int h = 0; h < MPL / 2; ++h) {
-          const int i = 2 * tl + 2 * TS * h;
-          *reinterpret_cast<float2*>(wp + i) = __ffma2_rn(C2, X2[h], __fmul2_rn(NSQ, Y2[h]));
-          *reinterpret_cast<float2*>(wq + i) = __ffma2_rn(S2, X2[h], __fmul2_rn(CQ, Y2[h]));
+          *reinterpret_cast<float2*>(wp + 2 * TS * h) = __ffma2_rn(C2, X2[h], __fmul2_rn(NSQ, Y2[h]));
+          *reinterpret_cast<float2*>(wq + 2 * TS * h) = __ffma2_rn(S2, X2[h], __fmul2_rn(CQ, Y2[h]));
         }
         if (tl == 0) {
-          nrm[p] = fmaxf(al - t * gabs, 0.f);
-          nrm[q] = be + t * gabs;
+          nrm[p] = fmaxf(al - tt * gabs, 0.f);
+          nrm[q] = be + tt * gabs;
           *rot = 1;
         }
       }
@@ -1209,6 +1213,7 @@ int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const
   const int teams = std::max(1, (pairs * TS + 31) / 32);
   const int per_warp = (teams + maxw - 1) / maxw;
   const int nwarps = std::max(1, (teams + per_warp - 1) / per_warp);
+  if ((pairs + nwarps * (32 / TS) - 1) / (nwarps * (32 / TS)) > 4) return LTB_EUNSUPPORTED;  // <= 4 slots per team
   auto kern = jacobi_qr_kernel<TS, MPL, MINB>;
   LTB_TRY(ensure_smem(ctx, kern, smem, true));
   kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, o, max_sweeps, pitch);
