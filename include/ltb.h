@@ -136,6 +136,14 @@ int ltb_mode_product(ltb_ctx* ctx, int64_t outer, int64_t nin, int64_t inner, in
  * C[b] = op_a(A[b]) * op_b(B[b]) for b < batch; op_a(A) is m x k, op_b(B) is k x n,
  * each stored row-major with the given leading dimension and batch stride.
  */
+/* l_product (linalg.py:34-43) host to host in one pipelined call: real spec, real
+ * float32 / float64 tensors A (I1 x L x trailing), B (L x I2 x trailing) -> C
+ * (I1 x I2 x trailing), C-order host buffers (pinned ones let the copies overlap
+ * the compute in both directions).  LTB_EUNSUPPORTED (no error text) for complex
+ * transform domains, which need the real-output check of the generic path. */
+int ltb_l_product_host(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1, int64_t L, int64_t I2, int dtype,
+                       const void* h_a, const void* h_b, void* h_c);
+
 int ltb_slice_gemm(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, int64_t k,
                    int op_a, const void* d_a, int64_t lda, int64_t stride_a,
                    int op_b, const void* d_b, int64_t ldb, int64_t stride_b,

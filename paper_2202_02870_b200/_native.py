@@ -57,6 +57,7 @@ _SIGNATURES = {
     "ltb_spec_destroy": ([_vp], None),
     "ltb_transform": ([_vp, _vp, _i64, _int, _int, _int, _vp, _int, _int, _vp, _dp], _int),
     "ltb_transform_pair": ([_vp, _vp, _i64, _int, _int, _int, _vp, _vp, _int, _int, _vp, _vp], _int),
+    "ltb_l_product_host": ([_vp, _vp, _i64, _i64, _i64, _int, _vp, _vp, _vp], _int),
     "ltb_mode_product": ([_vp, _i64, _i64, _i64, _i64, _int, _vp, _int, _vp, _int, _vp], _int),
     "ltb_slice_gemm": ([_vp, _int, _i64, _i64, _i64, _i64, _int, _vp, _i64, _i64, _int, _vp, _i64, _i64,
                         _vp, _i64, _i64], _int),

@@ -132,6 +132,8 @@ struct ltb_ctx {
   double* d_scratch = nullptr;  // 64 doubles
   unsigned int* d_counter = nullptr;
   unsigned long long* d_stats = nullptr;  // [0] Jacobi slices, [1] Jacobi sweeps
+  // copy streams of the pipelined host-to-host l_product (created on first use)
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
 };
 
 struct ltb_spec {

@@ -98,6 +98,20 @@ def l_product(a, b, spec: TransformSpec, *, out: np.ndarray | None = None) -> np
     m, k, n = a.shape[0], a.shape[1], b.shape[1]
     trailing = a.shape[2:]
     P = num_rep(a.shape)
+    if (a.dtype == b.dtype and a.dtype in (np.float32, np.float64) and not spec.is_complex and spec.modes
+            and hat_dtype == a.dtype):
+        # real transform domain: one pipelined native call (host copies overlap the compute)
+        c_shape = (m, n) + tuple(trailing)
+        res = out if out is not None else np.empty(c_shape, a.dtype)
+        if res.shape != c_shape or res.dtype != a.dtype or not res.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous {a.dtype} array of shape {c_shape}")
+        ac, bc = np.ascontiguousarray(a), np.ascontiguousarray(b)
+        st = nat.lib().ltb_l_product_host(nat.context(), device_spec(spec, trailing).ptr, m, k, n,
+                                          nat.dtype_code(a.dtype), ac.ctypes.data_as(C.c_void_p),
+                                          bc.ctypes.data_as(C.c_void_p), res.ctypes.data_as(C.c_void_p))
+        if st != 3:  # LTB_EUNSUPPORTED -> the generic path below
+            nat.check(st)
+            return res
     if a.dtype == b.dtype and np.isrealobj(a) and m * k == k * n and spec.modes:
         # K1 of both operands in one call (one tensor-core launch on the fp32 path)
         src_dtype = nat.real_of(hat_dtype)
