@@ -700,12 +700,18 @@ __global__ void __launch_bounds__(NTMAX, 1)
       T* y = C + (size_t)q * mp;
       T ga = zero_v<T>();
       T xr[MPL > 0 ? MPL : 1], yr[MPL > 0 ? MPL : 1];
-      if constexpr (MPL > 0) {  // rows past m are zero padding
+      if constexpr (MPL > 0) {  // rows past m are zero padding; two consecutive rows per vector access
 #pragma unroll
-        for (int e = 0; e < MPL; ++e) {
-          xr[e] = x[lane + 32 * e];
-          yr[e] = y[lane + 32 * e];
+        for (int e = 0; e < MPL; e += 2) {
+          const int i = 2 * lane + 32 * e;
+          const vec2<T> vx = *reinterpret_cast<const vec2<T>*>(x + i);
+          const vec2<T> vy = *reinterpret_cast<const vec2<T>*>(y + i);
+          xr[e] = vx.a;
+          xr[e + 1] = vx.b;
+          yr[e] = vy.a;
+          yr[e + 1] = vy.b;
           fma_acc(ga, conj_v(xr[e]), yr[e]);
+          fma_acc(ga, conj_v(xr[e + 1]), yr[e + 1]);
         }
       } else {
         for (int i = lane; i < m; i += 32) fma_acc(ga, conj_v(x[i]), y[i]);
@@ -727,10 +733,16 @@ __global__ void __launch_bounds__(NTMAX, 1)
       }
       if constexpr (MPL > 0) {
 #pragma unroll
-        for (int e = 0; e < MPL; ++e) {
-          const T yv = ph * yr[e];
-          x[lane + 32 * e] = c * xr[e] - sn * yv;
-          y[lane + 32 * e] = sn * xr[e] + c * yv;
+        for (int e = 0; e < MPL; e += 2) {
+          const int i = 2 * lane + 32 * e;
+          const T y0 = ph * yr[e], y1 = ph * yr[e + 1];
+          vec2<T> vx, vy;
+          vx.a = c * xr[e] - sn * y0;
+          vx.b = c * xr[e + 1] - sn * y1;
+          vy.a = sn * xr[e] + c * y0;
+          vy.b = sn * xr[e + 1] + c * y1;
+          *reinterpret_cast<vec2<T>*>(x + i) = vx;
+          *reinterpret_cast<vec2<T>*>(y + i) = vy;
         }
       } else {
         for (int i = lane; i < rows; i += 32) {
