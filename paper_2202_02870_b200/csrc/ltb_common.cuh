@@ -230,6 +230,8 @@ void ltb_ws_free(ltb_ctx* ctx, void* p);
 int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,
                        int layout_in, const void* d_in, int dtype_out, int layout_out, void* d_out,
                        double* d_sumsq /* device, 2 doubles, may be null */);
+int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
+                       float* V, int warm, const int* skip);
 int ltb_svt_mirror_impl(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1, int64_t I2,
                         const void* d_a, double tau, void* d_out, const int* d_skip);
 int ltb_transform_pair_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,

@@ -43,7 +43,16 @@ struct ltb_pga {
   int done = 0;  // iterations executed so far
   bool converged = false;
   double pobs_sumsq = 0.0;
+  // fp32 real transform domain: right singular bases carried between iterations
+  // (ltb_svt_carry_impl); allocated on first use, warm after the first SVT
+  float* vcarry = nullptr;
+  int warm = 0;
+  bool carry_off = false;
 };
+
+// 1: fp32 PGA carries the right singular bases between iterations (warm-started SVT)
+static int g_pga_carry = 1;
+extern "C" void ltb_debug_set_pga_carry(int v) { g_pga_carry = v; }
 
 namespace {
 
@@ -224,8 +233,20 @@ int pga_transforms(ltb_pga* g, int k, double beta, double mu, double tol, double
     LTB_TRY((launch_xform_tile<Tc, Tm>(ctx, p, ld, st, (const Tm*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
   }
   // slice SVT with tau = mu_k
-  // (conjugate slice pairs of the real iterate are solved once)
-  LTB_TRY(ltb_svt_mirror_impl(ctx, g->spec, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, g->hat_b, skip));
+  // fp32 real transform domain: the SVT carries the slices' right bases between iterations
+  int carry = LTB_EUNSUPPORTED;
+  if (g->hat_dtype == LTB_F32 && !g->carry_off && g_pga_carry) {
+    const int64_t n = std::min(g->I1, g->I2);
+    if (!g->vcarry) LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * g->P * n * n, (void**)&g->vcarry));
+    carry = ltb_svt_carry_impl(ctx, g->P, g->I1, g->I2, (const float*)g->hat_a, mu, (float*)g->hat_b, g->vcarry,
+                               g->warm, skip);
+    if (carry == LTB_OK) g->warm = 1;
+    else if (carry == LTB_EUNSUPPORTED) g->carry_off = true;
+    else return carry;
+  }
+  // otherwise (conjugate slice pairs of the real iterate are solved once)
+  if (carry != LTB_OK)
+    LTB_TRY(ltb_svt_mirror_impl(ctx, g->spec, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, g->hat_b, skip));
   // inverse with the fused norms epilogue
   if (!pga_plan<Tc, Tm>(g->spec, g->NT, 1, p, &smem))
     return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
@@ -421,6 +442,7 @@ void ltb_pga_destroy(ltb_pga* g) {
   ltb_ws_free(ctx, g->d_records);
   ltb_ws_free(ctx, g->d_state);
   ltb_ws_free(ctx, g->d_scalars);
+  ltb_ws_free(ctx, g->vcarry);
   cudaStreamSynchronize(ctx->stream);
   delete g;
 }

@@ -1032,6 +1032,15 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
       if (o.kept_out) o.kept_out[b] = 0;
       if (o.stats) atomicAdd(&o.stats[0], 1ull);
     }
+    // carry mode: an identity basis with unit sigma keeps the carried V unchanged
+    if (o.v_out) {
+      float* vy = reinterpret_cast<float*>(o.v_out) + b * (int64_t)n * n;
+      for (int l = tid; l < n * n; l += nth) vy[l] = (l / n == l % n) ? 1.f : 0.f;
+    }
+    if (o.sv_out)
+      for (int j = tid; j < n; j += nth) reinterpret_cast<float*>(o.sv_out)[b * n + j] = 1.f;
+    if (o.d_out)
+      for (int j = tid; j < n; j += nth) reinterpret_cast<float*>(o.d_out)[b * n + j] = 0.f;
     return;
   }
 
@@ -1202,10 +1211,19 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     const bool keep = sj > (float)o.tau && sj > 0.f;
     kept_local += keep;
     scale[j] = keep ? sqrtf((sj - (float)o.tau) / sj) / sj : 0.f;
+    // carry mode: sqrt((sigma - tau)_+ / sigma), the weight of v_j in svt = G V diag(.) V^T
+    if (o.d_out) reinterpret_cast<float*>(o.d_out)[b * n + rank] = keep ? sqrtf((sj - (float)o.tau) / sj) : 0.f;
   }
   if (kept_local) atomicAdd(&flags[2], kept_local);
   __syncthreads();
   if (o.kept_out && tid == 0) o.kept_out[b] = flags[2];
+  if (o.v_out) {  // carry mode: the unscaled Jacobi columns y_j = sigma_j v_j, sorted
+    float* vy = reinterpret_cast<float*>(o.v_out) + b * (int64_t)n * n;
+    for (int l = tid; l < n * n; l += nth) {
+      const int j = l / n, i = l - j * n;
+      vy[(int64_t)rank_sh[j] * n + i] = W[(size_t)j * pitch + i];
+    }
+  }
   if (!o.w_out) return;
   float* dst = reinterpret_cast<float*>(o.w_out) + b * (int64_t)n * n;
   for (int l = tid; l < n * n; l += nth) {
@@ -1266,6 +1284,113 @@ int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const 
 #undef LTB_QR
 }
 
+// ---------------------------------------------------------------- SVT with a carried right basis
+// Inside PGA the iterates change slowly, so the right singular vectors V of
+// one iteration's slices precondition the next: the QR-preconditioned Jacobi
+// runs on A0 = G V_prev (G^T V_prev oriented), whose columns are already
+// nearly orthogonal, and converges in a few sweeps.  With V = V_prev V_A0
+// (V_A0 from the normalised Jacobi columns, completed to an orthonormal basis)
+//   svt(G) = G V diag((s - tau)_+ / s) V^T          (I1 >= I2)
+//   svt(G) = V diag((s - tau)_+ / s) V^T G          (I1 <  I2, V of G^T)
+// V is re-orthonormalised by one Newton-Schulz step, V <- V (3I - V^T V) / 2,
+// every call, so rounding does not accumulate across iterations.
+__global__ void ns_combine_kernel(int64_t batch, int n, const float* __restrict__ S, float* __restrict__ M,
+                                  const int* skip) {
+  if (skip && *skip) return;
+  const int64_t total = batch * (int64_t)n * n;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = l % ((int64_t)n * n);
+    M[l] = (r / n == r % n ? 1.5f : 0.f) - 0.5f * S[l];
+  }
+}
+
+__global__ void col_scale_kernel(int64_t batch, int n, const float* __restrict__ V, const float* __restrict__ d,
+                                 float* __restrict__ T, const int* skip) {
+  if (skip && *skip) return;
+  const int64_t total = batch * (int64_t)n * n;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = l / ((int64_t)n * n);
+    T[l] = V[l] * d[b * n + (int)(l % n)];
+  }
+}
+
+}  // namespace
+
+// fp32 SVT of `batch` I1 x I2 slices carrying the n x n right bases V (row-major,
+// n = min(I1, I2)) between calls; warm == 0 starts from the identity.
+// LTB_EUNSUPPORTED when the slice shape does not fit the QR-preconditioned kernel.
+int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
+                       float* V, int warm, const int* skip) {
+  const bool trans = I1 < I2;
+  const int64_t m = trans ? I2 : I1, n = trans ? I1 : I2;
+  if (batch <= 0 || n < 32) return LTB_EUNSUPPORTED;
+  const int64_t nn = n * n;
+  float *A0 = nullptr, *Y = nullptr, *sv = nullptr, *dd = nullptr, *VR = nullptr, *Vn = nullptr, *S = nullptr;
+  int* kept = nullptr;
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * n * m, (void**)&A0));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * nn, (void**)&Y));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * n, (void**)&sv));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * n, (void**)&dd));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * nn, (void**)&VR));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * nn, (void**)&Vn));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * nn, (void**)&S));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * batch, (void**)&kept));
+  auto release = [&]() {
+    for (void* p : {(void*)A0, (void*)Y, (void*)sv, (void*)dd, (void*)VR, (void*)Vn, (void*)S, (void*)kept})
+      ltb_ws_free(ctx, p);
+  };
+  const int F = LTB_F32;
+  const float* src = G;
+  if (warm) {  // A0 = V^T G (I1 < I2) or G V: the preconditioned slices, same shape as G
+    if (trans)
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, m, n, LTB_OP_T, V, n, nn, LTB_OP_N, G, m, n * m, A0, m, n * m, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, skip));
+    else
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, m, n, n, LTB_OP_N, G, n, m * n, LTB_OP_N, V, n, nn, A0, n, m * n, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, skip));
+    src = A0;
+  }
+  JacobiOut o{nullptr, sv, Y, kept, dd, tau, skip};
+  o.stats = ctx->d_stats;
+  const int st = launch_jacobi_qr(ctx, batch, I1, I2, src, o);
+  if (st != LTB_OK) {
+    release();
+    return st;
+  }
+  // V_A0: normalised Jacobi columns completed to an orthonormal basis (row-major, column j = v_j)
+  LTB_TRY(ensure_smem(ctx, complete_u_kernel<float>, (size_t)n * sizeof(float)));
+  complete_u_kernel<float><<<(unsigned)batch, 256, (size_t)n * sizeof(float), ctx->stream>>>((int)n, (int)n, Y, sv, VR);
+  LTB_LAUNCH_CHECK(ctx);
+  const float* Vc = VR;  // V_prev V_A0
+  if (warm) {
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, V, n, nn, LTB_OP_N, VR, n, nn, Vn, n, nn, nullptr, nullptr,
+                          nullptr, nullptr, nullptr, skip));
+    Vc = Vn;
+  }
+  // Newton-Schulz: V = Vc (3I - Vc^T Vc) / 2
+  LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_T, Vc, n, nn, LTB_OP_N, Vc, n, nn, S, n, nn, nullptr, nullptr,
+                        nullptr, nullptr, nullptr, skip));
+  const unsigned grid = grid_for(batch * nn, 256, ctx->num_sms * 8);
+  ns_combine_kernel<<<grid, 256, 0, ctx->stream>>>(batch, (int)n, S, Y, skip);  // Y reused as M
+  LTB_LAUNCH_CHECK(ctx);
+  LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, Vc, n, nn, LTB_OP_N, Y, n, nn, V, n, nn, nullptr, nullptr,
+                        nullptr, nullptr, nullptr, skip));
+  // T = V diag(sqrt((s - tau)_+ / s)),  Z = T T^T (K limited to the kept count),  out
+  col_scale_kernel<<<grid, 256, 0, ctx->stream>>>(batch, (int)n, V, dd, VR, skip);  // VR reused as T
+  LTB_LAUNCH_CHECK(ctx);
+  LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, VR, n, nn, LTB_OP_T, VR, n, nn, S, n, nn, nullptr, nullptr,
+                        kept, nullptr, nullptr, skip));
+  if (trans)
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, m, n, LTB_OP_N, S, n, nn, LTB_OP_N, G, m, n * m, out, m, n * m, nullptr,
+                          nullptr, nullptr, nullptr, nullptr, skip));
+  else
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, m, n, n, LTB_OP_N, G, n, m * n, LTB_OP_N, S, n, nn, out, n, m * n, nullptr,
+                          nullptr, nullptr, nullptr, nullptr, skip));
+  release();
+  return LTB_OK;
+}
+
+namespace {
 }  // namespace
 
 extern "C" void ltb_debug_set_svd_blocked(int v) { g_force_blocked = v; }
