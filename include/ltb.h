@@ -73,7 +73,8 @@ int ltb_ctx_set_stream(ltb_ctx* ctx, void* stream);
 int ltb_ctx_synchronize(ltb_ctx* ctx);
 /* number of ltb kernels launched on this context since creation */
 int64_t ltb_ctx_launch_count(const ltb_ctx* ctx);
-/* device-side counters: h_out[0] = Jacobi slices solved, h_out[1] = Jacobi sweeps run */
+/* device-side counters (3 entries): h_out[0] = Jacobi slices solved, h_out[1] = Jacobi sweeps run,
+ * h_out[2] = most sweeps of one slice */
 int ltb_ctx_stats(ltb_ctx* ctx, int64_t* h_out, int reset);
 
 /* ---------------------------------------------------------------- memory */

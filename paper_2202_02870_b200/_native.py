@@ -154,11 +154,11 @@ def launch_count() -> int:
     return int(lib().ltb_ctx_launch_count(context()))
 
 
-def jacobi_stats(reset: bool = False) -> tuple:
-    """(slices solved, sweeps run) by the Jacobi kernels since the last reset."""
-    out = (_i64 * 2)()
+def jacobi_stats(reset: bool = False, with_max: bool = False) -> tuple:
+    """(slices solved, sweeps run[, most sweeps of one slice]) by the Jacobi kernels since the last reset."""
+    out = (_i64 * 3)()
     check(lib().ltb_ctx_stats(context(), out, int(reset)))
-    return int(out[0]), int(out[1])
+    return (int(out[0]), int(out[1]), int(out[2])) if with_max else (int(out[0]), int(out[1]))
 
 
 def dtype_code(dt) -> int:

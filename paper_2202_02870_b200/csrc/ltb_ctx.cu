@@ -147,11 +147,12 @@ int ltb_ctx_synchronize(ltb_ctx* ctx) {
 int64_t ltb_ctx_launch_count(const ltb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int ltb_ctx_stats(ltb_ctx* ctx, int64_t* h_out, int reset) {
-  unsigned long long v[2] = {0, 0};
+  unsigned long long v[3] = {0, 0, 0};
   LTB_CUDA_TRY(ctx, cudaMemcpyAsync(v, ctx->d_stats, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream));
   LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   h_out[0] = (int64_t)v[0];
   h_out[1] = (int64_t)v[1];
+  h_out[2] = (int64_t)v[2];
   if (reset) LTB_CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_stats, 0, sizeof(v), ctx->stream));
   return LTB_OK;
 }

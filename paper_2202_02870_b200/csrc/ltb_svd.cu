@@ -416,7 +416,8 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
 // is >= (m - slot) / m, so every candidate is accepted (no rejection loop).
 template <typename T>
 __global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
-                                  const typename scalar_traits<T>::real* __restrict__ sv, T* __restrict__ U) {
+                                  const typename scalar_traits<T>::real* __restrict__ sv, T* __restrict__ U,
+                                  int any_nonzero = 0) {
   using R = typename scalar_traits<T>::real;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   R* rn = reinterpret_cast<R*>(smem_raw);  // residual row norms, m entries
@@ -430,7 +431,10 @@ __global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
   __shared__ int good_count;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
   const R smax = n > 0 ? sb[0] : (R)0;
-  const R thr = smax * (R)max(m, 1) * eps_of<R>::value;
+  // t_svd: columns above the rank threshold of numpy's matrix_rank; any_nonzero (the carried
+  // PGA basis): every column with sigma > 0, since converged Jacobi columns are orthogonal
+  // relative to their own norms and only an orthonormal basis is needed there
+  const R thr = any_nonzero ? (R)0 : smax * (R)max(m, 1) * eps_of<R>::value;
   // number of leading good columns (sorted descending, so good ones are a prefix)
   if (tid == 0) {
     int g = 0;
@@ -1184,6 +1188,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   if (o.stats && tid == 0) {
     atomicAdd(&o.stats[0], 1ull);
     atomicAdd(&o.stats[1], (unsigned long long)sweeps_done);
+    atomicMax(&o.stats[2], (unsigned long long)sweeps_done);  // the launch waits for its slowest slice
   }
   // ---- singular values, descending ranks, scaled columns y~_j
   float* sig = nrm;
@@ -1359,7 +1364,8 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
   }
   // V_A0: normalised Jacobi columns completed to an orthonormal basis (row-major, column j = v_j)
   LTB_TRY(ensure_smem(ctx, complete_u_kernel<float>, (size_t)n * sizeof(float)));
-  complete_u_kernel<float><<<(unsigned)batch, 256, (size_t)n * sizeof(float), ctx->stream>>>((int)n, (int)n, Y, sv, VR);
+  complete_u_kernel<float><<<(unsigned)batch, 256, (size_t)n * sizeof(float), ctx->stream>>>((int)n, (int)n, Y, sv, VR,
+                                                                                              1);
   LTB_LAUNCH_CHECK(ctx);
   const float* Vc = VR;  // V_prev V_A0
   if (warm) {

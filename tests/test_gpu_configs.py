@@ -132,3 +132,21 @@ def test_config4_reduced_pga():
     ref, recs, _ = O.pga_complete(m, mask, ospec, tol=1e-300, max_iters=3)
     assert trace.iterations == 3
     assert rel_err(x, ref) < 1e-4
+
+
+def test_config3_recipe_long_run_fp32_carry():
+    """Config-3 recipe at 64 x 72 x 3 x 20 for 90 iterations in fp32: the warm-started SVT
+    (right bases carried across iterations) stays within the fp32 tolerance of the fp64 oracle
+    trajectory, iterate and per-iteration relative change."""
+    m, mask = cfg3_data(shape=(64, 72, 3, 20), rank=4, seed=3)
+    spec = L.make_spec("dct", m.shape)
+    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=90)
+    x, trace = L.pga_complete(m, mask, cfg, precision="fp32")
+    ref, recs, _ = O.pga_complete(m, mask, O.ospec("dct", m.shape), tol=1e-300, max_iters=90)
+    assert trace.iterations == 90
+    assert rel_err(x, ref) < 1e-4
+    rc = np.array([r.rel_change for r in trace.records])
+    rr = np.array([r[3] for r in recs])
+    fin = np.isfinite(rr)
+    np.testing.assert_array_equal(np.isfinite(rc), fin)  # x_next == 0 (inf) on the same iterations
+    assert np.max(np.abs(rc[fin] - rr[fin]) / np.maximum(rr[fin], 1e-12)) < 1e-2
