@@ -448,6 +448,7 @@ __global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
     Ub[(int64_t)i * m + j] = Wb[(int64_t)j * m + i] * ((R)1 / sb[j]);
   }
   __syncthreads();
+  if (g0 >= m) return;  // every column normalised: nothing to complete
   for (int i = tid; i < m; i += nth) {
     R acc = 0;
     for (int j = 0; j < g0; ++j) acc += abs2_v(Ub[(int64_t)i * m + j]);
