@@ -420,7 +420,7 @@ def run_ours(args):
                 "frac": achieved / hbm_peak, "peak_source": f"{peak_src} HBM copy (MEASURED_PEAKS.json)",
                 "alg_per_launch": f"{alg_bytes[dom]} B ({alg_desc[dom]})",
                 "arith_intensity_flop_per_byte": alg_flops[dom] / alg_bytes[dom]}
-    roof["traffic"] = None
+    roof["traffic"] = _ncu_traffic(names[dom])
     roof["phase_ms"] = dict(zip(names, [round(float(x), 5) for x in phase_avg]))
 
     line = {
@@ -466,6 +466,15 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def _ncu_traffic(kernel):
+    """dram bytes read + written per launch of `kernel` from the committed ncu capture
+    (profiles/r01_traffic.json, see profiles/r01_ncu_summary.md), or None."""
+    try:
+        return json.load(open(ROOT / "profiles" / "r01_traffic.json")).get(kernel)
+    except (OSError, ValueError):
+        return None
 
 
 def bench_pga(L, nat, torch, args):
@@ -515,7 +524,8 @@ def bench_pga(L, nat, torch, args):
     fp32_peak = 74.4
     roof = {"kernel": "K3 SVT (QR-preconditioned one-sided Jacobi + recomposition)", "bound": "fp32",
             "achieved": k3_flop / t_k3 / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": k3_flop / t_k3 / 1e12 / fp32_peak, "traffic": None,
+            "frac": k3_flop / t_k3 / 1e12 / fp32_peak,
+            "traffic": _ncu_traffic("K3 SVT (QR-preconditioned one-sided Jacobi + recomposition)"),
             "alg_per_launch": f"{k3_flop} flop nominal (300 slices x (6mn^2 + 20n^3 + 2mn^2))",
             "peak_source": "FP32 FFMA nominal 148 SM x 128 x 2 x 1.965 GHz (SURVEY.md §8(d))",
             "k3_ms": t_k3 * 1e3,
