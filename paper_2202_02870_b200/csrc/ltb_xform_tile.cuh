@@ -222,6 +222,47 @@ __device__ __forceinline__ void mode_step(const XformParams& p, const ModeStep& 
   }
 }
 
+// fp32: each work item takes two tubes (t and t + TT/2) as one float2 and RBM
+// outputs, so the FMAs issue as FFMA2 against the broadcast matrix entry
+template <int RBM>
+__device__ __forceinline__ void mode_step_f2(const XformParams& p, const ModeStep& ms, const float* __restrict__ src,
+                                             float* __restrict__ dst, const float* __restrict__ Msm, int tid) {
+  const int n = ms.n, npad = ms.npad, lo = (int)ms.lo, hi = (int)ms.hi;
+  const int half = p.TT >> 1, pitch = p.pitch;
+  const int hshift = p.ttshift - 1;
+  const int nblk = npad / RBM;
+  const int work = hi * lo * nblk * half;
+  for (int w = tid; w < work; w += kXformThreads) {
+    const int t = w & (half - 1);
+    const int r0 = w >> hshift;
+    const int r1 = fdiv(r0, nblk, ms.inv_nblk);
+    const int iblk = r0 - r1 * nblk;
+    const int hi_i = fdiv(r1, lo, ms.inv_lo);
+    const int lo_i = r1 - hi_i * lo;
+    const int i0 = iblk * RBM;
+    const int base = hi_i * n * lo + lo_i;
+    float2 acc[RBM];
+#pragma unroll
+    for (int rr = 0; rr < RBM; ++rr) acc[rr] = make_float2(0.f, 0.f);
+    const float* col = src + base * pitch + t;
+    const int jstride = lo * pitch;
+    const float* mrowp = Msm + i0;
+    for (int j = 0; j < n; ++j) {
+      const float2 v = make_float2(col[j * jstride], col[j * jstride + half]);
+      const mrow<float, RBM> mv = *reinterpret_cast<const mrow<float, RBM>*>(mrowp + j * npad);
+#pragma unroll
+      for (int rr = 0; rr < RBM; ++rr) acc[rr] = __ffma2_rn(make_float2(mv.v[rr], mv.v[rr]), v, acc[rr]);
+    }
+    float* out = dst + base * pitch + t;
+#pragma unroll
+    for (int rr = 0; rr < RBM; ++rr)
+      if (i0 + rr < n) {
+        out[(i0 + rr) * jstride] = acc[rr].x;
+        out[(i0 + rr) * jstride + half] = acc[rr].y;
+      }
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 template <typename Tc, typename Tm, class Loader, class Storer>
 __global__ void __launch_bounds__(kXformThreads)
@@ -268,11 +309,25 @@ __global__ void __launch_bounds__(kXformThreads)
     const ModeStep& ms = p.step[s];
     const Tm* Mg = mats + ms.mat_off;
     const Tm* Msm = Ms + ms.smem_off;
-    switch (ms.rb) {
-      case 1: mode_step<Tc, Tm, 1>(p, ms, src, dst, Msm, Mg, tid); break;
-      case 2: mode_step<Tc, Tm, 2>(p, ms, src, dst, Msm, Mg, tid); break;
-      case 4: mode_step<Tc, Tm, 4>(p, ms, src, dst, Msm, Mg, tid); break;
-      default: mode_step<Tc, Tm, RB>(p, ms, src, dst, Msm, Mg, tid); break;
+    bool done = false;
+    if constexpr (std::is_same<Tc, float>::value && std::is_same<Tm, float>::value) {
+      if (p.mats_in_smem && TT >= 2) {
+        switch (ms.rb) {
+          case 1: mode_step_f2<1>(p, ms, src, dst, Msm, tid); break;
+          case 2: mode_step_f2<2>(p, ms, src, dst, Msm, tid); break;
+          case 4: mode_step_f2<4>(p, ms, src, dst, Msm, tid); break;
+          default: mode_step_f2<RB>(p, ms, src, dst, Msm, tid); break;
+        }
+        done = true;
+      }
+    }
+    if (!done) {
+      switch (ms.rb) {
+        case 1: mode_step<Tc, Tm, 1>(p, ms, src, dst, Msm, Mg, tid); break;
+        case 2: mode_step<Tc, Tm, 2>(p, ms, src, dst, Msm, Mg, tid); break;
+        case 4: mode_step<Tc, Tm, 4>(p, ms, src, dst, Msm, Mg, tid); break;
+        default: mode_step<Tc, Tm, RB>(p, ms, src, dst, Msm, Mg, tid); break;
+      }
     }
     __syncthreads();
     Tc* tmp = src;
