@@ -989,16 +989,29 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
 //   svt(W) = W V diag((s - tau)_+ / s) V^T = W (Y~ Y~^T),  y~_j = y_j sqrt((s_j - tau)_+ / s_j) / s_j,
 // so the kernel emits Y~ (sorted, scaled) and two tensor-core GEMMs finish:
 // Z = Y~ Y~^T, then out = A Z (I1 >= I2) or Z A (I1 < I2).
-template <int TS, int MPL, int MINB>
+// CHOL: A holds the Gram matrices G = W^T W (batch x n x n, symmetric) of slices whose
+// columns are nearly orthogonal (the carried PGA bases); the triangular factor comes from
+// an in-place Cholesky, G = L L^T with L = R^T, accurate here because the diagonally
+// scaled Gram matrix is well conditioned, and much shorter than the Householder QR.
+template <int TS, int MPL, int MINB, bool CHOL = false>
 __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
-    jacobi_qr_kernel(int64_t I1, int64_t I2, const float* __restrict__ A, JacobiOut o, int max_sweeps, int pitch) {
+    jacobi_qr_kernel(int64_t I1, int64_t I2, const float* __restrict__ A, JacobiOut o, int max_sweeps, int pitch,
+                     unsigned long long* dbg) {
   if (o.skip && *o.skip) return;
+  auto stamp = [&](int slot) {  // optional stage timeline of CTA 0 (%globaltimer ns)
+    if (dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long tns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+      dbg[slot] = tns;
+    }
+  };
+  stamp(0);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const bool trans = I1 < I2;
-  const int m = (int)(trans ? I2 : I1);
   const int n = (int)(trans ? I1 : I2);
+  const int m = CHOL ? n : (int)(trans ? I2 : I1);
   const int64_t b = blockIdx.x;
-  const float* Ab = A + b * I1 * I2;
+  const float* Ab = A + b * (CHOL ? (int64_t)n * n : I1 * I2);
   float* W = reinterpret_cast<float*>(smem_raw);  // n columns, pitch >= max(m, TS * MPL), even
   float* vhead = W + (size_t)n * pitch;           // v_k[0] of the reflectors
   float* beta = vhead + n;
@@ -1007,7 +1020,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
   constexpr int TR = TS * MPL;  // register-tile rows of X (rows n..TR-1 are zero)
 
-  if (!trans) {
+  if (CHOL || !trans) {  // (G is symmetric: its rows are its columns)
     for (int l = tid; l < m * n; l += nth) {
       const int i = l / n, j = l - i * n;
       W[(size_t)j * pitch + i] = Ab[l];
@@ -1020,13 +1033,18 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   }
   if (tid < 4) flags[tid] = 0;
   __syncthreads();
-  // ||A||_F <= tau: nothing survives the threshold (sigma_max <= ||A||_F)
+  stamp(1);
+  // ||A||_F <= tau: nothing survives the threshold (sigma_max <= ||A||_F; trace(G) = ||A||_F^2)
   if (warp == 0) {
     float s2 = 0.f;
-    for (int l = lane; l < m * n; l += 32) {
-      const int j = l / m, i = l - j * m;
-      const float v = W[(size_t)j * pitch + i];
-      s2 += v * v;
+    if (CHOL) {
+      for (int j = lane; j < n; j += 32) s2 += W[(size_t)j * pitch + j];
+    } else {
+      for (int l = lane; l < m * n; l += 32) {
+        const int j = l / m, i = l - j * m;
+        const float v = W[(size_t)j * pitch + i];
+        s2 += v * v;
+      }
     }
     s2 = warp_sum(s2);
     if (lane == 0) flags[3] = (o.tau > 0.0 && (double)s2 <= o.tau * o.tau) ? 1 : 0;
@@ -1049,6 +1067,8 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     return;
   }
 
+  stamp(2);
+  if constexpr (!CHOL) {
   // ---- Householder QR: R on and above the diagonal, v_k below it (v_k[0] in vhead)
   for (int k = 0; k < n; ++k) {
     float* wk = W + (size_t)k * pitch;
@@ -1083,6 +1103,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     }
     __syncthreads();
   }
+  stamp(3);
   // ---- X = R^T in place: R[i][j] (row i < column j, upper triangle) moves to column i,
   // row j (below the diagonal, where the reflector lived); then clear the upper triangle
   // and the rows n .. TR-1
@@ -1096,6 +1117,43 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     if (j < i || j >= n) W[(size_t)i * pitch + j] = 0.f;
   }
   __syncthreads();
+
+  stamp(4);
+  } else {
+    // ---- Cholesky G = L L^T in place (column j of L in column j, rows >= j); a non-positive
+    // pivot (rank-deficient slice) zeroes its column.  The owner of column k+1 finishes it
+    // right after its trailing update, so each step costs one block barrier.
+    auto finish = [&](int j) {  // one warp: pivot and scaling of column j
+      float* wj = W + (size_t)j * pitch;
+      const float pj = wj[j];
+      const float d = pj >= FLT_MIN ? sqrtf(pj) : 0.f;
+      const float inv = d > 0.f ? 1.f / d : 0.f;
+      __syncwarp();
+      if (lane == 0) wj[j] = d;
+      for (int i = j + 1 + lane; i < n; i += 32) wj[i] *= inv;
+      __syncwarp();
+    };
+    if (warp == 0) finish(0);
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+      const float* lk = W + (size_t)k * pitch;
+      for (int j = k + 1 + warp; j < n; j += nwarps) {
+        float* wj = W + (size_t)j * pitch;
+        const float ljk = lk[j];
+        if (ljk != 0.f)
+          for (int i = j + lane; i < n; i += 32) wj[i] = fmaf(-lk[i], ljk, wj[i]);
+        __syncwarp();
+        if (j == k + 1) finish(j);
+      }
+      __syncthreads();
+    }
+    // X = L: clear the upper triangle and the rows n .. TR-1
+    for (int l = tid; l < n * TR; l += nth) {
+      const int c = l / TR, r = l - c * TR;
+      if (r < c || r >= n) W[(size_t)c * pitch + r] = 0.f;
+    }
+    __syncthreads();
+  }
 
   // ---- one-sided Jacobi on the n columns of X (n rows), as jacobi_kernel's fp32 path
   const float tol = FLT_EPSILON * sqrtf((float)max(n, 1));
@@ -1186,6 +1244,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     sweeps_done = sweep + 1;
     if (!any) break;
   }
+  stamp(5);
   if (o.stats && tid == 0) {
     atomicAdd(&o.stats[0], 1ull);
     atomicAdd(&o.stats[1], (unsigned long long)sweeps_done);
@@ -1238,9 +1297,11 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   }
 }
 
+unsigned long long* g_qr_dbg = nullptr;  // stage timeline hook (CTA 0)
+
 size_t jacobi_qr_smem(int n, int pitch) { return ((size_t)n * pitch + 4 * (size_t)n + 1) * 4 + (n + 8) * 4 + 16; }
 
-template <int TS, int MPL, int MINB>
+template <int TS, int MPL, int MINB, bool CHOL>
 int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o,
                       int max_sweeps, int n, int pitch) {
   const size_t smem = jacobi_qr_smem(n, pitch);
@@ -1250,18 +1311,21 @@ int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const
   const int per_warp = (teams + maxw - 1) / maxw;
   const int nwarps = std::max(1, (teams + per_warp - 1) / per_warp);
   if ((pairs + nwarps * (32 / TS) - 1) / (nwarps * (32 / TS)) > 4) return LTB_EUNSUPPORTED;  // <= 4 slots per team
-  auto kern = jacobi_qr_kernel<TS, MPL, MINB>;
+  auto kern = jacobi_qr_kernel<TS, MPL, MINB, CHOL>;
   LTB_TRY(ensure_smem(ctx, kern, smem, true));
-  kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, o, max_sweeps, pitch);
+  kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, o, max_sweeps, pitch, g_qr_dbg);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
 
 // 1 when the QR-preconditioned resident kernel takes this fp32 SVT; 0 to use the others
 int g_svt_qr = 1;
+int g_qr_max_sweeps = 40;  // timing hook: 0 measures the QR and emission stages alone
 
 // LTB_EUNSUPPORTED when the shape does not fit the QR-preconditioned kernel
-int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o) {
+// chol: A holds n x n Gram matrices (I1 == I2 == n), factored by Cholesky instead of Householder
+int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o,
+                     bool chol = false) {
   const int m = (int)std::max(I1, I2), n = (int)std::min(I1, I2);
   if (!g_svt_qr || g_force_blocked || n < 32 || batch > 0x7fffffff) return LTB_EUNSUPPORTED;
   int TSv = 16, MPLv = 0;
@@ -1276,10 +1340,13 @@ int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const 
   const size_t smem = jacobi_qr_smem(n, pitch);
   if (smem > kSmemLimit) return LTB_EUNSUPPORTED;
   const bool two = 2 * (smem + 1024) <= 228 * 1024;
-  const int ms = 40;
-#define LTB_QR(TS_, MPL_) \
-  return two ? launch_qr_variant<TS_, MPL_, 2>(ctx, batch, I1, I2, A, o, ms, n, pitch) \
-             : launch_qr_variant<TS_, MPL_, 1>(ctx, batch, I1, I2, A, o, ms, n, pitch)
+  const int ms = g_qr_max_sweeps;
+#define LTB_QR(TS_, MPL_)                                                                              \
+  if (chol)                                                                                              \
+    return two ? launch_qr_variant<TS_, MPL_, 2, true>(ctx, batch, I1, I2, A, o, ms, n, pitch)          \
+               : launch_qr_variant<TS_, MPL_, 1, true>(ctx, batch, I1, I2, A, o, ms, n, pitch);         \
+  return two ? launch_qr_variant<TS_, MPL_, 2, false>(ctx, batch, I1, I2, A, o, ms, n, pitch)           \
+             : launch_qr_variant<TS_, MPL_, 1, false>(ctx, batch, I1, I2, A, o, ms, n, pitch)
   if (TSv == 32) { LTB_QR(32, 8); }
   switch (MPLv) {
     case 4: LTB_QR(16, 4);
@@ -1325,6 +1392,9 @@ __global__ void col_scale_kernel(int64_t batch, int n, const float* __restrict__
 // fp32 SVT of `batch` I1 x I2 slices carrying the n x n right bases V (row-major,
 // n = min(I1, I2)) between calls; warm == 0 starts from the identity.
 // LTB_EUNSUPPORTED when the slice shape does not fit the QR-preconditioned kernel.
+int g_carry_chol = 1;  // warm carried SVT: Cholesky of the Gram matrix (1) or Householder (0)
+extern "C" void ltb_debug_set_carry_chol(int v) { g_carry_chol = v; }
+
 int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
                        float* V, int warm, const int* skip) {
   const bool trans = I1 < I2;
@@ -1358,7 +1428,20 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
   }
   JacobiOut o{nullptr, sv, Y, kept, dd, tau, skip};
   o.stats = ctx->d_stats;
-  const int st = launch_jacobi_qr(ctx, batch, I1, I2, src, o);
+  int st;
+  if (warm && g_carry_chol) {
+    // A0's columns are nearly orthogonal: factor its Gram matrix (tensor-core GEMM) by
+    // Cholesky instead of a Householder QR of A0 (Y reused as the Gram stack)
+    if (trans)  // oriented W = A0^T: G = A0 A0^T
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, m, LTB_OP_N, A0, m, n * m, LTB_OP_T, A0, m, n * m, S, n, nn, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, skip));
+    else  // W = A0: G = A0^T A0
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, m, LTB_OP_T, A0, n, m * n, LTB_OP_N, A0, n, m * n, S, n, nn, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, skip));
+    st = launch_jacobi_qr(ctx, batch, n, n, S, o, true);
+  } else {
+    st = launch_jacobi_qr(ctx, batch, I1, I2, src, o);
+  }
   if (st != LTB_OK) {
     release();
     return st;
@@ -1402,6 +1485,8 @@ namespace {
 
 extern "C" void ltb_debug_set_svd_blocked(int v) { g_force_blocked = v; }
 extern "C" void ltb_debug_set_svt_qr(int v) { g_svt_qr = v; }
+extern "C" void ltb_debug_set_qr_max_sweeps(int v) { g_qr_max_sweeps = v; }
+extern "C" void ltb_debug_set_qr_timeline(void* p) { g_qr_dbg = (unsigned long long*)p; }
 
 // SVT of `batch` row-major I1 x I2 slices: out = U (S - tau)_+ V^H
 int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2, const void* d_a, double tau,
