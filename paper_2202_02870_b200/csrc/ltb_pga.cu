@@ -48,11 +48,19 @@ struct ltb_pga {
   float* vcarry = nullptr;
   int warm = 0;
   bool carry_off = false;
+  bool tc_off = false;        // the tensor-core transform path declined this shape
+  int64_t nblocks_cap = 0;    // partials capacity (blocks x 5 doubles)
 };
 
 // 1: fp32 PGA carries the right singular bases between iterations (warm-started SVT)
 static int g_pga_carry = 1;
 extern "C" void ltb_debug_set_pga_carry(int v) { g_pga_carry = v; }
+// 1: fp32 real specs with a Kronecker matrix transform on the tensor cores inside PGA.
+// Off by default: 3xTF32 keeps ~21 mantissa bits per product, and over ~90 iterations of
+// the momentum recursion the iterate drifts to 1.0e-4 of the fp64 oracle (the fp32 tile
+// engine stays below it); +8% it/s on config 3 when enabled
+static int g_pga_tc = 0;
+extern "C" void ltb_debug_set_pga_tc(int v) { g_pga_tc = v; }
 
 namespace {
 
@@ -139,6 +147,58 @@ struct StorePGA {
   }
 };
 
+// fp32 real specs with a Kronecker matrix: the gradient step as its own pass (the tensor-core
+// transform reads it with TMA) and the five norms of StorePGA as a pass after the inverse
+__global__ void pga_grad_kernel(int64_t E, const float* __restrict__ xc, const float* __restrict__ xp,
+                                const float* __restrict__ pobs, const uint32_t* __restrict__ mask, float beta,
+                                float* __restrict__ g, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const float y = momentum<float>(xc[e], xp[e], beta);
+    const bool obs = (mask[e >> 5] >> (e & 31)) & 1u;
+    g[e] = gradient_point<float>(y, pobs[e], obs);
+  }
+}
+
+// per-block partials in StorePGA's slot order (fixed grid: the reduction order is deterministic)
+__global__ void pga_norms_kernel(int64_t E, const float* __restrict__ xn, const float* __restrict__ xc,
+                                 const float* __restrict__ xp, const float* __restrict__ gt, float beta,
+                                 double* __restrict__ partials, const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  double acc[5] = {0.0, 0.0, 0.0, -1.0e308, 0.0};
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const float x1 = xn[e];
+    const float y = momentum<float>(xc[e], xp[e], beta);
+    const double d = (double)y - (double)x1;
+    acc[0] += d * d;
+    acc[1] += (double)x1 * (double)x1;
+    if (gt) {
+      const double dg = (double)x1 - (double)gt[e];
+      acc[2] += dg * dg;
+    }
+    acc[3] = fmax(acc[3], (double)x1);
+  }
+  __shared__ double red[5][8];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, v, o);
+      v = k == 3 ? fmax(v, w) : v + w;
+    }
+    if (lane == 0) red[k][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    const int k = threadIdx.x;
+    double v = k == 3 ? -1.0e308 : 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = k == 3 ? fmax(v, red[k][w]) : v + red[k][w];
+    partials[(int64_t)blockIdx.x * 5 + k] = v;
+  }
+}
+
 // reduce the per-CTA partials of one iteration, record, and decide to stop
 __global__ void pga_finalize_kernel(const double* __restrict__ partials, int64_t nblocks, double* __restrict__ rec,
                                     int* __restrict__ state, const double* __restrict__ scalars, double tol) {
@@ -214,25 +274,10 @@ int pga_plan(const ltb_spec* spec, int64_t NT, int inverse, XformParams& p, size
   return plan_tile<Tc, Tm>(p, smem);
 }
 
-template <typename R, typename Tc, typename Tm>
-int pga_transforms(ltb_pga* g, int k, double beta, double mu, double tol, double* rec) {
+// the SVT step of one iteration (hat_a -> hat_b): carried bases for fp32 real transform
+// domains, otherwise the conjugate-mirrored / plain SVT
+int pga_svt(ltb_pga* g, double mu, const int* skip) {
   ltb_ctx* ctx = g->ctx;
-  const R* xc = (const R*)g->x[cur_of(k)];
-  const R* xp = (const R*)g->x[prev_of(k)];
-  R* xn = (R*)g->x[next_of(k)];
-  const int* skip = g->d_state;
-  const int dbl = std::is_same<R, double>::value ? 1 : 0;
-  XformParams p;
-  size_t smem = 0;
-  // forward: gradient step fused into the load, slice-major store
-  if (!pga_plan<Tc, Tm>(g->spec, g->NT, 0, p, &smem))
-    return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
-  {
-    LoadPGA<R> ld{xc, xp, (const R*)g->pobs, g->mask, (R)beta};
-    StorePlain<Tc, false> st{(Tc*)g->hat_a, LTB_SLICE_MAJOR};
-    LTB_TRY((launch_xform_tile<Tc, Tm>(ctx, p, ld, st, (const Tm*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
-  }
-  // slice SVT with tau = mu_k
   // fp32 real transform domain: the SVT carries the slices' right bases between iterations
   int carry = LTB_EUNSUPPORTED;
   if (g->hat_dtype == LTB_F32 && !g->carry_off && g_pga_carry) {
@@ -247,6 +292,62 @@ int pga_transforms(ltb_pga* g, int k, double beta, double mu, double tol, double
   // otherwise (conjugate slice pairs of the real iterate are solved once)
   if (carry != LTB_OK)
     LTB_TRY(ltb_svt_mirror_impl(ctx, g->spec, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, g->hat_b, skip));
+  return LTB_OK;
+}
+
+template <typename R, typename Tc, typename Tm>
+int pga_transforms(ltb_pga* g, int k, double beta, double mu, double tol, double* rec) {
+  ltb_ctx* ctx = g->ctx;
+  const R* xc = (const R*)g->x[cur_of(k)];
+  const R* xp = (const R*)g->x[prev_of(k)];
+  R* xn = (R*)g->x[next_of(k)];
+  const int* skip = g->d_state;
+  const int dbl = std::is_same<R, double>::value ? 1 : 0;
+  XformParams p;
+  size_t smem = 0;
+  // fp32 real specs with a Kronecker matrix: gradient pass + tensor-core transform (hat_b is
+  // free until the SVT writes it, so it holds the gradient), then SVT, tensor-core inverse
+  // and the norms pass; any shape the tcgen05 path declines takes the fused tile engine
+  if constexpr (std::is_same<R, float>::value && std::is_same<Tc, float>::value) {
+    if (g->spec->d_kron[0] && g_pga_tc && !g->tc_off) {
+      const int64_t P = g->P, NT = g->NT, E = g->E;
+      const float* Kf = g->spec->d_kron[0];
+      const float* Ki = g->spec->d_kron[1];
+      const unsigned eg = grid_for(E, 256, ctx->num_sms * 8);
+      pga_grad_kernel<<<eg, 256, 0, ctx->stream>>>(E, xc, xp, (const float*)g->pobs, g->mask, (float)beta,
+                                                   (float*)g->hat_b, skip);
+      LTB_LAUNCH_CHECK(ctx);
+      int st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, false, (const float*)g->hat_b, P, 0, false, Kf, P, 0,
+                               (float*)g->hat_a, NT, 0, 3, true, Kf + P * P, nullptr, nullptr, nullptr, skip);
+      if (st == LTB_OK) {
+        LTB_TRY(pga_svt(g, mu, skip));
+        st = ltb_tc_gemm_f32(ctx, 1, NT, P, P, true, (const float*)g->hat_b, NT, 0, false, Ki, P, 0, xn, P, 0, 3,
+                             false, Ki + P * P, nullptr, nullptr, nullptr, skip);
+        if (st != LTB_OK) return st == LTB_EUNSUPPORTED ? ltb_set_error(ctx, LTB_ECUDA, "pga: inverse tc path") : st;
+        const int nb = (int)std::min<int64_t>(g->nblocks_cap, 2 * ctx->num_sms);
+        pga_norms_kernel<<<nb, 256, 0, ctx->stream>>>(E, xn, xc, xp, (const float*)g->gt, (float)beta,
+                                                      g->partials, skip);
+        LTB_LAUNCH_CHECK(ctx);
+        g->nblocks = nb;
+        pga_finalize_kernel<<<1, 160, 0, ctx->stream>>>(g->partials, g->nblocks, rec, g->d_state, g->d_scalars,
+                                                        tol);
+        LTB_LAUNCH_CHECK(ctx);
+        return LTB_OK;
+      }
+      if (st != LTB_EUNSUPPORTED) return st;
+      g->tc_off = true;  // this shape stays on the fused tile engine
+    }
+  }
+  // forward: gradient step fused into the load, slice-major store
+  if (!pga_plan<Tc, Tm>(g->spec, g->NT, 0, p, &smem))
+    return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
+  {
+    LoadPGA<R> ld{xc, xp, (const R*)g->pobs, g->mask, (R)beta};
+    StorePlain<Tc, false> st{(Tc*)g->hat_a, LTB_SLICE_MAJOR};
+    LTB_TRY((launch_xform_tile<Tc, Tm>(ctx, p, ld, st, (const Tm*)g->spec->d_mats[dbl][0], nullptr, skip, smem)));
+  }
+  // slice SVT with tau = mu_k
+  LTB_TRY(pga_svt(g, mu, skip));
   // inverse with the fused norms epilogue
   if (!pga_plan<Tc, Tm>(g->spec, g->NT, 1, p, &smem))
     return ltb_set_error(ctx, LTB_ESHAPE, "pga: tube too long for the fused transform");
@@ -311,6 +412,7 @@ int ltb_pga_create(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t i1, in
   alloc(hs * E, &g->hat_a);
   alloc(hs * E, &g->hat_b);
   alloc(sizeof(double) * 5 * nb, (void**)&g->partials);
+  g->nblocks_cap = nb;
   alloc(sizeof(int) * 4, (void**)&g->d_state);
   alloc(sizeof(double) * 4, (void**)&g->d_scalars);
   if (h_gt) alloc(rs * E, &g->gt);
