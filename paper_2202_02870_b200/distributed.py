@@ -72,29 +72,36 @@ class DeviceEngine:
         s = torch.cuda.current_stream().cuda_stream
         nat.check(nat.lib().ltb_ctx_set_stream(nat.context(), s if s else 1))
 
-    def _xform(self, x: torch.Tensor, rows: int, cols: int, inverse: bool, layout_in, layout_out, out_dtype):
+    def _xform(self, x: torch.Tensor, rows: int, cols: int, inverse: bool, layout_in, layout_out, out_dtype,
+               out=None):
         out_shape = (self.P, rows, cols) if layout_out == nat.SLICE_MAJOR else (rows, cols) + self.trailing
-        out = torch.empty(out_shape, dtype=_TORCH_DT[np.dtype(out_dtype)], device=x.device)
+        if out is None:
+            out = torch.empty(out_shape, dtype=_TORCH_DT[np.dtype(out_dtype)], device=x.device)
+        elif tuple(out.shape) != out_shape or out.dtype != _TORCH_DT[np.dtype(out_dtype)] or not out.is_contiguous():
+            raise ShapeError(f"out must be a contiguous {out_shape} {np.dtype(out_dtype)} tensor")
         if out.numel():
             xv, ov = _view(x.contiguous()), _view(out)
             nat.check(nat.lib().ltb_transform(nat.context(), self.handle.ptr, rows * cols, int(inverse), xv.code,
                                               layout_in, xv.ptr, ov.code, layout_out, ov.ptr, None))
         return out
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, out=None) -> torch.Tensor:
         """(rows, cols, trailing) -> slice-major (P, rows, cols)."""
         hat_dt = forward_dtype(np.dtype(str(x.dtype).replace("torch.", "")), self.spec)
-        return self._xform(x, x.shape[0], x.shape[1], False, nat.TUBE_MAJOR, nat.SLICE_MAJOR, hat_dt)
+        return self._xform(x, x.shape[0], x.shape[1], False, nat.TUBE_MAJOR, nat.SLICE_MAJOR, hat_dt, out)
 
-    def inverse(self, hat: torch.Tensor, real: bool) -> torch.Tensor:
+    def inverse(self, hat: torch.Tensor, real: bool, out=None) -> torch.Tensor:
         dt = np.dtype(str(hat.dtype).replace("torch.", ""))
         out_dt = nat.real_of(dt) if real else dt
-        return self._xform(hat, hat.shape[1], hat.shape[2], True, nat.SLICE_MAJOR, nat.TUBE_MAJOR, out_dt)
+        return self._xform(hat, hat.shape[1], hat.shape[2], True, nat.SLICE_MAJOR, nat.TUBE_MAJOR, out_dt, out)
 
-    def slice_gemm(self, ah: torch.Tensor, bh: torch.Tensor) -> torch.Tensor:
+    def slice_gemm(self, ah: torch.Tensor, bh: torch.Tensor, out=None) -> torch.Tensor:
         P, m, k = ah.shape
         n = bh.shape[2]
-        out = torch.empty((P, m, n), dtype=ah.dtype, device=ah.device)
+        if out is None:
+            out = torch.empty((P, m, n), dtype=ah.dtype, device=ah.device)
+        elif tuple(out.shape) != (P, m, n) or out.dtype != ah.dtype or not out.is_contiguous():
+            raise ShapeError(f"out must be a contiguous {(P, m, n)} {ah.dtype} tensor")
         a, b, c = _view(ah.contiguous()), _view(bh.contiguous()), _view(out)
         nat.check(nat.lib().ltb_slice_gemm(nat.context(), a.code, P, m, n, k, nat.OP_N, a.ptr, k, m * k, nat.OP_N,
                                            b.ptr, n, k * n, c.ptr, n, m * n))
@@ -174,27 +181,134 @@ def slices_to_fibres(slices: torch.Tensor, P: int, group=None) -> torch.Tensor:
 
 
 # ----------------------------------------------------------------- sharded operations
-def dist_l_product(a_rows: torch.Tensor, b_rows: torch.Tensor, engine, group=None) -> torch.Tensor:
+class DistLProductPlan:
+    """Row-sharded a *_L b (linalg.py:34-43) with every buffer allocated once.
+
+    Rank g holds rows R_g of A (r_g x l x trailing) and the row block K_g of B (k_g x I2 x
+    trailing) and produces rows R_g of C.  One step: K1 of both local operands into
+    slice-major buffers, an all-gather of the B-hat row blocks straight into one contiguous
+    (world, P, kmax, I2) buffer (the only exchange; no all-to-all is needed), one permute to
+    (P, l, I2), the slice GEMM and K1'.  The row-block sizes are exchanged once here (the
+    only host synchronisation), so `run` is a fixed launch sequence on the current stream."""
+
+    def __init__(self, a_shape, b_shape, engine, dtype: torch.dtype, device, group=None, exchange=None):
+        self.engine, self.group = engine, group
+        self.world, self.rank = _world(group)
+        # exchange=True keeps the all-gather + permute even on one rank (tests of that path)
+        self.exchange = self.world > 1 if exchange is None else bool(exchange)
+        a_shape, b_shape = tuple(a_shape), tuple(b_shape)
+        r, l = a_shape[:2]
+        k_g, I2 = b_shape[:2]
+        if a_shape[2:] != b_shape[2:] or a_shape[2:] != tuple(engine.trailing):
+            raise ShapeError(f"trailing dims of {a_shape} and {b_shape} must both be {tuple(engine.trailing)}")
+        sizes = torch.zeros(self.world, dtype=torch.int64, device=device)
+        mine = torch.tensor([k_g], dtype=torch.int64, device=device)
+        if self.world > 1:
+            dist.all_gather_into_tensor(sizes, mine, group=group)
+        else:
+            sizes.copy_(mine)
+        self.sizes = [int(v) for v in sizes.tolist()]
+        if sum(self.sizes) != l:
+            raise ShapeError(f"B row blocks {self.sizes} do not add up to A's column count {l}")
+        np_dt = np.dtype(str(dtype).replace("torch.", ""))
+        hat_t = _TORCH_DT[np.dtype(forward_dtype(np_dt, engine.spec))]
+        P, kmax = engine.P, max(self.sizes)
+        self.a_shape, self.b_shape, self.dtype = a_shape, b_shape, dtype
+        self.real = not dtype.is_complex
+        self.k_g, self.kmax, self.I2, self.l, self.P = k_g, kmax, I2, l, P
+        new = lambda *shape, dt=hat_t: torch.empty(shape, dtype=dt, device=device)
+        self.ha = new(P, r, l)
+        self.hc = new(P, r, I2)
+        # own row block, padded to kmax rows so every rank contributes an equal all-gather block
+        self.hb_loc = torch.zeros((P, kmax, I2), dtype=hat_t, device=device)
+        self.hb_tmp = None if k_g == kmax else new(P, k_g, I2)
+        self.equal = len(set(self.sizes)) == 1
+        if not self.exchange:
+            self.hb_all, self.hb, self.rows = None, self.hb_loc, None
+        else:
+            self.hb_all = new(self.world * P * kmax * I2)
+            self.hb = new(P, l, I2)
+            # unequal blocks: the valid rows of the permuted (P, world * kmax, I2) gather
+            self.rows = None if self.equal else torch.tensor(
+                [g * kmax + i for g, s in enumerate(self.sizes) for i in range(s)], dtype=torch.int64, device=device)
+        self.c_shape = (r, I2) + tuple(engine.trailing)
+
+    def _check(self, a, b):
+        if tuple(a.shape) != self.a_shape or tuple(b.shape) != self.b_shape:
+            raise ShapeError(f"plan was built for A {self.a_shape}, B {self.b_shape}; got {tuple(a.shape)}, "
+                             f"{tuple(b.shape)}")
+
+    def _local(self, a, b):
+        """Phase 1: K1 of the local A rows and B row block (no communication)."""
+        eng = self.engine
+        eng.forward(a, out=self.ha)
+        if self.hb_tmp is None:
+            eng.forward(b, out=self.hb_loc)
+        else:
+            eng.forward(b, out=self.hb_tmp)
+            self.hb_loc[:, : self.k_g].copy_(self.hb_tmp)
+
+    def _exchange(self):
+        """Phase 2: the B-hat all-gather (the only collective)."""
+        if self.exchange:
+            dist.all_gather_into_tensor(self.hb_all, self.hb_loc.reshape(-1), group=self.group)
+
+    def _finish(self, out):
+        """Phase 3: permute the gathered blocks to (P, l, I2), slice GEMM, K1'."""
+        if self.exchange:
+            P, W, kmax, I2 = self.P, self.world, self.kmax, self.I2
+            gathered = self.hb_all.view(W, P, kmax, I2).transpose(0, 1)  # (P, W, kmax, I2)
+            if self.equal:
+                self.hb.view(P, W, kmax, I2).copy_(gathered)
+            else:
+                torch.index_select(gathered.reshape(P, W * kmax, I2), 1, self.rows, out=self.hb)
+        self.engine.slice_gemm(self.ha, self.hb, out=self.hc)
+        return self.engine.inverse(self.hc, self.real, out=out)
+
+    def run(self, a: torch.Tensor, b: torch.Tensor, out=None) -> torch.Tensor:
+        self._check(a, b)
+        self._local(a, b)
+        self._exchange()
+        return self._finish(out)
+
+    def graphed(self, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, stream):
+        """Capture the two compute phases for the fixed buffers a, b, out as CUDA graphs on
+        `stream` (the stream the engine's context launches on) and return a step callable:
+        replay phase 1, the all-gather eagerly on the same stream, replay phase 3.  The
+        collective stays outside the graphs so capture never depends on the NCCL build."""
+        self._check(a, b)
+        self.run(a, b, out=out)  # settle kernel attributes / tensor-map caches before capture
+        g1, g3 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        if not self.exchange:
+            with torch.cuda.graph(g3, stream=stream):  # no collective: one graph for the whole step
+                self._local(a, b)
+                self._finish(out)
+            return g3.replay
+        with torch.cuda.graph(g1, stream=stream):
+            self._local(a, b)
+        with torch.cuda.graph(g3, stream=stream):
+            self._finish(out)
+
+        def step():
+            g1.replay()
+            self._exchange()
+            g3.replay()
+
+        return step
+
+
+def dist_l_product(a_rows: torch.Tensor, b_rows: torch.Tensor, engine, group=None, out=None) -> torch.Tensor:
     """Row-sharded a *_L b (linalg.py:34-43): rank g holds rows R_g of A (I1 x l x ...) and the row
     block K_g of B (l x I2 x ...); returns rows R_g of C.  B-hat is all-gathered (NCCL all-gather);
-    no all-to-all is needed."""
-    world, _ = _world(group)
-    ah = engine.forward(a_rows)                    # (P, r_g, l)
-    bh_local = engine.forward(b_rows)              # (P, k_g, I2)
-    sizes = [torch.zeros(1, dtype=torch.int64, device=bh_local.device) for _ in range(world)]
-    dist.all_gather(sizes, torch.tensor([bh_local.shape[1]], dtype=torch.int64, device=bh_local.device), group=group)
-    sizes = [int(s.item()) for s in sizes]
-    kmax = max(sizes)
-    P, _, I2 = bh_local.shape
-    # all-gather needs equal blocks: pad the row block to the largest, trim after
-    padded = bh_local.new_zeros((P, kmax, I2))
-    padded[:, : bh_local.shape[1]] = bh_local
-    parts = [bh_local.new_empty((P, kmax, I2)) for _ in range(world)]
-    dist.all_gather(parts, padded, group=group)
-    bh = torch.cat([p[:, :s] for p, s in zip(parts, sizes)], dim=1)  # (P, l, I2)
-    ch = engine.slice_gemm(ah, bh)
-    real = not (a_rows.is_complex() or b_rows.is_complex())
-    return engine.inverse(ch, real)
+    no all-to-all is needed.  The DistLProductPlan is cached on the engine per shape/dtype."""
+    key = (tuple(a_rows.shape), tuple(b_rows.shape), a_rows.dtype, str(a_rows.device), id(group))
+    plans = engine.__dict__.setdefault("_dist_plans", {})
+    plan = plans.get(key)
+    if plan is None:
+        if a_rows.dtype != b_rows.dtype:
+            raise ShapeError(f"operand dtypes differ: {a_rows.dtype} vs {b_rows.dtype}")
+        plan = plans[key] = DistLProductPlan(a_rows.shape, b_rows.shape, engine, a_rows.dtype, a_rows.device, group)
+    return plan.run(a_rows.contiguous(), b_rows.contiguous(), out=out)
 
 
 def dist_svt(x_rows: torch.Tensor, tau: float, I1: int, engine, group=None) -> torch.Tensor:

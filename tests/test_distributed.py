@@ -24,19 +24,28 @@ class OracleEngine:
         self.trailing = tuple(trailing)
         self.P = int(np.prod(trailing))
 
-    def forward(self, x):
+    @staticmethod
+    def _into(res, out):
+        if out is None:
+            return res
+        assert tuple(out.shape) == tuple(res.shape) and out.dtype == res.dtype
+        out.copy_(res)
+        return out
+
+    def forward(self, x, out=None):
         a = x.numpy()
         h = O.forward(a, self.spec)
-        return torch.from_numpy(np.ascontiguousarray(h.reshape(a.shape[0], a.shape[1], self.P).transpose(2, 0, 1)))
+        res = torch.from_numpy(np.ascontiguousarray(h.reshape(a.shape[0], a.shape[1], self.P).transpose(2, 0, 1)))
+        return self._into(res, out)
 
-    def inverse(self, hat, real):
+    def inverse(self, hat, real, out=None):
         h = hat.numpy()
         t = np.ascontiguousarray(h.transpose(1, 2, 0)).reshape((h.shape[1], h.shape[2]) + self.trailing)
-        out = O.inverse(t, self.spec, assume_real=real)
-        return torch.from_numpy(np.ascontiguousarray(out))
+        res = O.inverse(t, self.spec, assume_real=real)
+        return self._into(torch.from_numpy(np.ascontiguousarray(res)), out)
 
-    def slice_gemm(self, ah, bh):
-        return torch.from_numpy(np.matmul(ah.numpy(), bh.numpy()))
+    def slice_gemm(self, ah, bh, out=None):
+        return self._into(torch.from_numpy(np.matmul(ah.numpy(), bh.numpy())), out)
 
     def svt(self, hat, tau):
         h = hat.numpy()

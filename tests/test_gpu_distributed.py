@@ -12,7 +12,8 @@ import torch
 import torch.distributed as dist
 
 import paper_2202_02870_b200 as L
-from paper_2202_02870_b200.distributed import DeviceEngine, dist_l_product, dist_pga_complete, dist_svt
+from paper_2202_02870_b200.distributed import (DeviceEngine, DistLProductPlan, dist_l_product, dist_pga_complete,
+                                               dist_svt)
 from conftest import rel_err
 
 pytestmark = pytest.mark.gpu
@@ -40,6 +41,23 @@ def test_dist_l_product_device(nccl_world1):
     c = dist_l_product(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), eng)
     torch.cuda.synchronize()
     assert rel_err(c.cpu().numpy(), L.l_product(a, b, spec)) < 1e-5
+
+
+@pytest.mark.parametrize("transform,dtype,tol", [("dct", np.float32, 1e-5), ("fft", np.float64, 1e-10)])
+def test_dist_plan_exchange_device(nccl_world1, transform, dtype, tol):
+    """The plan with its NCCL all-gather + permute kept at world 1, preallocated output."""
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((40, 24, 4, 6)).astype(dtype)
+    b = rng.standard_normal((24, 36, 4, 6)).astype(dtype)
+    spec = L.make_spec(transform, (40, 36, 4, 6))
+    eng = DeviceEngine(spec, (4, 6))
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    plan = DistLProductPlan(ta.shape, tb.shape, eng, ta.dtype, ta.device, exchange=True)
+    out = torch.empty(plan.c_shape, dtype=ta.dtype, device="cuda")
+    for _ in range(2):  # buffers are reused across runs
+        plan.run(ta, tb, out=out)
+    torch.cuda.synchronize()
+    assert rel_err(out.cpu().numpy(), L.l_product(a, b, spec)) < tol
 
 
 def test_dist_svt_device(nccl_world1):
