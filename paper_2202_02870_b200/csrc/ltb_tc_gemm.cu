@@ -465,7 +465,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // resident constant with a precomputed lo part (RB).
 constexpr int kTm3 = 4;                   // TMEM A stages (hi + lo, 64 columns each)
 constexpr int kThreads3 = 512;            // 16 warps: TMA, MMA, 4 A converters, 2 B converters, 8 epilogue
-constexpr int kConvA = 128, kConvB = 64;  // converter threads (warps 2-5 for A, 6-7 for B)
+// converter threads: warps 2-5 for A; for B warps 6-7 plus, without a resident B (the
+// epilogue then has 4 warps), warps 12-15
+constexpr int kConvA = 128, kConvB = 192;
 
 template <int BN, bool A_MN, bool B_MN, bool RB>
 struct Tc3Cfg {
@@ -500,6 +502,31 @@ __device__ __forceinline__ void umma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, u
       "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
 
+// warp-uniform issue: every lane executes the call, one elected lane issues the
+// instruction, so the operands stay in uniform registers (no per-MMA R2UR
+// waterfall, which a lane-0-only branch forces and which halves the MMA rate)
+__device__ __forceinline__ void umma_tf32_ta_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
@@ -520,6 +547,11 @@ struct Tc3Extras {
   const int* skip;       // device flag, or null
   float* c_direct;       // C^T output written with coalesced per-column stores (lanes = rows), or null
   int64_t ldc, sc;
+  // C written by the warps themselves (each 32 x 32 box staged in shared memory, then read
+  // back four 128-byte rows per instruction and stored coalesced) instead of TMA stores:
+  // keeps the epilogue out of the TMA unit's queue, which the operand loads fill; or null
+  float* c_lsu;
+  int c_vec;  // C, ldc and sc allow 16-byte vector stores
 };
 
 template <int BN, bool A_MN, bool B_MN, bool RB>
@@ -538,6 +570,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
     }
   };
   if (threadIdx.x == 0) stamp(0);
+  auto cta_stamp = [&](int k) {  // per-CTA start / end (slots 256 + 2 * CTA + k)
+    if (dbg) {
+      unsigned long long tns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+      dbg[256 + 2 * blockIdx.x + k] = tns;
+    }
+  };
+  if (threadIdx.x == 0) cta_stamp(0);
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int SMS = Cfg::SMS;
@@ -621,8 +661,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tma_load_3d(b_lo(0, kt), &tmBlo, bres, kt * kBK, 0, 0);
         }
       }
-      int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int it = 0, j_t = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++j_t) {
         int b, m0, n0;
         decode(t, b, m0, n0);
         const int kt_b = ktiles_of(b);
@@ -630,6 +670,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
           const int s = it % SMS;
           mbar_wait(&sfree[s], ((it / SMS) & 1) ^ 1);
           if (it == 0) stamp(2);
+          if (kt == 0 && j_t < 16) stamp(16 + j_t);
           mbar_expect_tx(&full[s], RB ? Cfg::A_BYTES : Cfg::A_BYTES + Cfg::B_BYTES);
           const int k0 = kt * kBK;
           if (!A_MN) {
@@ -671,22 +712,27 @@ __global__ void __launch_bounds__(kThreads3, 1)
         const int s = it % SMS, ts = it % kTm3;
         mbar_wait(&tfull[ts], (it / kTm3) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t ahi = tmem + (uint32_t)(Cfg::ACOL + 64 * ts), alo = ahi + 32;
+        if (lane == 0 && it < 16) stamp(80 + it);
+        const uint32_t ahi = tmem + (uint32_t)(Cfg::ACOL + 64 * ts), alo = ahi + 32;
+        // descriptor address field = byte address >> 4 (< 2^14 for any shared-memory
+        // address), so the K step is added to the descriptor directly
+        const uint64_t dbh0 = umma_desc(smem_u32(b_hi(s, kt)), lboB, sboB, B_MN);
+        const uint64_t dbl0 = umma_desc(smem_u32(b_lo(s, kt)), lboB, sboB, B_MN);
 #pragma unroll
-          for (int kk = 0; kk < kBK / 8; ++kk) {
-            const uint32_t kofb = (B_MN ? 1024u : 32u) * kk;
-            const uint64_t dbh = umma_desc(smem_u32(b_hi(s, kt)) + kofb, lboB, sboB, B_MN);
-            const uint64_t dbl = umma_desc(smem_u32(b_lo(s, kt)) + kofb, lboB, sboB, B_MN);
-            umma_tf32_ta(dacc, ahi + 8 * kk, dbh, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
-            umma_tf32_ta(dacc, ahi + 8 * kk, dbl, idesc, 1u);
-            umma_tf32_ta(dacc, alo + 8 * kk, dbh, idesc, 1u);
-          }
-          if (it == 0) stamp(4);
-          umma_commit(&tfree[ts]);
-          if (!RB) umma_commit(&sfree[s]);  // B of this smem stage has been read
-          if (kt == kt_b - 1) umma_commit(&accf[a]);
+        for (int kk = 0; kk < kBK / 8; ++kk) {
+          const uint64_t kof = (uint64_t)(((B_MN ? 1024u : 32u) * kk) >> 4);
+          umma_tf32_ta_w(dacc, ahi + 8 * kk, dbh0 + kof, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+          umma_tf32_ta_w(dacc, ahi + 8 * kk, dbl0 + kof, idesc, 1u);
+          umma_tf32_ta_w(dacc, alo + 8 * kk, dbh0 + kof, idesc, 1u);
         }
+        if (lane == 0) {
+          if (it == 0) stamp(4);
+          if (it < 16) stamp(112 + it);
+          if (kt == kt_b - 1 && j < 16) stamp(32 + j);
+        }
+        umma_commit_w(&tfree[ts]);
+        if (!RB) umma_commit_w(&sfree[s]);  // B of this smem stage has been read
+        if (kt == kt_b - 1) umma_commit_w(&accf[a]);
         __syncwarp();
       }
     }
@@ -702,6 +748,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       for (int kt = 0; kt < kt_b; ++kt, ++it) {
         const int s = it % SMS, ts = it % kTm3;
         mbar_wait(&full[s], (it / SMS) & 1);
+        if (threadIdx.x == 64 && it < 16) stamp(96 + it);
         uint32_t hi[32], lo[32];
         const unsigned char* ab = a_raw(s);
         if (!A_MN) {  // 128B-swizzled rows: 16-byte chunk c of row r sits at c ^ (r & 7)
@@ -735,13 +782,15 @@ __global__ void __launch_bounds__(kThreads3, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         if (it == 0 && threadIdx.x == 64) stamp(3);
+        if (threadIdx.x == 64 && it < 16) stamp(64 + it);
+        if (threadIdx.x == 160 && it < 16) stamp(128 + it);
         mbar_arrive(&tfull[ts]);
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < 8 || (!RB && warp >= 12)) {
     // ---------------------------------------------------------------- B split in shared memory
     if constexpr (!RB) {
-      const int cv = threadIdx.x - 192;  // 0 .. kConvB-1
+      const int cv = warp < 8 ? threadIdx.x - 192 : threadIdx.x - 320;  // 0 .. kConvB-1
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int b, m0, n0;
@@ -777,6 +826,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const int a = j & 1;
       mbar_wait(&accf[a], (j >> 1) & 1);
       if (j == 0 && q == 0 && lane == 0) stamp(5);
+      const bool tl = (j < 4 && warp == 8 && lane == 0);
+      int ck = 0;
+      if (tl) stamp(160 + 4 * j);
       tc_fence_after();
       const int row0 = m0 + 32 * q;
       const bool zero = ktiles_of(b) == 0;
@@ -786,6 +838,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
         uint32_t r[32];
         if (!zero) {
           tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * BN + c0), r);
+          if (tl && ck < 2) stamp(179 + 8 * j + 4 * ck);
         } else {
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) r[jj] = 0u;
@@ -810,8 +863,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
           continue;
         }
         unsigned char* box = ebuf + (nbox & 1) * 4096;
-        if (lane == 0) bulk_wait_read<1>();
+        if (!ex.c_lsu && lane == 0) bulk_wait_read<1>();
         __syncwarp();
+        if (tl && ck < 2) stamp(176 + 8 * j + 4 * ck);
         if (!ct) {
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj)
@@ -824,7 +878,38 @@ __global__ void __launch_bounds__(kThreads3, 1)
             *reinterpret_cast<float*>(box + jj * 128 + (((lane >> 2) ^ (jj & 7)) << 4) + ((lane & 3) << 2)) =
                 __uint_as_float(r[jj]);
         }
+        if (tl && ck < 2) stamp(177 + 8 * j + 4 * ck);
+        if (ex.c_lsu) {
+          // box row r (output row of C, or of C^T when ct), 16-byte chunk cc at
+          // r * 128 + ((cc ^ (r & 7)) << 4): 8 lanes per row, 4 rows per instruction
+          __syncwarp();
+          const int r_lim = ct ? N : M, c_lim = ct ? M : N;
+          const int gr0 = ct ? n0 + c0 : row0, gc = (ct ? row0 : n0 + c0) + 4 * (lane & 7);
+          float* cbase = ex.c_lsu + (int64_t)b * ex.sc;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + (lane >> 3), gr = gr0 + r;
+            const float4 v = *reinterpret_cast<const float4*>(box + r * 128 + (((lane & 7) ^ (r & 7)) << 4));
+            if (gr < r_lim) {
+              float* dst = cbase + (int64_t)gr * ex.ldc + gc;
+              if (ex.c_vec && gc + 3 < c_lim) {
+                *reinterpret_cast<float4*>(dst) = v;
+              } else {
+                const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if (gc + u < c_lim) dst[u] = e[u];
+              }
+            }
+          }
+          __syncwarp();
+          if (tl && ck < 2) stamp(162 + 4 * j + ck);
+          ++ck;
+          ++nbox;
+          continue;
+        }
         fence_proxy_async();
+        if (tl && ck < 2) stamp(178 + 8 * j + 4 * ck);
         __syncwarp();
         if (lane == 0 && row0 < M) {
           if (!ct)
@@ -832,14 +917,17 @@ __global__ void __launch_bounds__(kThreads3, 1)
           else
             tma_store_3d(&tmC, box, row0, n0 + c0, b);
           bulk_commit();
+          if (tl) stamp(162 + 4 * j + min(ck, 1));
+          ++ck;
         }
         ++nbox;
       }
       tc_fence_before();
       if (j == 0 && q == 0 && lane == 0) stamp(6);
+      if (j < 16 && q == 0 && half == 0 && lane == 0) stamp(48 + j);
       mbar_arrive(&acce[a]);
     }
-    if (lane == 0) bulk_wait_all();
+    if (!ex.c_lsu && lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -847,6 +935,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
     tc_fence_after();
     if (lane == 0) stamp(7);
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if (lane == 0) cta_stamp(1);
   }
 }
 
@@ -868,6 +957,9 @@ int g_rb = 1;
 int g_tc3 = 1;
 // transposed outputs: coalesced direct stores (1) / smem box + TMA store (0)
 int g_ct_direct = 0;
+// tc3 epilogue: warp-coalesced stores from the shared-memory box (1) / TMA tensor stores (0,
+// measured faster on the config-2 step: 51 vs 63 us)
+int g_epi_lsu = 0;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1007,7 +1099,9 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
                     int64_t lda, int64_t sa, bool b_mn, const float* B, int64_t ldb, int64_t sb, float* C,
                     int64_t ldc, int64_t sc, int split, bool c_trans, const float* b_lo, const int* klim,
                     const float* rscale, const float* cscale, const int* skip) {
-  const Tc3Extras ex{klim, rscale, cscale, skip, (c_trans && g_ct_direct) ? C : nullptr, ldc, sc};
+  const bool c_vec = (reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 4 == 0 && (batch == 1 || sc % 4 == 0);
+  const Tc3Extras ex{klim, rscale, cscale, skip, (c_trans && g_ct_direct) ? C : nullptr, ldc, sc,
+                     g_epi_lsu ? C : nullptr, c_vec ? 1 : 0};
   const bool extras = klim || rscale || cscale || skip;
   if (batch < 1 || M < 1 || N < 1 || K < 1 || batch > 65535) return LTB_EUNSUPPORTED;
   if (M > (1 << 30) || N > (1 << 30) || K > (1 << 30)) return LTB_EUNSUPPORTED;
@@ -1067,6 +1161,7 @@ extern "C" void ltb_tc_debug_set_pdl(int v) { g_pdl = v; }
 extern "C" void ltb_tc_debug_set_rb(int v) { g_rb = v; }
 extern "C" void ltb_tc_debug_set_tc3(int v) { g_tc3 = v; }
 extern "C" void ltb_tc_debug_set_ct_direct(int v) { g_ct_direct = v; }
+extern "C" void ltb_tc_debug_set_epi_lsu(int v) { g_epi_lsu = v; }
 extern "C" void ltb_tc_debug_set_timeline(void* d_buf) { g_dbg = (unsigned long long*)d_buf; }
 
 extern "C" void ltb_tc_debug_set_mn_strides(uint32_t lbo, uint32_t sbo) {
@@ -1082,4 +1177,164 @@ extern "C" int ltb_tc_gemm(ltb_ctx* ctx, int64_t batch, int64_t m, int64_t n, in
                            ldb, sb, (float*)d_c, ldc, sc, split, false, nullptr);
   if (st == LTB_EUNSUPPORTED) return ltb_set_error(ctx, LTB_EUNSUPPORTED, "tc_gemm: shape/alignment unsupported");
   return st;
+}
+
+// ------------------------------------------------------------------ debug: raw MMA issue rate
+// One CTA issues `iters` x 12 kind::tf32 MMAs (M = 128, N = BN, K = 8 each) into one
+// accumulator; returns SM cycles from the first issue to the commit's arrival.
+// pattern 0: A from shared memory, one A / one B tile; 1: A from TMEM, one A / one B;
+// 2: the 3xTF32 order of tc3_kernel (A hi/lo in TMEM, B hi/lo in smem, per K step
+// hi*hi, hi*lo, lo*hi); 3: the same MMAs grouped by operand pair (4 x hi*hi, 4 x hi*lo,
+// 4 x lo*hi).  pattern | 4: warps 4-7 load TMEM (32 columns each, like the epilogue)
+// while the MMAs run; | 8: warps 8-11 store TMEM (like the converters); | 16: warps
+// 12-15 stream shared memory (float4 reads + writes); | 32: A at TMEM column 192 (as
+// tc3_kernel with BN = 96); | 64: 148 CTAs (one per SM) instead of one; | 128: random
+// operand values instead of zeros; | 256: B cycles through 3 K blocks (timing only).
+template <int BN>
+__global__ void mma_rate_kernel(int pattern, int iters, unsigned long long* out) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ volatile int done;
+  constexpr int ABYTES = kBM * 128, BBYTES = BN * 128;
+  if (threadIdx.x == 0) done = 0;
+  const bool rnd = pattern & 128;
+  auto hv = [&](uint32_t i) {  // deterministic pseudo-random value in [-1, 1)
+    i = i * 2654435761u + 12345u;
+    i ^= i >> 13;
+    i *= 0x5bd1e995u;
+    i ^= i >> 15;
+    return rnd ? (float)(i & 0xFFFFFF) / 8388608.f - 1.f : 0.f;
+  };
+  for (int i = threadIdx.x; i < (ABYTES + 6 * BBYTES + 32768) / 16; i += blockDim.x)
+    reinterpret_cast<float4*>(base)[i] = make_float4(hv(4 * i), hv(4 * i + 1), hv(4 * i + 2), hv(4 * i + 3));
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int warp = threadIdx.x >> 5;
+  const int mode = pattern & 3;
+  if (warp < 4) {  // A hi / lo tiles in TMEM (columns 192 .. 319)
+    uint32_t r[32];
+    for (int c = 0; c < 4; ++c) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(hv(threadIdx.x * 131 + c * 32 + i + 7777));
+      tmem_st32(tmem + ((uint32_t)(32 * warp) << 16) + 192u + 32u * c, r);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp >= 4 && warp < 8 && (pattern & 4)) {
+    uint32_t r[32];
+    unsigned acc = 0;
+    while (!done) {
+      tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 320u, r);
+      acc += r[0];
+    }
+    if (acc == 12345u) out[1] = acc;
+  } else if (warp >= 8 && warp < 12 && (pattern & 8)) {
+    uint32_t r[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) r[i] = 0u;
+    while (!done) {
+      tmem_st32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 416u, r);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+  } else if (warp >= 12 && (pattern & 16)) {
+    float4* sp = reinterpret_cast<float4*>(base + ABYTES + 6 * BBYTES);
+    const int t = threadIdx.x - 384;
+    while (!done) {
+#pragma unroll 4
+      for (int i = t; i < 2048; i += 128) {
+        float4 v = sp[i];
+        v.x += 1.f;
+        sp[(i + 64) & 2047] = v;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = idesc_tf32(BN, false, false);
+    const uint32_t sa = smem_u32(base), sbh = smem_u32(base + ABYTES), sbl = sbh + BBYTES;
+    const uint32_t acol = (pattern & 32) ? 192u : 256u;
+    const uint32_t ahi = tmem + acol, alo = tmem + acol + 32u;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      if (mode == 0) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_tf32(tmem, umma_desc(sa + 32u * kk, 16u, 1024u), umma_desc(sbh + 32u * kk, 16u, 1024u), idesc,
+                      (i | r | kk) ? 1u : 0u);
+      } else if (mode == 1) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_tf32_ta(tmem, ahi + 8u * kk, umma_desc(sbh + 32u * kk, 16u, 1024u), idesc, (i | r | kk) ? 1u : 0u);
+      } else if (mode == 2) {
+        // | 256: B cycles through 3 K blocks (hi + lo each), like the resident Kronecker matrix
+        const uint32_t boff = (pattern & 256) ? (uint32_t)(i % 3) * 2u * BBYTES : 0u;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t dbh = umma_desc(sbh + boff + 32u * kk, 16u, 1024u),
+                         dbl = umma_desc(sbh + boff + BBYTES + 32u * kk, 16u, 1024u);
+          umma_tf32_ta(tmem, ahi + 8u * kk, dbh, idesc, (i | kk) ? 1u : 0u);
+          umma_tf32_ta(tmem, ahi + 8u * kk, dbl, idesc, 1u);
+          umma_tf32_ta(tmem, alo + 8u * kk, dbh, idesc, 1u);
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_tf32_ta(tmem, ahi + 8u * kk, umma_desc(sbh + 32u * kk, 16u, 1024u), idesc, (i | kk) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_tf32_ta(tmem, ahi + 8u * kk, umma_desc(sbl + 32u * kk, 16u, 1024u), idesc, 1u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_tf32_ta(tmem, alo + 8u * kk, umma_desc(sbh + 32u * kk, 16u, 1024u), idesc, 1u);
+      }
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    if (blockIdx.x == 0) out[0] = (unsigned long long)(clock64() - t0);
+    done = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int BN>
+static int run_mma_rate(int pattern, int iters, unsigned long long* d_out) {
+  auto k = mma_rate_kernel<BN>;
+  const int smem = kBM * 128 + 6 * BN * 128 + 32768 + 1024;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return LTB_ECUDA;
+  k<<<(pattern & 64) ? 148 : 1, 512, smem>>>(pattern, iters, d_out);
+  return cudaGetLastError() == cudaSuccess ? LTB_OK : LTB_ECUDA;
+}
+
+extern "C" int ltb_tc_debug_mma_rate(int bn, int pattern, int iters, unsigned long long* d_out) {
+  switch (bn) {
+    case 64: return run_mma_rate<64>(pattern, iters, d_out);
+    case 96: return run_mma_rate<96>(pattern, iters, d_out);
+    case 128: return run_mma_rate<128>(pattern, iters, d_out);
+    case 256: return run_mma_rate<256>(pattern, iters, d_out);
+    default: return LTB_EPARAM;
+  }
 }
