@@ -274,6 +274,7 @@ def run_ours_dist(args):
             e1.synchronize()
             if i >= args.warmup:
                 e2e_times.append(e0.elapsed_time(e1) / 1e3)
+    pga = None if args.skip_extras else bench_pga_dist(L, torch, dist, eng_cls=DeviceEngine, args=args)
     t = torch.tensor([sum(times), sum(e2e_times)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t[0].item())
@@ -298,9 +299,45 @@ def run_ours_dist(args):
                 "api": "distributed.DistLProductPlan.run per rank, pinned host operands in / rows of C out"},
         "gpu_launches": int(launches), "clocks": clocks.summary(),
     }
+    if pga is not None:
+        line["pga"] = pga
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def bench_pga_dist(L, torch, dist, eng_cls, args):
+    """Config-3 PGA over all ranks (SURVEY.md §8(e), strong scaling): rank g owns a block of
+    i1 rows for the transforms and gradient step and a block of slices for K3; the layout
+    change is an NCCL all-to-all each way per iteration.  Time = max over ranks."""
+    from paper_2202_02870_b200.distributed import blocks, dist_pga_complete
+
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    m, mask = _cfg3_data_host()
+    spec = L.make_spec("dct", CFG3["shape"])
+    r0, r1 = blocks(m.shape[0], ws)[rank]
+    mu0 = 0.9 * float(np.linalg.norm(m.astype(np.float64)))  # cfg.nu * ||M||_F over the full tensor
+    eng = eng_cls(spec, m.shape[2:])
+    mt = torch.from_numpy(np.ascontiguousarray(m[r0:r1])).cuda()
+    kt = torch.from_numpy(np.ascontiguousarray(mask[r0:r1])).cuda()
+    res = None
+    for n in (3, args.pga_iters):  # warm-up run, then the timed run
+        cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=n)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        x, trace = dist_pga_complete(mt, kt, cfg, m.shape[0], eng, mu0=mu0)
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        res = (trace.iterations, float(t[0]))
+    its, secs = res
+    return {"metric": "PGA completion iters/sec", "value": its / secs, "unit": "it/s", "iterations": its,
+            "seconds": secs, "dtype": "f32", "scaling": "strong", "n_gpus": ws,
+            "timing": "device-synchronised wall time of the whole solve, max over ranks",
+            "config": {"workload": "config3 144x176x3x100 rank-10 DCT(modes 3,4), Bernoulli(0.2), tol 1e-300",
+                       "parallelism": f"i1 rows x{ws} (K1, K1', gradient) / slices x{ws} (K3), NCCL all-to-all",
+                       "data": "synthetic stand-in for the paper's colour videos (not in this container)"}}
 
 
 def run_ours(args):

@@ -177,6 +177,14 @@ int ltb_slice_svt(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,
  * and mirrored; otherwise identical to ltb_slice_svt. */
 int ltb_spec_slice_svt(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1, int64_t I2,
                        const void* d_a, double tau, void* d_out);
+/* svt's slice step for a caller that iterates (the PGA loop of completion.py:165-172
+ * run outside ltb_pga_run, e.g. by the slice-sharded multi-GPU solver): fp32 real
+ * slices, warm-started from the right singular bases of the previous call.
+ * d_v (batch x n x n, n = min(I1, I2)) is caller-owned: read when warm != 0 and
+ * rewritten on return; pass warm = 0 on the first call.  Needs n >= 32
+ * (LTB_EUNSUPPORTED otherwise: use ltb_slice_svt). */
+int ltb_slice_svt_carry(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* d_a, double tau,
+                        float* d_out, float* d_v, int warm);
 int ltb_slice_svd(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,
                   const void* d_a, void* d_u, void* d_s, void* d_v);
 int ltb_slice_singular_values(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,
@@ -188,6 +196,11 @@ int ltb_slice_singular_values(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m,
  * Deterministic (fixed-order two-stage) in float64. */
 int ltb_reduce_sumsq(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y,
                      double* h_out);
+
+/* as ltb_reduce_sumsq, result left in device memory (d_out[0..1]) with no host
+ * synchronisation (stream-ordered) */
+int ltb_reduce_sumsq_device(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y,
+                            double* d_out);
 
 /* Σ conj(x) * y in float64: h_out = {re, im} (inner_product / np.vdot, core.py:26-35) */
 int ltb_reduce_dot(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y, double* h_out);

@@ -64,6 +64,8 @@ _SIGNATURES = {
     "ltb_tc_gemm": ([_vp, _i64, _i64, _i64, _i64, _int, _vp, _i64, _i64, _int, _vp, _i64, _i64, _vp, _i64, _i64, _int],
                     _int),
     "ltb_slice_svt":([_vp, _int, _i64, _i64, _i64, _vp, C.c_double, _vp], _int),
+    "ltb_slice_svt_carry": ([_vp, _i64, _i64, _i64, _vp, C.c_double, _vp, _vp, _int], _int),
+    "ltb_reduce_sumsq_device": ([_vp, _int, _i64, _vp, _vp, _vp], _int),
     "ltb_spec_slice_svt": ([_vp, _vp, _int, _i64, _i64, _i64, _vp, C.c_double, _vp], _int),
     "ltb_slice_svd": ([_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp], _int),
     "ltb_slice_singular_values": ([_vp, _int, _i64, _i64, _i64, _vp, _vp], _int),

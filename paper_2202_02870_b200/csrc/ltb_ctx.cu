@@ -418,6 +418,22 @@ int ltb_slice_svt(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, 
   return ltb_svt_impl(ctx, dtype, batch, m, n, d_a, tau, nullptr, d_out, nullptr);
 }
 
+int ltb_slice_svt_carry(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* d_a, double tau,
+                        float* d_out, float* d_v, int warm) {
+  if (!(tau >= 0)) return ltb_set_error(ctx, LTB_EPARAM, "tau must be >= 0, got %g", tau);
+  if (batch < 0 || I1 < 0 || I2 < 0) return ltb_set_error(ctx, LTB_ESHAPE, "svt_carry: negative extent");
+  if (batch == 0 || I1 == 0 || I2 == 0) return LTB_OK;
+  const int st = ltb_svt_carry_impl(ctx, batch, I1, I2, d_a, tau, d_out, d_v, warm, nullptr);
+  if (st == LTB_EUNSUPPORTED)
+    return ltb_set_error(ctx, LTB_EUNSUPPORTED, "svt_carry: min(I1, I2) = %lld < 32",
+                         (long long)std::min(I1, I2));
+  return st;
+}
+
+int ltb_reduce_sumsq_device(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y, double* d_out) {
+  return ltb_reduce_sumsq_dev(ctx, dtype, n, d_x, d_y, d_out);
+}
+
 int ltb_reduce_sumsq(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y, double* h_out) {
   LTB_TRY(ltb_reduce_sumsq_dev(ctx, dtype, n, d_x, d_y, ctx->d_scratch));
   LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 2 * sizeof(double), cudaMemcpyDeviceToHost,

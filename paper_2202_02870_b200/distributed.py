@@ -115,6 +115,38 @@ class DeviceEngine:
                                               float(tau), o.ptr))
         return out
 
+    def svt_carried(self, hat: torch.Tensor, tau: float, state: dict) -> torch.Tensor:
+        """svt of this rank's slices warm-started from the right bases of the previous call
+        (ltb_slice_svt_carry, the fp32 PGA path of ltb_pga_run); `state` keeps the bases
+        between iterations.  Other dtypes and slices narrower than 32 use ltb_slice_svt."""
+        nb, m, n = hat.shape
+        if hat.dtype != torch.float32 or min(m, n) < 32 or not hat.numel():
+            return self.svt(hat, tau)
+        if state.get("v") is None or state["v"].shape[0] != nb:
+            state["v"] = torch.empty((nb, min(m, n), min(m, n)), dtype=torch.float32, device=hat.device)
+            state["warm"] = 0
+        out = torch.empty_like(hat)
+        h = hat.contiguous()
+        nat.check(nat.lib().ltb_slice_svt_carry(nat.context(), nb, m, n, h.data_ptr(), float(tau), out.data_ptr(),
+                                                state["v"].data_ptr(), int(state["warm"])))
+        state["warm"] = 1
+        return out
+
+    def norms_device(self, y, xn, gt) -> torch.Tensor:
+        """As `norms`, left on the device (float64 [sum (y - x+)^2, sum x+^2, sum (x+ - gt)^2,
+        max x+]) with no host synchronisation."""
+        buf = torch.zeros(6, dtype=torch.float64, device=xn.device)
+        if xn.numel():
+            lib, ctx, code = nat.lib(), nat.context(), _view(xn).code
+            nat.check(lib.ltb_reduce_sumsq_device(ctx, code, xn.numel(), y.data_ptr(), xn.data_ptr(), buf.data_ptr()))
+            nat.check(lib.ltb_reduce_sumsq_device(ctx, code, xn.numel(), xn.data_ptr(), None, buf[2:].data_ptr()))
+            if gt is not None:
+                nat.check(lib.ltb_reduce_sumsq_device(ctx, code, xn.numel(), xn.data_ptr(), gt.data_ptr(),
+                                                      buf[4:].data_ptr()))
+        else:
+            buf[3] = -math.inf
+        return torch.stack([buf[0], buf[2], buf[4], buf[3]])
+
     def gradient(self, xc, xp, pobs, mask_u8, beta):
         y, g = torch.empty_like(xc), torch.empty_like(xc)
         if xc.numel():
@@ -311,16 +343,20 @@ def dist_l_product(a_rows: torch.Tensor, b_rows: torch.Tensor, engine, group=Non
     return plan.run(a_rows.contiguous(), b_rows.contiguous(), out=out)
 
 
-def dist_svt(x_rows: torch.Tensor, tau: float, I1: int, engine, group=None) -> torch.Tensor:
+def dist_svt(x_rows: torch.Tensor, tau: float, I1: int, engine, group=None, carry=None) -> torch.Tensor:
     """Row-sharded svt (linalg.py:168-181): transform rows, all-to-all to slice blocks, SVT,
-    all-to-all back, inverse transform rows."""
+    all-to-all back, inverse transform rows.  `carry` (a dict kept by the caller across PGA
+    iterations) selects the engine's warm-started SVT when it has one."""
     if tau < 0:
         from .errors import ParameterError
 
         raise ParameterError(f"tau must be >= 0, got {tau}")
     hat = engine.forward(x_rows)
     sl = fibres_to_slices(hat, I1, group)
-    sl = engine.svt(sl, tau)
+    if carry is not None and hasattr(engine, "svt_carried"):
+        sl = engine.svt_carried(sl, tau, carry)
+    else:
+        sl = engine.svt(sl, tau)
     back = slices_to_fibres(sl, hat.shape[0], group)
     return engine.inverse(back, not x_rows.is_complex())
 
@@ -355,13 +391,23 @@ def dist_pga_complete(m_rows: torch.Tensor, mask_rows: torch.Tensor, cfg: Comple
     x_prev = torch.zeros_like(m_rows)
     x_cur = torch.zeros_like(m_rows)
     trace = CompletionTrace()
+    carry = {}  # right singular bases of this rank's slices, carried between iterations
+    on_device = hasattr(engine, "norms_device")
     for k in range(1, cfg.max_iters + 1):
         y, g = engine.gradient(x_cur, x_prev, pobs, mask_u8, betas[k - 1])
-        x_next = dist_svt(g, mus[k - 1], I1, engine, group)
-        loc = engine.norms(y, x_next, ground_truth_rows)
-        sums = allsum([float(loc[0]), float(loc[1]), float(loc[2])])
-        peak = torch.tensor([float(loc[3])], dtype=torch.float64, device=m_rows.device)
-        dist.all_reduce(peak, op=dist.ReduceOp.MAX, group=group)
+        x_next = dist_svt(g, mus[k - 1], I1, engine, group, carry=carry)
+        if on_device:  # reduce on the device; one host synchronisation per iteration
+            loc = engine.norms_device(y, x_next, ground_truth_rows)
+            sums, peak = loc[:3].clone(), loc[3:].clone()
+            dist.all_reduce(sums, group=group)
+            dist.all_reduce(peak, op=dist.ReduceOp.MAX, group=group)
+            both = torch.cat([sums, peak]).tolist()
+            sums, peak = both[:3], both[3:]
+        else:
+            loc = engine.norms(y, x_next, ground_truth_rows)
+            sums = allsum([float(loc[0]), float(loc[1]), float(loc[2])])
+            peak = torch.tensor([float(loc[3])], dtype=torch.float64, device=m_rows.device)
+            dist.all_reduce(peak, op=dist.ReduceOp.MAX, group=group)
         rel = rel_change(float(sums[0]), float(sums[1]), pobs_zero)
         rec = IterationRecord(k=k, mu=mus[k - 1], t=ts[k - 1], rel_change=rel)
         if ground_truth_rows is not None:

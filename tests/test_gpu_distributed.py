@@ -79,3 +79,23 @@ def test_dist_pga_device(nccl_world1, golden):
     ref, rtrace = L.pga_complete(m, mask, cfg)
     assert trace.iterations == rtrace.iterations
     assert rel_err(x.cpu().numpy(), ref) < 1e-10
+
+
+def test_dist_pga_fp32_carried_device(nccl_world1):
+    """fp32 slices of width >= 32 take the warm-started SVT (ltb_slice_svt_carry) and the
+    device-side norms; the iterate must match the single-device fp32 solver within the fp32
+    tolerance after enough iterations for every slice to be solved."""
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((48, 4, 3, 5))
+    b = rng.standard_normal((4, 40, 3, 5))
+    spec = L.make_spec("dct", (48, 40, 3, 5))
+    x0 = L.l_product(a, b, spec)
+    m = x0.astype(np.float32)
+    mask = rng.random(m.shape) < 0.5
+    cfg = L.CompletionConfig(spec=spec, max_iters=60, tol=1e-300)
+    mu0 = cfg.nu * float(np.linalg.norm(m.astype(np.float64)))
+    x, trace = dist_pga_complete(torch.from_numpy(m).cuda(), torch.from_numpy(mask).cuda(), cfg, m.shape[0],
+                                 DeviceEngine(spec, m.shape[2:]), mu0=mu0)
+    ref, rtrace = L.pga_complete(m.astype(np.float64), mask, cfg)
+    assert trace.iterations == rtrace.iterations == 60
+    assert rel_err(x.cpu().numpy(), ref) < 1e-4
