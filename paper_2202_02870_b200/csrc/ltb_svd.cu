@@ -76,6 +76,7 @@ struct JacobiOut {
   double tau;
   const int* skip;   // device flag: nonzero -> return immediately
   unsigned long long* stats;  // optional: [0] += slices, [1] += sweeps
+  float tol_scale = 1.f;      // QR/Cholesky-preconditioned fp32 path: rotation threshold multiplier
 };
 
 template <typename T, bool WANT_V, bool GLOBAL, int TS, int MPL, int MINB>
@@ -1156,7 +1157,7 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   }
 
   // ---- one-sided Jacobi on the n columns of X (n rows), as jacobi_kernel's fp32 path
-  const float tol = FLT_EPSILON * sqrtf((float)max(n, 1));
+  const float tol = FLT_EPSILON * sqrtf((float)max(n, 1)) * o.tol_scale;
   const int npl = n + (n & 1);
   const int npairs = npl / 2;
   constexpr int TPW = 32 / TS;
@@ -1321,6 +1322,9 @@ int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const
 // 1 when the QR-preconditioned resident kernel takes this fp32 SVT; 0 to use the others
 int g_svt_qr = 1;
 int g_qr_max_sweeps = 40;  // timing hook: 0 measures the QR and emission stages alone
+// lanes per column pair in the fp32 QR/Cholesky Jacobi: 8 (one pair per team per round,
+// fewer padding rows; 10-30% faster for 64 <= n <= 192, tools/qr_ts_ab.py) or 16
+int g_qr_ts = 8;
 
 // LTB_EUNSUPPORTED when the shape does not fit the QR-preconditioned kernel
 // chol: A holds n x n Gram matrices (I1 == I2 == n), factored by Cholesky instead of Householder
@@ -1329,7 +1333,10 @@ int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const 
   const int m = (int)std::max(I1, I2), n = (int)std::min(I1, I2);
   if (!g_svt_qr || g_force_blocked || n < 32 || batch > 0x7fffffff) return LTB_EUNSUPPORTED;
   int TSv = 16, MPLv = 0;
-  if (n <= 64) MPLv = 4;
+  if (g_qr_ts == 8 && n > 48 && n <= 192) {  // 8-lane teams: one pair per team per round
+    TSv = 8;
+    MPLv = n <= 64 ? 8 : n <= 128 ? 16 : n <= 144 ? 18 : n <= 160 ? 20 : 24;
+  } else if (n <= 64) MPLv = 4;
   else if (n <= 128) MPLv = 8;
   else if (n <= 160) MPLv = 10;
   else if (n <= 192) MPLv = 12;
@@ -1337,6 +1344,9 @@ int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const 
   else return LTB_EUNSUPPORTED;
   int pitch = std::max(m, TSv * MPLv);
   pitch += pitch & 1;
+  // an 8-lane team reads 64 bytes of its column: with pitch = 16 (mod 32) floats the four
+  // teams of a warp (consecutive columns) alternate bank halves instead of colliding
+  if (TSv == 8) pitch += (16 - pitch % 32 + 32) % 32;
   const size_t smem = jacobi_qr_smem(n, pitch);
   if (smem > kSmemLimit) return LTB_EUNSUPPORTED;
   const bool two = 2 * (smem + 1024) <= 228 * 1024;
@@ -1348,6 +1358,15 @@ int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const 
   return two ? launch_qr_variant<TS_, MPL_, 2, false>(ctx, batch, I1, I2, A, o, ms, n, pitch)           \
              : launch_qr_variant<TS_, MPL_, 1, false>(ctx, batch, I1, I2, A, o, ms, n, pitch)
   if (TSv == 32) { LTB_QR(32, 8); }
+  if (TSv == 8) {
+    switch (MPLv) {
+      case 8: LTB_QR(8, 8);
+      case 16: LTB_QR(8, 16);
+      case 18: LTB_QR(8, 18);
+      case 20: LTB_QR(8, 20);
+      default: LTB_QR(8, 24);
+    }
+  }
   switch (MPLv) {
     case 4: LTB_QR(16, 4);
     case 8: LTB_QR(16, 8);
@@ -1394,6 +1413,9 @@ __global__ void col_scale_kernel(int64_t batch, int n, const float* __restrict__
 // LTB_EUNSUPPORTED when the slice shape does not fit the QR-preconditioned kernel.
 int g_carry_chol = 1;  // warm carried SVT: Cholesky of the Gram matrix (1) or Householder (0)
 extern "C" void ltb_debug_set_carry_chol(int v) { g_carry_chol = v; }
+// carried SVT: multiplier of the Jacobi rotation threshold eps * sqrt(n)
+float g_carry_tol_scale = 1.f;
+extern "C" void ltb_debug_set_carry_tol_scale(float v) { g_carry_tol_scale = v; }
 
 int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
                        float* V, int warm, const int* skip) {
@@ -1428,6 +1450,7 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
   }
   JacobiOut o{nullptr, sv, Y, kept, dd, tau, skip};
   o.stats = ctx->d_stats;
+  o.tol_scale = g_carry_tol_scale;
   int st;
   if (warm && g_carry_chol) {
     // A0's columns are nearly orthogonal: factor its Gram matrix (tensor-core GEMM) by
@@ -1486,6 +1509,7 @@ namespace {
 extern "C" void ltb_debug_set_svd_blocked(int v) { g_force_blocked = v; }
 extern "C" void ltb_debug_set_svt_qr(int v) { g_svt_qr = v; }
 extern "C" void ltb_debug_set_qr_max_sweeps(int v) { g_qr_max_sweeps = v; }
+extern "C" void ltb_debug_set_qr_ts(int v) { g_qr_ts = v; }
 extern "C" void ltb_debug_set_qr_timeline(void* p) { g_qr_dbg = (unsigned long long*)p; }
 
 // SVT of `batch` row-major I1 x I2 slices: out = U (S - tau)_+ V^H
