@@ -86,26 +86,72 @@ template <> __device__ __forceinline__ float gradient_point<float>(float y, floa
   return __fsub_rn(y, __fsub_rn(observed ? y : 0.f, pobs));
 }
 
+// the PGA prologue: x_cur, x_prev, p_obs and the tile's packed mask words are staged by
+// cp.async (all of a thread's copies in flight at once; x_cur in S0, x_prev in S1,
+// p_obs in the extra tile, R views of S1 / extra when the tile is complex), then
+// finish() forms the gradient point in place
 template <typename R>
 struct LoadPGA {
+  static constexpr int kExtraBufs = 1;
+  static constexpr bool kMaskWords = true;
   const R* xc;
   const R* xp;
   const R* pobs;
   const uint32_t* mask;
   R beta;
   template <typename Tc>
-  __device__ __forceinline__ void load(const XformParams& p, Tc* S, int64_t tube0, int nt, int tid) const {
+  __device__ __forceinline__ void stage(const XformParams& p, Tc* S0, Tc* S1, unsigned char* extra, R*& sx, R*& sp,
+                                        R*& so, uint32_t*& sm) const {
+    const size_t tile = (size_t)p.P * p.pitch;
+    if constexpr (std::is_same<Tc, R>::value) {
+      sx = S0;
+      sp = S1;
+    } else {
+      sx = reinterpret_cast<R*>(S1);
+      sp = sx + tile;
+    }
+    so = reinterpret_cast<R*>(extra);
+    sm = reinterpret_cast<uint32_t*>(extra + tile * sizeof(Tc));
+  }
+  template <typename Tc>
+  __device__ __forceinline__ void load(const XformParams& p, Tc* S0, Tc* S1, unsigned char* extra, int64_t tube0,
+                                       int nt, int tid) const {
     const int P = p.P, pitch = p.pitch;
     const int64_t e0 = tube0 * P;
     const int cnt = nt * P;
+    R *sx, *sp, *so;
+    uint32_t* sm;
+    stage(p, S0, S1, extra, sx, sp, so, sm);
     for (int l = tid; l < cnt; l += kXformThreads) {
-      const int64_t e = e0 + l;
-      const R y = momentum<R>(xc[e], xp[e], beta);
-      const bool obs = (mask[e >> 5] >> (e & 31)) & 1u;
-      const R g = gradient_point<R>(y, pobs[e], obs);
       int t, q;
       split_tube(l, P, p.invP, t, q);
-      S[q * pitch + t] = cvt<Tc>(g);
+      const int i = q * pitch + t;
+      cp_async<sizeof(R)>(sx + i, xc + e0 + l);
+      cp_async<sizeof(R)>(sp + i, xp + e0 + l);
+      cp_async<sizeof(R)>(so + i, pobs + e0 + l);
+    }
+    const int64_t w0 = e0 >> 5;
+    const int nw = (int)(((e0 + cnt - 1) >> 5) - w0 + 1);
+    for (int w = tid; w < nw; w += kXformThreads) cp_async<4>(sm + w, mask + w0 + w);
+  }
+  template <typename Tc>
+  __device__ __forceinline__ void finish(const XformParams& p, Tc* S0, Tc* S1, unsigned char* extra, int64_t tube0,
+                                         int nt, int tid) const {
+    const int P = p.P, pitch = p.pitch;
+    const int64_t e0 = tube0 * P;
+    const int cnt = nt * P;
+    const int b0 = (int)(e0 & 31);  // bit of element e0 in the first staged word
+    R *sx, *sp, *so;
+    uint32_t* sm;
+    stage(p, S0, S1, extra, sx, sp, so, sm);
+    for (int l = tid; l < cnt; l += kXformThreads) {
+      int t, q;
+      split_tube(l, P, p.invP, t, q);
+      const int i = q * pitch + t;
+      const R y = momentum<R>(sx[i], sp[i], beta);
+      const int bit = b0 + l;
+      const bool obs = (sm[bit >> 5] >> (bit & 31)) & 1u;
+      S0[i] = cvt<Tc>(gradient_point<R>(y, so[i], obs));
     }
   }
 };
@@ -126,23 +172,39 @@ struct StorePGA {
     const int P = p.P, pitch = p.pitch;
     const int64_t e0 = tube0 * P;
     const int cnt = nt * P;
-    for (int l = tid; l < cnt; l += kXformThreads) {
-      int t, q;
-      split_tube(l, P, p.invP, t, q);
-      const Tc v = S[q * pitch + t];
-      const int64_t e = e0 + l;
-      const R x1 = re_v(v);
-      const R y = momentum<R>(xc[e], xp[e], beta);
-      const double d = (double)y - (double)x1;
-      acc[0] += d * d;
-      acc[1] += (double)x1 * (double)x1;
-      if (gt) {
-        const double dg = (double)x1 - (double)gt[e];
-        acc[2] += dg * dg;
+    constexpr int U = 8;  // U elements' global loads issued before any is used
+    for (int l0 = tid; l0 < cnt; l0 += U * kXformThreads) {
+      R c[U], pv[U], g[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int l = l0 + u * kXformThreads;
+        if (l < cnt) {
+          c[u] = xc[e0 + l];
+          pv[u] = xp[e0 + l];
+          g[u] = gt ? gt[e0 + l] : R(0);
+        }
       }
-      acc[3] = fmax(acc[3], (double)x1);
-      acc[4] += (double)im_v(v) * (double)im_v(v);
-      xn[e] = x1;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int l = l0 + u * kXformThreads;
+        if (l < cnt) {
+          int t, q;
+          split_tube(l, P, p.invP, t, q);
+          const Tc v = S[q * pitch + t];
+          const R x1 = re_v(v);
+          const R y = momentum<R>(c[u], pv[u], beta);
+          const double d = (double)y - (double)x1;
+          acc[0] += d * d;
+          acc[1] += (double)x1 * (double)x1;
+          if (gt) {
+            const double dg = (double)x1 - (double)g[u];
+            acc[2] += dg * dg;
+          }
+          acc[3] = fmax(acc[3], (double)x1);
+          acc[4] += (double)im_v(v) * (double)im_v(v);
+          xn[e0 + l] = x1;
+        }
+      }
     }
   }
 };
@@ -271,7 +333,8 @@ int pga_plan(const ltb_spec* spec, int64_t NT, int inverse, XformParams& p, size
   p = XformParams{};
   p.NT = NT;
   build_steps(spec, inverse, p);
-  return plan_tile<Tc, Tm>(p, smem);
+  // the forward's LoadPGA stages p_obs in one extra tile plus the packed mask words
+  return inverse ? plan_tile<Tc, Tm>(p, smem) : plan_tile<Tc, Tm>(p, smem, LoadPGA<float>::kExtraBufs, true);
 }
 
 // the SVT step of one iteration (hat_a -> hat_b): carried bases for fp32 real transform

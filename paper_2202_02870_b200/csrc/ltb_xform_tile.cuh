@@ -90,17 +90,54 @@ __device__ __forceinline__ void split_tube(int l, int P, float invP, int& t, int
   }
 }
 
+// ---------------------------------------------------------------- async copies
+// LDGSTS: global -> shared without a register round trip, so every thread keeps all of
+// its tile loads in flight at once (a plain load + st.shared loop holds one per thread,
+// which left the tile engine at a few hundred GB/s); completion via cp.async.wait_all
+template <int B>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gmem), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---------------------------------------------------------------- loaders
+// load(p, S0, S1, extra, tube0, nt, tid): fill S0 (q-major, pitch) with the tile's tube
+// values; S1 (same size) and `extra` (extra_bytes) are free scratch until the first mode
+// step.  Outstanding cp.async copies are waited for by the kernel before its barrier.
 template <typename Tin>
 struct LoadPlain {
+  static constexpr int kExtraBufs = 0;  // additional tile-sized buffers in shared memory
+  static constexpr bool kMaskWords = false;
   const Tin* in;
   int layout;
   template <typename Tc>
-  __device__ __forceinline__ void load(const XformParams& p, Tc* S, int64_t tube0, int nt, int tid) const {
+  __device__ __forceinline__ void load(const XformParams& p, Tc* S, Tc* /*S1*/, unsigned char* /*extra*/,
+                                       int64_t tube0, int nt, int tid) const {
     const int P = p.P, TT = p.TT, pitch = p.pitch;
+    if constexpr (std::is_same<Tin, Tc>::value) {
+      if (layout == LTB_TUBE_MAJOR) {
+        const Tin* src = in + tube0 * P;
+        const int cnt = nt * P;
+        for (int l = tid; l < cnt; l += kXformThreads) {
+          int t, q;
+          split_tube(l, P, p.invP, t, q);
+          cp_async<sizeof(Tc)>(S + q * pitch + t, src + l);
+        }
+      } else {
+        const int cnt = P * TT;
+        for (int l = tid; l < cnt; l += kXformThreads) {
+          const int q = l >> p.ttshift;
+          const int t = l & (TT - 1);
+          if (t < nt) cp_async<sizeof(Tc)>(S + q * pitch + t, in + (int64_t)q * p.NT + tube0 + t);
+        }
+      }
+      return;
+    }
     if (layout == LTB_TUBE_MAJOR) {
       const Tin* src = in + tube0 * P;
       const int cnt = nt * P;
+#pragma unroll 4
       for (int l = tid; l < cnt; l += kXformThreads) {
         int t, q;
         split_tube(l, P, p.invP, t, q);
@@ -108,6 +145,7 @@ struct LoadPlain {
       }
     } else {
       const int cnt = P * TT;
+#pragma unroll 4
       for (int l = tid; l < cnt; l += kXformThreads) {
         const int q = l >> p.ttshift;
         const int t = l & (TT - 1);
@@ -115,6 +153,8 @@ struct LoadPlain {
       }
     }
   }
+  template <typename Tc>
+  __device__ __forceinline__ void finish(const XformParams&, Tc*, Tc*, unsigned char*, int64_t, int, int) const {}
 };
 
 // ---------------------------------------------------------------- storers
@@ -132,6 +172,7 @@ struct StorePlain {
     if (layout == LTB_TUBE_MAJOR) {
       Tout* o = out + tube0 * P;
       const int cnt = nt * P;
+#pragma unroll 4
       for (int l = tid; l < cnt; l += kXformThreads) {
         int t, q;
         split_tube(l, P, p.invP, t, q);
@@ -160,8 +201,10 @@ struct StorePlain {
   }
 };
 
-// RB consecutive matrix entries, one or two vector loads
-template <typename Tm, int RB> struct alignas(sizeof(Tm) * RB >= 16 ? 16 : sizeof(Tm) * RB) mrow {
+// RB consecutive matrix entries in vector loads (alignment: the largest power of two
+// dividing the row, at most 16 bytes, so row i0 = iblk * RB stays aligned for any RB)
+constexpr int mrow_align(int bytes) { return bytes % 16 == 0 ? 16 : bytes % 8 == 0 ? 8 : bytes % 4 == 0 ? 4 : 2; }
+template <typename Tm, int RB> struct alignas(mrow_align(sizeof(Tm) * RB)) mrow {
   Tm v[RB];
 };
 
@@ -247,6 +290,7 @@ __device__ __forceinline__ void mode_step_f2(const XformParams& p, const ModeSte
     const float* col = src + base * pitch + t;
     const int jstride = lo * pitch;
     const float* mrowp = Msm + i0;
+#pragma unroll 4
     for (int j = 0; j < n; ++j) {
       const float2 v = make_float2(col[j * jstride], col[j * jstride + half]);
       const mrow<float, RBM> mv = *reinterpret_cast<const mrow<float, RBM>*>(mrowp + j * npad);
@@ -275,9 +319,9 @@ __global__ void __launch_bounds__(kXformThreads)
   const int mat_bytes = p.mats_in_smem ? (p.mat_smem_elems * (int)sizeof(Tm) + 127) / 128 * 128 : 0;
   Tc* S0 = reinterpret_cast<Tc*>(smem_raw + mat_bytes);
   Tc* S1 = S0 + (size_t)p.P * p.pitch;
+  unsigned char* extra = reinterpret_cast<unsigned char*>(S1 + (size_t)p.P * p.pitch);
   const int tid = threadIdx.x;
   const int TT = p.TT;
-  const int pitch = p.pitch;
 
   // stage the transposed, zero-padded mode matrices once per (persistent) CTA:
   // Ms[off + j * npad + i] = M[i][j]
@@ -300,8 +344,13 @@ __global__ void __launch_bounds__(kXformThreads)
   const int64_t tube0 = tile * TT;
   const int nt = (int)min((int64_t)TT, p.NT - tube0);
   __syncthreads();  // previous tile's store has drained S0/S1
-  ld.load(p, S0, tube0, nt, tid);
+  ld.load(p, S0, S1, extra, tube0, nt, tid);
+  cp_async_wait_all();
   __syncthreads();
+  if constexpr (Loader::kExtraBufs > 0 || Loader::kMaskWords) {
+    ld.finish(p, S0, S1, extra, tube0, nt, tid);
+    __syncthreads();
+  }
 
   Tc* src = S0;
   Tc* dst = S1;
@@ -312,11 +361,15 @@ __global__ void __launch_bounds__(kXformThreads)
     bool done = false;
     if constexpr (std::is_same<Tc, float>::value && std::is_same<Tm, float>::value) {
       if (p.mats_in_smem && TT >= 2) {
-        switch (ms.rb) {
+        switch (ms.rb) {  // kF2Blocks
           case 1: mode_step_f2<1>(p, ms, src, dst, Msm, tid); break;
           case 2: mode_step_f2<2>(p, ms, src, dst, Msm, tid); break;
           case 4: mode_step_f2<4>(p, ms, src, dst, Msm, tid); break;
-          default: mode_step_f2<RB>(p, ms, src, dst, Msm, tid); break;
+          case 6: mode_step_f2<6>(p, ms, src, dst, Msm, tid); break;
+          case 10: mode_step_f2<10>(p, ms, src, dst, Msm, tid); break;
+          case 12: mode_step_f2<12>(p, ms, src, dst, Msm, tid); break;
+          case 16: mode_step_f2<16>(p, ms, src, dst, Msm, tid); break;
+          default: mode_step_f2<8>(p, ms, src, dst, Msm, tid); break;
         }
         done = true;
       }
@@ -364,16 +417,52 @@ __global__ void __launch_bounds__(kXformThreads)
 // Pick tubes-per-tile (power of two) and the matrix staging; returns 0 when
 // the tile does not fit in shared memory.  Fills p.TT / ttshift / pitch /
 // mats_in_smem and the total dynamic shared memory.
+// fp32 FFMA2 mode steps: the register block (matrix rows per work item) of each mode is
+// picked from kF2Blocks so that the step's work items (rows / rb x fibres x tube pairs)
+// fill whole rounds of the CTA's threads; e.g. n = 100 under a 3 x 100 spec with 16-tube
+// tiles: rb = 8 gives 312 items (two rounds, the second 22% busy), rb = 10 gives 240 (one)
+constexpr int kF2Blocks[] = {1, 2, 4, 6, 8, 10, 12, 16};
+
+inline void plan_matrices_f2(XformParams& p) {
+  const int half = p.TT >> 1;
+  int off = 0;
+  for (int s = 0; s < p.nsteps; ++s) {
+    ModeStep& ms = p.step[s];
+    int64_t best = -1;
+    for (int rb : kF2Blocks) {
+      const int64_t nblk = (ms.n + rb - 1) / rb;
+      const int64_t items = ms.hi * ms.lo * nblk * half;
+      const int64_t cost = (items + kXformThreads - 1) / kXformThreads * (rb + 3);  // rb FFMA2 + loads per j
+      if (best < 0 || cost < best) {
+        best = cost;
+        ms.rb = rb;
+      }
+    }
+    ms.npad = (ms.n + ms.rb - 1) / ms.rb * ms.rb;
+    ms.inv_nblk = 1.0f / (float)(ms.npad / ms.rb);
+    ms.inv_lo = 1.0f / (float)ms.lo;
+    off = (off + 3) / 4 * 4;  // 16-byte aligned matrix starts
+    ms.smem_off = off;
+    off += ms.n * ms.npad;
+  }
+  p.mat_smem_elems = off;
+}
+
+// extra_bufs: loader scratch tiles beyond S0 / S1; mask_words: room for the tile's
+// packed observation-mask words (PGA prologue)
 template <typename Tc, typename Tm>
-inline int plan_tile(XformParams& p, size_t* smem_out) {
+inline int plan_tile(XformParams& p, size_t* smem_out, int extra_bufs = 0, bool mask_words = false) {
   plan_matrices<Tc>(p);
   const size_t mat_bytes = ((size_t)p.mat_smem_elems * sizeof(Tm) + 127) / 128 * 128;
   p.mats_in_smem = mat_bytes <= 48 * 1024 ? 1 : 0;
   const size_t mb = p.mats_in_smem ? mat_bytes : 0;
-  auto smem_for = [&](int tt) { return mb + (size_t)2 * p.P * (tt + 1) * sizeof(Tc); };
+  auto smem_for = [&](int tt) {
+    return mb + (size_t)(2 + extra_bufs) * p.P * (tt + 1) * sizeof(Tc) +
+           (mask_words ? ((size_t)tt * p.P / 32 + 2) * 4 : 0);
+  };
   int TT = 0;
-  for (int tt = 32; tt >= 8 && !TT; tt >>= 1)
-    if (smem_for(tt) <= 100 * 1024) TT = tt;
+  for (int tt = 32; tt >= 8 && !TT; tt >>= 1)  // two CTAs per SM
+    if (smem_for(tt) <= 112 * 1024) TT = tt;
   for (int tt = 32; tt >= 1 && !TT; tt >>= 1)
     if (smem_for(tt) <= 200 * 1024) TT = tt;
   if (!TT) return 0;
@@ -382,6 +471,16 @@ inline int plan_tile(XformParams& p, size_t* smem_out) {
   while ((1 << p.ttshift) < TT) ++p.ttshift;
   p.pitch = TT + 1;
   *smem_out = smem_for(TT);
+  if constexpr (std::is_same<Tc, float>::value && std::is_same<Tm, float>::value) {
+    if (p.mats_in_smem && TT >= 2) {  // the FFMA2 steps: rebalance the register blocks
+      const XformParams keep = p;
+      plan_matrices_f2(p);
+      const size_t mb2 = ((size_t)p.mat_smem_elems * sizeof(Tm) + 127) / 128 * 128;
+      const size_t total = *smem_out - mb + mb2;
+      if (mb2 <= 48 * 1024 && (total <= *smem_out || total <= 112 * 1024)) *smem_out = total;
+      else p = keep;
+    }
+  }
   return TT;
 }
 
