@@ -77,6 +77,9 @@ struct JacobiOut {
   const int* skip;   // device flag: nonzero -> return immediately
   unsigned long long* stats;  // optional: [0] += slices, [1] += sweeps
   float tol_scale = 1.f;      // QR/Cholesky-preconditioned fp32 path: rotation threshold multiplier
+  // QR/Cholesky path: stop after a sweep whose rotations all had |<w_p, w_q>| / (|w_p| |w_q|)
+  // below this (0: stop only after a sweep without rotations)
+  float early_stop = 0.f;
 };
 
 template <typename T, bool WANT_V, bool GLOBAL, int TS, int MPL, int MINB>
@@ -1171,6 +1174,8 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   const int stride = nwarps * TPW;
   const int nslot = (npairs + stride - 1) / stride;  // <= 4 for every launched shape
   const float* const Wc = W + 2 * tl;
+  int* smax = flags + 4;  // per-sweep-parity largest relative rotated |gamma| (float bits; rank_sh later)
+  if (tid == 0) smax[0] = smax[1] = 0;
   for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
     int* rot = &flags[sweep & 1];
     for (int j = warp; j < n; j += nwarps) {
@@ -1213,7 +1218,8 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
         const float al = active ? nrm[p] : 0.f;
         const float be = active ? nrm[q] : 0.f;
         const float gabs = fabsf(g);
-        if (!active || !(gabs > tol * sqrt_apx(al) * sqrt_apx(be)) || !(fminf(fminf(al, be), gabs) >= FLT_MIN)) continue;
+        const float sab = sqrt_apx(al) * sqrt_apx(be);
+        if (!active || !(gabs > tol * sab) || !(fminf(fminf(al, be), gabs) >= FLT_MIN)) continue;
         const float zeta = (be - al) * (0.5f * rcp_apx(gabs));
         const float az = fabsf(zeta);
         const float den = az < 1e18f ? az + sqrt_apx(fmaf(az, az, 1.f)) : 2.f * az;
@@ -1234,16 +1240,23 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
           nrm[p] = fmaxf(al - tt * gabs, 0.f);
           nrm[q] = be + tt * gabs;
           *rot = 1;
+          atomicMax(&smax[sweep & 1], __float_as_int(gabs * rcp_apx(sab)));
         }
       }
       __syncthreads();
     }
     const int any = *rot;
+    const float worst = __int_as_float(smax[sweep & 1]);
     __syncthreads();
-    if (tid == 0) flags[(sweep + 1) & 1] = 0;
+    if (tid == 0) flags[(sweep + 1) & 1] = smax[(sweep + 1) & 1] = 0;
     __syncthreads();
     sweeps_done = sweep + 1;
-    if (!any) break;
+    // without rotations the sweep changed nothing; when every rotation of the sweep had a
+    // relative inner product below early_stop, the inner products the later rotations
+    // disturbed are of order early_stop^2 between columns of distinct norms (quadratic
+    // convergence); between columns of nearly equal norms a rotation can be wide, but
+    // there the singular values, and so the SVT's shrink factors, nearly coincide
+    if (!any || worst < o.early_stop) break;
   }
   stamp(5);
   if (o.stats && tid == 0) {
@@ -1416,6 +1429,13 @@ extern "C" void ltb_debug_set_carry_chol(int v) { g_carry_chol = v; }
 // carried SVT: multiplier of the Jacobi rotation threshold eps * sqrt(n)
 float g_carry_tol_scale = 1.f;
 extern "C" void ltb_debug_set_carry_tol_scale(float v) { g_carry_tol_scale = v; }
+// warm carried SVT: stop the Jacobi after a sweep whose rotated pairs all had a relative
+// inner product below g_carry_early * sqrt(tol) (tol = the rotation threshold), i.e. the
+// inner products left behind are ~tol; 0 runs to a sweep without rotations.  Config-3 PGA
+// (tools/pga_early_ab.py): 2.77 -> 1.98 sweeps per slice, +13% it/s, the 200-iteration
+// iterate's error against the fp64 run unchanged (3.2e-5)
+float g_carry_early = 1.f;
+extern "C" void ltb_debug_set_carry_early(float v) { g_carry_early = v; }
 
 int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
                        float* V, int warm, const int* skip) {
@@ -1451,6 +1471,7 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
   JacobiOut o{nullptr, sv, Y, kept, dd, tau, skip};
   o.stats = ctx->d_stats;
   o.tol_scale = g_carry_tol_scale;
+  if (warm) o.early_stop = g_carry_early * sqrtf(FLT_EPSILON * sqrtf((float)n) * g_carry_tol_scale);
   int st;
   if (warm && g_carry_chol) {
     // A0's columns are nearly orthogonal: factor its Gram matrix (tensor-core GEMM) by

@@ -67,6 +67,20 @@ def test_config3_pga_full_size_first_iterations(precision, tol):
                                rtol=1e-3 if precision == "fp32" else 1e-8)
 
 
+def test_config3_pga_full_run_fp32_vs_fp64():
+    """The whole config-3 run (200 iterations) in fp32 -- carried right bases, Cholesky warm
+    path, early-stopped Jacobi sweeps -- against the same run in fp64 (itself pinned to the
+    oracle at 1e-10 on the first iterations above and on config 1 / the golden traces)."""
+    m, mask = cfg3_data()
+    spec = L.make_spec("dct", m.shape)
+    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=200)
+    x32, t32 = L.pga_complete(m, mask, cfg, precision="fp32")
+    x64, t64 = L.pga_complete(m, mask, cfg, precision="fp64")
+    assert t32.iterations == t64.iterations == 200
+    assert rel_err(x32, x64) < 1e-4
+    assert [r.mu for r in t32.records] == [r.mu for r in t64.records]
+
+
 def test_config1_pga_full():
     rng = np.random.default_rng(0)
     a = rng.standard_normal((64, 5, 16))
