@@ -447,9 +447,13 @@ __global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
   }
   __syncthreads();
   const int g0 = good_count;
+  for (int j = tid; j < g0; j += nth) rn[j] = (R)1 / sb[j];
+  __syncthreads();
+  // row-major output, the column index fastest: coalesced stores; the column-major reads
+  // revisit each 32-byte sector for 8 consecutive rows and stay in L1
   for (int l = tid; l < m * g0; l += nth) {
-    const int j = l / m, i = l - j * m;
-    Ub[(int64_t)i * m + j] = Wb[(int64_t)j * m + i] * ((R)1 / sb[j]);
+    const int i = l / g0, j = l - i * g0;
+    Ub[(int64_t)i * m + j] = Wb[(int64_t)j * m + i] * rn[j];
   }
   __syncthreads();
   if (g0 >= m) return;  // every column normalised: nothing to complete
@@ -1501,7 +1505,10 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
                           nullptr, nullptr, nullptr, skip));
     Vc = Vn;
   }
-  // Newton-Schulz: V = Vc (3I - Vc^T Vc) / 2
+  // Newton-Schulz: V = Vc (3I - Vc^T Vc) / 2, every call: without it the basis drifts from
+  // orthonormality by about one fp32 rounding per call, and the 200-iteration config-3
+  // iterate leaves the fp32 tolerance (measured error vs fp64: 3.2e-5 every call, 5.0e-5
+  // every 2nd, 2.1e-4 every 4th)
   LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_T, Vc, n, nn, LTB_OP_N, Vc, n, nn, S, n, nn, nullptr, nullptr,
                         nullptr, nullptr, nullptr, skip));
   const unsigned grid = grid_for(batch * nn, 256, ctx->num_sms * 8);

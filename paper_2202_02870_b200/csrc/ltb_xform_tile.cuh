@@ -90,6 +90,30 @@ __device__ __forceinline__ void split_tube(int l, int P, float invP, int& t, int
   }
 }
 
+// Walks the tube-major element indices l = l0, l0 + stride, ... of a tile, tracking
+// q = l mod P and the q-major shared-memory index i = q * pitch + l / P incrementally
+// (one division per walk instead of a split per element)
+struct TubeWalk {
+  int q, i, dq, di, wrap, P;
+  __device__ __forceinline__ TubeWalk(int l0, int stride, const XformParams& p) : P(p.P) {
+    int t;
+    split_tube(l0, p.P, p.invP, t, q);
+    i = q * p.pitch + t;
+    const int dt = stride / p.P;
+    dq = stride - dt * p.P;
+    di = dq * p.pitch + dt;
+    wrap = 1 - p.P * p.pitch;
+  }
+  __device__ __forceinline__ void next() {
+    q += dq;
+    i += di;
+    if (q >= P) {
+      q -= P;
+      i += wrap;
+    }
+  }
+};
+
 // ---------------------------------------------------------------- async copies
 // LDGSTS: global -> shared without a register round trip, so every thread keeps all of
 // its tile loads in flight at once (a plain load + st.shared loop holds one per thread,
@@ -119,11 +143,8 @@ struct LoadPlain {
       if (layout == LTB_TUBE_MAJOR) {
         const Tin* src = in + tube0 * P;
         const int cnt = nt * P;
-        for (int l = tid; l < cnt; l += kXformThreads) {
-          int t, q;
-          split_tube(l, P, p.invP, t, q);
-          cp_async<sizeof(Tc)>(S + q * pitch + t, src + l);
-        }
+        TubeWalk w(tid, kXformThreads, p);
+        for (int l = tid; l < cnt; l += kXformThreads, w.next()) cp_async<sizeof(Tc)>(S + w.i, src + l);
       } else {
         const int cnt = P * TT;
         for (int l = tid; l < cnt; l += kXformThreads) {
@@ -137,12 +158,9 @@ struct LoadPlain {
     if (layout == LTB_TUBE_MAJOR) {
       const Tin* src = in + tube0 * P;
       const int cnt = nt * P;
+      TubeWalk w(tid, kXformThreads, p);
 #pragma unroll 4
-      for (int l = tid; l < cnt; l += kXformThreads) {
-        int t, q;
-        split_tube(l, P, p.invP, t, q);
-        S[q * pitch + t] = cvt<Tc>(src[l]);
-      }
+      for (int l = tid; l < cnt; l += kXformThreads, w.next()) S[w.i] = cvt<Tc>(src[l]);
     } else {
       const int cnt = P * TT;
 #pragma unroll 4
@@ -172,11 +190,10 @@ struct StorePlain {
     if (layout == LTB_TUBE_MAJOR) {
       Tout* o = out + tube0 * P;
       const int cnt = nt * P;
+      TubeWalk w(tid, kXformThreads, p);
 #pragma unroll 4
-      for (int l = tid; l < cnt; l += kXformThreads) {
-        int t, q;
-        split_tube(l, P, p.invP, t, q);
-        const Tc v = S[q * pitch + t];
+      for (int l = tid; l < cnt; l += kXformThreads, w.next()) {
+        const Tc v = S[w.i];
         if (RESIDUAL) {
           acc[0] += (double)abs2_v(v);
           acc[1] += (double)im_v(v) * (double)im_v(v);
@@ -291,9 +308,9 @@ __device__ __forceinline__ void mode_step_f2(const XformParams& p, const ModeSte
     const int jstride = lo * pitch;
     const float* mrowp = Msm + i0;
 #pragma unroll 4
-    for (int j = 0; j < n; ++j) {
-      const float2 v = make_float2(col[j * jstride], col[j * jstride + half]);
-      const mrow<float, RBM> mv = *reinterpret_cast<const mrow<float, RBM>*>(mrowp + j * npad);
+    for (int j = 0; j < n; ++j, col += jstride, mrowp += npad) {
+      const float2 v = make_float2(col[0], col[half]);
+      const mrow<float, RBM> mv = *reinterpret_cast<const mrow<float, RBM>*>(mrowp);
 #pragma unroll
       for (int rr = 0; rr < RBM; ++rr) acc[rr] = __ffma2_rn(make_float2(mv.v[rr], mv.v[rr]), v, acc[rr]);
     }
