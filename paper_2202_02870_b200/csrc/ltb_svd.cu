@@ -1001,7 +1001,9 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
 // columns are nearly orthogonal (the carried PGA bases); the triangular factor comes from
 // an in-place Cholesky, G = L L^T with L = R^T, accurate here because the diagonally
 // scaled Gram matrix is well conditioned, and much shorter than the Householder QR.
-template <int TS, int MPL, int MINB, bool CHOL = false>
+// SLOTS: most pairs per team per round (1 when the teams cover every pair: the slot
+// arrays then stay in registers instead of spilling to local memory)
+template <int TS, int MPL, int MINB, bool CHOL = false, int SLOTS = 4>
 __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     jacobi_qr_kernel(int64_t I1, int64_t I2, const float* __restrict__ A, JacobiOut o, int max_sweeps, int pitch,
                      unsigned long long* dbg) {
@@ -1190,16 +1192,16 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
       if (lane == 0) nrm[j] = s2;
     }
     __syncthreads();
-    int ps[4], qs[4];
+    int ps[SLOTS], qs[SLOTS];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < SLOTS; ++t) {
       const int k = warp * TPW + t * stride + team;
       ps[t] = (k == 0) ? m1 : k;
       qs[t] = (k == 0) ? 0 : m1 - k;
     }
     for (int r = 0; r < m1; ++r) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < SLOTS; ++t) {
         if (t >= nslot) break;
         const int k = warp * TPW + t * stride + team;
         const int p = ps[t], q = qs[t];
@@ -1328,8 +1330,9 @@ int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const
   const int teams = std::max(1, (pairs * TS + 31) / 32);
   const int per_warp = (teams + maxw - 1) / maxw;
   const int nwarps = std::max(1, (teams + per_warp - 1) / per_warp);
-  if ((pairs + nwarps * (32 / TS) - 1) / (nwarps * (32 / TS)) > 4) return LTB_EUNSUPPORTED;  // <= 4 slots per team
-  auto kern = jacobi_qr_kernel<TS, MPL, MINB, CHOL>;
+  const int slots = (pairs + nwarps * (32 / TS) - 1) / (nwarps * (32 / TS));
+  if (slots > 4) return LTB_EUNSUPPORTED;  // <= 4 slots per team
+  auto kern = slots == 1 ? jacobi_qr_kernel<TS, MPL, MINB, CHOL, 1> : jacobi_qr_kernel<TS, MPL, MINB, CHOL, 4>;
   LTB_TRY(ensure_smem(ctx, kern, smem, true));
   kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, o, max_sweeps, pitch, g_qr_dbg);
   LTB_LAUNCH_CHECK(ctx);
