@@ -1131,29 +1131,47 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   stamp(4);
   } else {
     // ---- Cholesky G = L L^T in place (column j of L in column j, rows >= j); a non-positive
-    // pivot (rank-deficient slice) zeroes its column.  The owner of column k+1 finishes it
-    // right after its trailing update, so each step costs one block barrier.
-    auto finish = [&](int j) {  // one warp: pivot and scaling of column j
-      float* wj = W + (size_t)j * pitch;
-      const float pj = wj[j];
-      const float d = pj >= FLT_MIN ? sqrtf(pj) : 0.f;
-      const float inv = d > 0.f ? 1.f / d : 0.f;
-      __syncwarp();
-      if (lane == 0) wj[j] = d;
-      for (int i = j + 1 + lane; i < n; i += 32) wj[i] *= inv;
-      __syncwarp();
-    };
-    if (warp == 0) finish(0);
-    __syncthreads();
-    for (int k = 0; k < n; ++k) {
-      const float* lk = W + (size_t)k * pitch;
-      for (int j = k + 1 + warp; j < n; j += nwarps) {
+    // pivot (rank-deficient slice) zeroes its column.  Blocked right-looking: warp 0 factors
+    // a panel of CB columns (warp-synchronous), then every warp applies the panel's rank-CB
+    // update to the trailing columns with the panel entries of its column in registers
+    // (CB + 2 shared-memory accesses per CB FMAs instead of 3 per FMA, two block barriers
+    // per panel instead of one per column).
+    constexpr int CB = 8;
+    for (int k0 = 0; k0 < n; k0 += CB) {
+      const int kend = min(k0 + CB, n);
+      if (warp == 0) {
+        for (int kk = k0; kk < kend; ++kk) {
+          float* wk = W + (size_t)kk * pitch;
+          const float pk = wk[kk];
+          const float d = pk >= FLT_MIN ? sqrtf(pk) : 0.f;
+          const float inv = d > 0.f ? 1.f / d : 0.f;
+          __syncwarp();
+          if (lane == 0) wk[kk] = d;
+          for (int i = kk + 1 + lane; i < n; i += 32) wk[i] *= inv;
+          __syncwarp();
+          for (int jj = kk + 1; jj < kend; ++jj) {  // the rest of the panel
+            float* wj = W + (size_t)jj * pitch;
+            const float ljk = wk[jj];
+            for (int i = jj + lane; i < n; i += 32) wj[i] = fmaf(-wk[i], ljk, wj[i]);
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      const int nk = kend - k0;
+      for (int j = kend + warp; j < n; j += nwarps) {
+        float lj[CB];
+#pragma unroll
+        for (int kk = 0; kk < CB; ++kk) lj[kk] = kk < nk ? W[(size_t)(k0 + kk) * pitch + j] : 0.f;
         float* wj = W + (size_t)j * pitch;
-        const float ljk = lk[j];
-        if (ljk != 0.f)
-          for (int i = j + lane; i < n; i += 32) wj[i] = fmaf(-lk[i], ljk, wj[i]);
-        __syncwarp();
-        if (j == k + 1) finish(j);
+        const float* lp = W + (size_t)k0 * pitch;
+        for (int i = j + lane; i < n; i += 32) {
+          float acc = wj[i];
+#pragma unroll
+          for (int kk = 0; kk < CB; ++kk)
+            if (kk < nk) acc = fmaf(-lp[(size_t)kk * pitch + i], lj[kk], acc);
+          wj[i] = acc;
+        }
       }
       __syncthreads();
     }
