@@ -14,9 +14,22 @@ ncu --set full --clock-control none --import-source on -k regex:tc3_kernel -c 3 
 python tools/prof_pga_late.py 120 2 > /dev/null 2>&1 && \
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:jacobi_qr_kernel -c 1 \
     -o gpurun_out/prof/${R}_jacobi_qr python tools/prof_pga_late.py 120 2 > /dev/null 2>&1
-ncu --profile-from-start off --set full --clock-control none -k regex:xform_tile_kernel -c 2 \
+ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:xform_tile_kernel -c 2 \
     -o gpurun_out/prof/${R}_xform_pga python tools/prof_pga_late.py 120 2 > /dev/null 2>&1
 python tools/svd_blocked_prof.py 1024 > /dev/null 2>&1 && \
 ncu --set full --clock-control none -k regex:jacobi_block_kernel -s 20 -c 1 -o gpurun_out/prof/${R}_jacobi_block \
     python tools/svd_blocked_prof.py 1024 > /dev/null 2>&1
+python tools/pga_kernel_breakdown.py 120 5 > gpurun_out/prof/${R}_pga_breakdown.txt 2>&1
 ls -la gpurun_out/prof
+# summaries on the box (the .ncu-rep files together exceed what gpurun copies back): markdown,
+# raw CSV per report, then drop the reports themselves
+P=gpurun_out/prof
+python tools/ncu_summary.py $P/${R}_ncu_summary.md \
+    $P/${R}_tc3.ncu-rep:"config-2 l_product tcgen05 kernels (paired forward K1, slice GEMM K2, inverse K1')" \
+    $P/${R}_jacobi_qr.ncu-rep:"config-3 PGA K3 (Cholesky-preconditioned Jacobi, warm iteration 121)" \
+    $P/${R}_xform_pga.ncu-rep:"config-3 PGA fused transforms (K1 + K4 prologue, K1' + norms epilogue)" \
+    $P/${R}_jacobi_block.ncu-rep:"config-4-size blocked Jacobi round (complex64 1024x1024)" \
+    --launches $P/${R}_launches.csv:"bench.py --steps 3 --warmup 3 --skip-extras --pga-iters 60"
+for f in $P/*.ncu-rep; do ncu -i $f --page raw --csv > ${f%.ncu-rep}_raw.csv 2>/dev/null; done
+rm -f $P/*.ncu-rep
+du -sh gpurun_out
