@@ -1229,14 +1229,14 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
         float* wp = const_cast<float*>(Wc) + (size_t)(active ? p : 0) * pitch;
         float* wq = const_cast<float*>(Wc) + (size_t)(active ? q : 0) * pitch;
         float2 X2[MPL / 2], Y2[MPL / 2];
-        float2 acc = make_float2(0.f, 0.f);
+        float2 acc[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
         for (int h = 0; h < MPL / 2; ++h) {
           X2[h] = *reinterpret_cast<const float2*>(wp + 2 * TS * h);
           Y2[h] = *reinterpret_cast<const float2*>(wq + 2 * TS * h);
-          acc = __ffma2_rn(X2[h], Y2[h], acc);
+          acc[h % 3] = __ffma2_rn(X2[h], Y2[h], acc[h % 3]);  // three chains (FFMA2 latency)
         }
-        float g = acc.x + acc.y;
+        float g = ((acc[0].x + acc[1].x) + acc[2].x) + ((acc[0].y + acc[1].y) + acc[2].y);
 #pragma unroll
         for (int off = TS / 2; off > 0; off >>= 1) g += __shfl_xor_sync(0xffffffffu, g, off);
         const float al = active ? nrm[p] : 0.f;
