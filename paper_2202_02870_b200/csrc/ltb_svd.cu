@@ -450,7 +450,8 @@ __global__ void complete_u_kernel(int m, int n, const T* __restrict__ w_sorted,
   for (int j = tid; j < g0; j += nth) rn[j] = (R)1 / sb[j];
   __syncthreads();
   // row-major output, the column index fastest: coalesced stores; the column-major reads
-  // revisit each 32-byte sector for 8 consecutive rows and stay in L1
+  // revisit each 32-byte sector for 8 consecutive rows and stay in L1 (a 32 x 32 shared-
+  // memory tile transpose measured slower: 25 tiles and 50 barriers per slice)
   for (int l = tid; l < m * g0; l += nth) {
     const int i = l / g0, j = l - i * g0;
     Ub[(int64_t)i * m + j] = Wb[(int64_t)j * m + i] * rn[j];
@@ -1424,23 +1425,27 @@ int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const 
 //   svt(G) = V diag((s - tau)_+ / s) V^T G          (I1 <  I2, V of G^T)
 // V is re-orthonormalised by one Newton-Schulz step, V <- V (3I - V^T V) / 2,
 // every call, so rounding does not accumulate across iterations.
-__global__ void ns_combine_kernel(int64_t batch, int n, const float* __restrict__ S, float* __restrict__ M,
-                                  const int* skip) {
+// one slice per blockIdx.y, 32-bit index math within the slice (the 64-bit divisions of a
+// flat index made these HBM passes run at a third of the bandwidth)
+__global__ void ns_combine_kernel(int n, const float* __restrict__ S, float* __restrict__ M, const int* skip) {
   if (skip && *skip) return;
-  const int64_t total = batch * (int64_t)n * n;
-  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = l % ((int64_t)n * n);
-    M[l] = (r / n == r % n ? 1.5f : 0.f) - 0.5f * S[l];
+  const int nn = n * n;
+  const int64_t off = (int64_t)blockIdx.y * nn;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
+    const int i = l / n;
+    M[off + l] = (l - i * n == i ? 1.5f : 0.f) - 0.5f * S[off + l];
   }
 }
 
-__global__ void col_scale_kernel(int64_t batch, int n, const float* __restrict__ V, const float* __restrict__ d,
-                                 float* __restrict__ T, const int* skip) {
+__global__ void col_scale_kernel(int n, const float* __restrict__ V, const float* __restrict__ d, float* __restrict__ T,
+                                 const int* skip) {
   if (skip && *skip) return;
-  const int64_t total = batch * (int64_t)n * n;
-  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < total; l += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = l / ((int64_t)n * n);
-    T[l] = V[l] * d[b * n + (int)(l % n)];
+  const int nn = n * n;
+  const int64_t off = (int64_t)blockIdx.y * nn;
+  const float* db = d + (int64_t)blockIdx.y * n;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
+    const int i = l / n;
+    T[off + l] = V[off + l] * db[l - i * n];
   }
 }
 
@@ -1466,7 +1471,7 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
                        float* V, int warm, const int* skip) {
   const bool trans = I1 < I2;
   const int64_t m = trans ? I2 : I1, n = trans ? I1 : I2;
-  if (batch <= 0 || n < 32) return LTB_EUNSUPPORTED;
+  if (batch <= 0 || batch > 65535 || n < 32) return LTB_EUNSUPPORTED;  // grid.y carries the slice
   const int64_t nn = n * n;
   float *A0 = nullptr, *Y = nullptr, *sv = nullptr, *dd = nullptr, *VR = nullptr, *Vn = nullptr, *S = nullptr;
   int* kept = nullptr;
@@ -1532,13 +1537,13 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
   // every 2nd, 2.1e-4 every 4th)
   LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_T, Vc, n, nn, LTB_OP_N, Vc, n, nn, S, n, nn, nullptr, nullptr,
                         nullptr, nullptr, nullptr, skip));
-  const unsigned grid = grid_for(batch * nn, 256, ctx->num_sms * 8);
-  ns_combine_kernel<<<grid, 256, 0, ctx->stream>>>(batch, (int)n, S, Y, skip);  // Y reused as M
+  const dim3 grid((unsigned)std::min<int64_t>((nn + 1023) / 1024, 64), (unsigned)batch);
+  ns_combine_kernel<<<grid, 256, 0, ctx->stream>>>((int)n, S, Y, skip);  // Y reused as M
   LTB_LAUNCH_CHECK(ctx);
   LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, Vc, n, nn, LTB_OP_N, Y, n, nn, V, n, nn, nullptr, nullptr,
                         nullptr, nullptr, nullptr, skip));
   // T = V diag(sqrt((s - tau)_+ / s)),  Z = T T^T (K limited to the kept count),  out
-  col_scale_kernel<<<grid, 256, 0, ctx->stream>>>(batch, (int)n, V, dd, VR, skip);  // VR reused as T
+  col_scale_kernel<<<grid, 256, 0, ctx->stream>>>((int)n, V, dd, VR, skip);  // VR reused as T
   LTB_LAUNCH_CHECK(ctx);
   LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, VR, n, nn, LTB_OP_T, VR, n, nn, S, n, nn, nullptr, nullptr,
                         kept, nullptr, nullptr, skip));
