@@ -134,6 +134,9 @@ struct ltb_ctx {
   unsigned long long* d_stats = nullptr;  // [0] Jacobi slices, [1] Jacobi sweeps
   // copy streams of the pipelined host-to-host l_product (created on first use)
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  // pageable host copies: two pinned staging buffers and their DMA events (first use)
+  void* h_stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev_stage[2] = {nullptr, nullptr};
 };
 
 struct ltb_spec {
