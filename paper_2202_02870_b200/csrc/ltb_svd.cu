@@ -1358,6 +1358,8 @@ int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const
   return LTB_OK;
 }
 
+// early-stop scale (x sqrt(tol)) for QR-path calls that do not set their own (0: off)
+float g_qr_early = 1.f;
 // 1 when the QR-preconditioned resident kernel takes this fp32 SVT; 0 to use the others
 int g_svt_qr = 1;
 int g_qr_max_sweeps = 40;  // timing hook: 0 measures the QR and emission stages alone
@@ -1367,10 +1369,15 @@ int g_qr_ts = 8;
 
 // LTB_EUNSUPPORTED when the shape does not fit the QR-preconditioned kernel
 // chol: A holds n x n Gram matrices (I1 == I2 == n), factored by Cholesky instead of Householder
-int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o,
+int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o_in,
                      bool chol = false) {
   const int m = (int)std::max(I1, I2), n = (int)std::min(I1, I2);
   if (!g_svt_qr || g_force_blocked || n < 32 || batch > 0x7fffffff) return LTB_EUNSUPPORTED;
+  JacobiOut o = o_in;
+  // cold calls too: stop after a sweep whose rotations all had relative inner products
+  // below sqrt(tol) (see jacobi_qr_kernel; tol = the rotation threshold)
+  if (o.early_stop == 0.f && g_qr_early > 0.f)
+    o.early_stop = g_qr_early * sqrtf(FLT_EPSILON * sqrtf((float)n) * o.tol_scale);
   int TSv = 16, MPLv = 0;
   if (g_qr_ts == 8 && n > 48 && n <= 192) {  // 8-lane teams: one pair per team per round
     TSv = 8;
@@ -1564,6 +1571,7 @@ extern "C" void ltb_debug_set_svd_blocked(int v) { g_force_blocked = v; }
 extern "C" void ltb_debug_set_svt_qr(int v) { g_svt_qr = v; }
 extern "C" void ltb_debug_set_qr_max_sweeps(int v) { g_qr_max_sweeps = v; }
 extern "C" void ltb_debug_set_qr_ts(int v) { g_qr_ts = v; }
+extern "C" void ltb_debug_set_qr_early(float v) { g_qr_early = v; }
 extern "C" void ltb_debug_set_qr_timeline(void* p) { g_qr_dbg = (unsigned long long*)p; }
 
 // SVT of `batch` row-major I1 x I2 slices: out = U (S - tau)_+ V^H
