@@ -609,6 +609,9 @@ struct BlockGeom {
 
 constexpr size_t kBlockSmem = 200 * 1024;
 int g_force_blocked = 0;  // test hook: route every slice size through the blocked tier
+// early-stop scale (x sqrt(tol)) of the fp32 Jacobi for calls that do not set their own
+// (QR path, blocked-tier svt / values; 0: run to a sweep without rotations)
+float g_qr_early = 1.f;
 
 __global__ void fill_int_kernel(int64_t n, int* __restrict__ p, int v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
@@ -639,7 +642,7 @@ __global__ void block_load_kernel(int64_t I1, int64_t I2, const T* __restrict__ 
 template <typename T, bool WANT_V, int MPL, int NTMAX>
 __global__ void __launch_bounds__(NTMAX, 1)
     jacobi_block_kernel(BlockGeom g, int round, int full, T* __restrict__ W, int* __restrict__ rot,
-                        const int* __restrict__ active, const int* __restrict__ skip) {
+                        const int* __restrict__ active, const int* __restrict__ skip, unsigned* __restrict__ relmax) {
   using R = typename scalar_traits<T>::real;
   constexpr bool CPLX = scalar_traits<T>::is_complex;
   if (skip && *skip) return;
@@ -667,6 +670,7 @@ __global__ void __launch_bounds__(NTMAX, 1)
   T* C = reinterpret_cast<T*>(smem_raw);
   R* nrm = reinterpret_cast<R*>(C + (size_t)2 * b * mp);
   int* flag = reinterpret_cast<int*>(nrm + 2 * b);
+  unsigned* fmax_sh = reinterpret_cast<unsigned*>(flag + 1);  // largest relative rotated |gamma| (float bits)
   T* Ws = W + s * (int64_t)g.n * mp;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
   auto gcol = [&](int l) { return l < b ? cp0 + l : cq0 + (l - b); };
@@ -678,7 +682,10 @@ __global__ void __launch_bounds__(NTMAX, 1)
     int4* dst = reinterpret_cast<int4*>(C + (size_t)l * mp);
     for (int v = lane; v < vpc; v += 32) dst[v] = src[v];
   }
-  if (tid == 0) *flag = 0;
+  if (tid == 0) {
+    *flag = 0;
+    *fmax_sh = 0u;
+  }
   __syncthreads();
   for (int l = warp; l < 2 * b; l += nwarps) {
     R s2 = 0;
@@ -770,6 +777,7 @@ __global__ void __launch_bounds__(NTMAX, 1)
         nrm[p] = fmax(al - t * gabs, (R)0);
         nrm[q] = be + t * gabs;
         *flag = 1;
+        if (relmax) atomicMax(fmax_sh, __float_as_uint((float)(gabs / (sqrt(al) * sqrt(be)))));
       }
     }
     __syncthreads();
@@ -780,12 +788,18 @@ __global__ void __launch_bounds__(NTMAX, 1)
     int4* dst = reinterpret_cast<int4*>(Ws + (int64_t)gcol(l) * mp);
     for (int v = lane; v < vpc; v += 32) dst[v] = src[v];
   }
-  if (tid == 0 && *flag) rot[s] = 1;
+  if (tid == 0 && *flag) {
+    rot[s] = 1;
+    if (relmax) atomicMax(&relmax[s], *fmax_sh);
+  }
 }
 
-// after a sweep: a slice without rotations is converged; count the rest
+// after a sweep: a slice without rotations is converged; count the rest.  relmax (svt /
+// values): so is a slice whose rotations all had relative inner products below `early`
+// (the inner products they left behind are ~early^2, as in jacobi_qr_kernel)
 __global__ void block_sweep_update_kernel(int64_t batch, int* __restrict__ rot, int* __restrict__ active,
-                                          int* __restrict__ count, unsigned long long* stats) {
+                                          int* __restrict__ count, unsigned long long* stats,
+                                          unsigned* __restrict__ relmax, float early) {
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
@@ -793,8 +807,10 @@ __global__ void block_sweep_update_kernel(int64_t batch, int* __restrict__ rot, 
   for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
     const int a = active[s];
     local += a;  // this slice took part in the sweep
-    active[s] = a && rot[s];
+    const bool small = relmax && __uint_as_float(relmax[s]) < early;
+    active[s] = a && rot[s] && !small;
     rot[s] = 0;
+    if (relmax) relmax[s] = 0u;
   }
   atomicAdd(&cnt, local);
   __syncthreads();
@@ -867,7 +883,7 @@ __global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, Jaco
 // the sweep loop of the blocked tier for one kernel variant
 template <typename T, bool WANT_V, int MPL, int NTMAX>
 int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int* rot, int* active, int* count,
-                     const JacobiOut& o, int max_sweeps) {
+                     const JacobiOut& o, int max_sweeps, unsigned* relmax, float early) {
   using R = typename scalar_traits<T>::real;
   const int nbp = g.nb + (g.nb & 1);
   const size_t smem = 2 * (size_t)g.mp * sizeof(T) * g.b + 2 * g.b * sizeof(R) + 16;
@@ -879,10 +895,10 @@ int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int*
   const int threads = 32 * std::min(g.b, NTMAX / 32);
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int r = 0; r < nbp - 1; ++r) {
-      kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip);
+      kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip, relmax);
       LTB_LAUNCH_CHECK(ctx);
     }
-    block_sweep_update_kernel<<<1, 256, 0, ctx->stream>>>(batch, rot, active, count, o.stats);
+    block_sweep_update_kernel<<<1, 256, 0, ctx->stream>>>(batch, rot, active, count, o.stats, relmax, early);
     LTB_LAUNCH_CHECK(ctx);
     if (cap != cudaStreamCaptureStatusNone) continue;  // no host read-back inside a capture
     LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -928,11 +944,18 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   T* W = nullptr;
   int* flags = nullptr;
   LTB_TRY(ltb_ws_alloc(ctx, sizeof(T) * (size_t)batch * g.n * g.mp, (void**)&W));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * (size_t)(2 * batch + 4), (void**)&flags));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * (size_t)(3 * batch + 4), (void**)&flags));
   int* rot = flags;
   int* active = flags + batch;
-  int* count = flags + 2 * batch;
+  unsigned* relmax = nullptr;
+  float early = 0.f;
+  if ((f32 || c32) && !WANT_V && g_qr_early > 0.f) {  // svt / values in single precision
+    relmax = reinterpret_cast<unsigned*>(flags + 2 * batch);
+    early = g_qr_early * sqrtf(FLT_EPSILON * sqrtf((float)std::max(g.m, 1)));
+  }
+  int* count = flags + 3 * batch;
   LTB_CUDA_TRY(ctx, cudaMemsetAsync(rot, 0, sizeof(int) * batch, ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaMemsetAsync(flags + 2 * batch, 0, sizeof(int) * batch, ctx->stream));
   fill_int_kernel<<<grid_for(batch, 256, 1024), 256, 0, ctx->stream>>>(batch, active, 1);
   LTB_LAUNCH_CHECK(ctx);
   {
@@ -943,14 +966,14 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   if (g.n > 1) {
     int st = LTB_OK;
     if constexpr (!WANT_V && (f32 || c32)) {
-      if (mpl == 8) st = run_block_sweeps<T, WANT_V, 8, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
-      else if (mpl == 16 && f32) st = run_block_sweeps<T, WANT_V, 16, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
-      else if (mpl == 16) st = run_block_sweeps<T, WANT_V, 16, 512>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
-      else if (mpl == 32 && f32) st = run_block_sweeps<T, WANT_V, 32, 512>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
-      else if (mpl == 32) st = run_block_sweeps<T, WANT_V, 32, 384>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
-      else st = run_block_sweeps<T, WANT_V, 0, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
+      if (mpl == 8) st = run_block_sweeps<T, WANT_V, 8, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+      else if (mpl == 16 && f32) st = run_block_sweeps<T, WANT_V, 16, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+      else if (mpl == 16) st = run_block_sweeps<T, WANT_V, 16, 512>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+      else if (mpl == 32 && f32) st = run_block_sweeps<T, WANT_V, 32, 512>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+      else if (mpl == 32) st = run_block_sweeps<T, WANT_V, 32, 384>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+      else st = run_block_sweeps<T, WANT_V, 0, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
     } else {
-      st = run_block_sweeps<T, WANT_V, 0, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps);
+      st = run_block_sweeps<T, WANT_V, 0, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
     }
     LTB_TRY(st);
   }
@@ -1358,8 +1381,6 @@ int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const
   return LTB_OK;
 }
 
-// early-stop scale (x sqrt(tol)) for QR-path calls that do not set their own (0: off)
-float g_qr_early = 1.f;
 // 1 when the QR-preconditioned resident kernel takes this fp32 SVT; 0 to use the others
 int g_svt_qr = 1;
 int g_qr_max_sweeps = 40;  // timing hook: 0 measures the QR and emission stages alone
