@@ -230,7 +230,7 @@ class CopyPool {
 
  private:
   void part(int t) {
-    const size_t per = (n_ / kCopyThreads + 63) & ~size_t(63);
+    const size_t per = ((n_ + kCopyThreads - 1) / kCopyThreads + 63) & ~size_t(63);  // covers n_
     const size_t b = std::min(n_, per * t), e = std::min(n_, b + per);
     if (e > b) std::memcpy(dst_ + b, src_ + b, e - b);
   }

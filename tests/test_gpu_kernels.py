@@ -287,3 +287,21 @@ def test_svt_qr_rank_deficient(shape):
     for i in range(batch):
         den = max(np.linalg.norm(ref[i]), 1e-30)
         assert np.linalg.norm(got[i] - ref[i]) / den < 1e-4 or np.linalg.norm(got[i]) < 1e-6
+
+
+@pytest.mark.parametrize("nbytes", [4, (1 << 20) + 4, (16 << 20) - 4, (16 << 20) + 4, (40 << 20) + 12])
+def test_host_device_copies_pageable_and_pinned(nbytes):
+    """Uploads / downloads of pageable numpy buffers go through the pinned staging pipeline
+    (chunks of 16 MiB, threaded host copies): bit-exact round trips at chunk boundaries, and
+    the same through pinned host memory (direct DMA)."""
+    import torch
+
+    rng = np.random.default_rng(nbytes)
+    x = rng.integers(0, 2**32, size=nbytes // 4, dtype=np.uint32).view(np.float32)
+    d = nat.DeviceArray.from_numpy(x)
+    np.testing.assert_array_equal(d.numpy().view(np.uint32), x.view(np.uint32))
+    pin = torch.empty(x.shape, dtype=torch.float32, pin_memory=True).numpy()
+    d.numpy(out=pin)
+    np.testing.assert_array_equal(pin.view(np.uint32), x.view(np.uint32))
+    d2 = nat.DeviceArray.from_numpy(pin)
+    np.testing.assert_array_equal(d2.numpy().view(np.uint32), x.view(np.uint32))
