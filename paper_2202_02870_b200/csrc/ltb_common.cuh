@@ -235,6 +235,8 @@ int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int i
                        double* d_sumsq /* device, 2 doubles, may be null */);
 int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
                        float* V, int warm, const int* skip);
+int ltb_svt_carry64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const double* G, double tau,
+                         double* out, double* V, int warm, const int* skip);
 int ltb_svt_mirror_impl(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1, int64_t I2,
                         const void* d_a, double tau, void* d_out, const int* d_skip);
 int ltb_transform_pair_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,

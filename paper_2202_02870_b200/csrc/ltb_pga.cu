@@ -46,6 +46,7 @@ struct ltb_pga {
   // fp32 real transform domain: right singular bases carried between iterations
   // (ltb_svt_carry_impl); allocated on first use, warm after the first SVT
   float* vcarry = nullptr;
+  double* vcarry64 = nullptr;  // the same for an fp64 real transform domain
   int warm = 0;
   bool carry_off = false;
   bool tc_off = false;        // the tensor-core transform path declined this shape
@@ -352,6 +353,16 @@ int pga_svt(ltb_pga* g, double mu, const int* skip) {
     else if (carry == LTB_EUNSUPPORTED) g->carry_off = true;
     else return carry;
   }
+  // fp64 real transform domain: the same carry with a warm-started resident Jacobi
+  if (g->hat_dtype == LTB_F64 && !g->carry_off && g_pga_carry) {
+    const int64_t n = std::min(g->I1, g->I2);
+    if (!g->vcarry64) LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * g->P * n * n, (void**)&g->vcarry64));
+    carry = ltb_svt_carry64_impl(ctx, g->P, g->I1, g->I2, (const double*)g->hat_a, mu, (double*)g->hat_b,
+                                 g->vcarry64, g->warm, skip);
+    if (carry == LTB_OK) g->warm = 1;
+    else if (carry == LTB_EUNSUPPORTED) g->carry_off = true;
+    else return carry;
+  }
   // otherwise (conjugate slice pairs of the real iterate are solved once)
   if (carry != LTB_OK)
     LTB_TRY(ltb_svt_mirror_impl(ctx, g->spec, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, g->hat_b, skip));
@@ -608,6 +619,7 @@ void ltb_pga_destroy(ltb_pga* g) {
   ltb_ws_free(ctx, g->d_state);
   ltb_ws_free(ctx, g->d_scalars);
   ltb_ws_free(ctx, g->vcarry);
+  ltb_ws_free(ctx, g->vcarry64);
   cudaStreamSynchronize(ctx->stream);
   delete g;
 }

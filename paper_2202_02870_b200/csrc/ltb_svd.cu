@@ -1588,6 +1588,72 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
 namespace {
 }  // namespace
 
+// fp64 SVT carrying the slices' right bases V (n x n row-major, n = min(I1, I2)) between
+// PGA iterations, as ltb_svt_carry_impl does in fp32 but without the QR / Cholesky stage:
+// the resident Jacobi (accumulating its rotations J) runs on A0 = G V (V^T G when I1 < I2),
+// whose columns are nearly orthogonal, so it needs a few sweeps instead of a dozen; its
+// columns w_j = sigma_j u_j are those of G itself (V J is orthogonal), so the usual V-free
+// recomposition with G applies unchanged, and V <- V J for the next call (rounding drift
+// ~1e-16 per call in fp64: no re-orthonormalisation).  warm == 0: A0 = G, V <- J.
+int ltb_svt_carry64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const double* G, double tau,
+                         double* out, double* V, int warm, const int* skip) {
+  const bool trans = I1 < I2;
+  const int64_t m = trans ? I2 : I1, n = trans ? I1 : I2, nn = n * n;
+  if (batch <= 0 || batch > 65535 || n < 2) return LTB_EUNSUPPORTED;
+  const int F = LTB_F64;
+  double *A0 = nullptr, *w = nullptr, *vc = nullptr, *z = nullptr, *d = nullptr;
+  int* kept = nullptr;
+  auto release = [&]() {
+    for (void* p : {(void*)A0, (void*)w, (void*)vc, (void*)z, (void*)d, (void*)kept}) ltb_ws_free(ctx, p);
+  };
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * I1 * I2, (void**)&A0));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * n * m, (void**)&w));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * nn, (void**)&vc));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * n * m, (void**)&z));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * n, (void**)&d));
+  LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * batch, (void**)&kept));
+  const double* src = G;
+  if (warm) {
+    if (trans)  // A0 = V^T G  (I1 x I2)
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, I1, I2, n, LTB_OP_T, V, n, nn, LTB_OP_N, G, I2, I1 * I2, A0, I2, I1 * I2,
+                            nullptr, nullptr, nullptr, nullptr, nullptr, skip));
+    else  // A0 = G V
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, I1, I2, n, LTB_OP_N, G, I2, I1 * I2, LTB_OP_N, V, n, nn, A0, I2, I1 * I2,
+                            nullptr, nullptr, nullptr, nullptr, nullptr, skip));
+    src = A0;
+  }
+  JacobiOut o{w, nullptr, vc, kept, d, tau, skip};
+  int st = launch_jacobi<double, true>(ctx, batch, I1, I2, src, o);
+  if (st != LTB_OK) {
+    release();
+    return st;
+  }
+  if (!trans) {
+    // Z = D W^T G (n x I2, rows limited to the kept count); out = W Z
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, I2, m, LTB_OP_C, w, m, n * m, LTB_OP_N, G, I2, I1 * I2, z, I2, n * I2,
+                          kept, nullptr, nullptr, d, nullptr, skip));
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, I1, I2, n, LTB_OP_T, w, m, n * m, LTB_OP_N, z, I2, n * I2, out, I2, I1 * I2,
+                          nullptr, nullptr, kept, nullptr, nullptr, skip));
+  } else {
+    // Y = G W D (I1 x n, columns limited to the kept count); out = Y W^T
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, I1, n, m, LTB_OP_N, G, I2, I1 * I2, LTB_OP_T, w, m, n * m, z, n, I1 * n,
+                          nullptr, kept, nullptr, nullptr, d, skip));
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, I1, I2, n, LTB_OP_N, z, n, I1 * n, LTB_OP_C, w, m, n * m, out, I2, I1 * I2,
+                          nullptr, nullptr, kept, nullptr, nullptr, skip));
+  }
+  // V <- V J (J's sorted columns are the rows of vc), or V <- J on the cold call
+  if (warm) {
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, V, n, nn, LTB_OP_T, vc, n, nn, A0, n, nn, nullptr, nullptr,
+                          nullptr, nullptr, nullptr, skip));
+    LTB_CUDA_TRY(ctx, cudaMemcpyAsync(V, A0, sizeof(double) * batch * nn, cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    cols_to_rowmajor_kernel<double><<<grid_for(batch * nn, 256, 4096), 256, 0, ctx->stream>>>(batch, (int)n, vc, V);
+    LTB_LAUNCH_CHECK(ctx);
+  }
+  release();
+  return LTB_OK;
+}
+
 extern "C" void ltb_debug_set_svd_blocked(int v) { g_force_blocked = v; }
 extern "C" void ltb_debug_set_svt_qr(int v) { g_svt_qr = v; }
 extern "C" void ltb_debug_set_qr_max_sweeps(int v) { g_qr_max_sweeps = v; }
