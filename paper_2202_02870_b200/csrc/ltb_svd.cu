@@ -283,10 +283,16 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
         const R al = active ? nrm[p] : (R)0;
         const R be = active ? nrm[q] : (R)0;
         const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
-        if (!active || !(gabs > tol * sqrt(al) * sqrt(be)) || al == (R)0 || be == (R)0) continue;
-        const R zeta = (be - al) / (2 * gabs);
-        const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
-        const R c = (R)1 / sqrt((R)1 + t * t);
+        // one square root for the test, and sqrt(1 + zeta^2) / rsqrt instead of hypot and a
+        // division below |zeta| = 1e100 (the rotation chain is the latency of a round)
+        constexpr bool DBL = sizeof(R) == 8;  // (fp32 keeps two roots: al * be may overflow)
+        const R sab = DBL ? sqrt(al * be) : sqrt(al) * sqrt(be);
+        if (!active || !(gabs > tol * sab) || al == (R)0 || be == (R)0) continue;
+        const R zeta = (be - al) * ((R)0.5 / gabs);
+        const R az = fabs(zeta);
+        const R den = az < (R)1e18 ? az + sqrt(fma(az, az, (R)1)) : (R)2 * az;
+        const R t = (zeta >= 0 ? (R)1 : (R)-1) / den;
+        const R c = DBL ? rsqrt(fma(t, t, (R)1)) : (R)1 / sqrt(fma(t, t, (R)1));
         const R s = c * t;
         // phase e^{-i phi} applied to column q so the Gram entry becomes real
         T ph;
