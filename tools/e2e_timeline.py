@@ -16,15 +16,14 @@ c = torch.empty((256, 256, 3, 32), dtype=torch.float32, pin_memory=True).numpy()
 a[...] = rng.standard_normal(a.shape)
 b[...] = rng.standard_normal(b.shape)
 spec = L.make_spec("dct", (256, 256, 3, 32))
-for ch, cb in [tuple(map(int, x.split("x"))) for x in (sys.argv[1:] or ["8x1", "4x4"])]:
+for ch in [int(x) for x in (sys.argv[1:] or ["8"])]:
     nat.lib().ltb_debug_set_lprod_chunks(ch)
-    nat.lib().ltb_debug_set_lprod_cols(cb)
     for _ in range(3):
         L.l_product(a, b, spec, out=c)
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
         L.l_product(a, b, spec, out=c)
     ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     t0 = min(e.time_range.start for e in ev)
-    print(f"--- {ch} x {cb}: span {(max(e.time_range.end for e in ev) - t0):.1f} us")
+    print(f"--- {ch} row chunks: span {(max(e.time_range.end for e in ev) - t0):.1f} us")
     for e in sorted(ev, key=lambda e: e.time_range.start):
         print(f"  {e.time_range.start - t0:8.1f} {e.time_range.end - t0:8.1f}  {e.name[:60]}")
