@@ -14,8 +14,8 @@ METRICS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
-    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed", "smem wavefronts %"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem wavefronts %"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
@@ -26,8 +26,16 @@ METRICS = [
 ]
 
 
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "nsecond": 1e-9,
+         "usecond": 1e-6, "msecond": 1e-3}
+
+
 def report_rows(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Rows of an .ncu-rep (via ncu -i) or of its `--page raw --csv` export."""
+    if path.endswith(".csv"):
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     if len(rows) < 3:
         return []
@@ -39,6 +47,12 @@ def report_rows(path):
             if key in h:
                 i = h.index(key)
                 d[label] = f"{r[i]} {units[i]}".strip()
+        try:  # achieved DRAM bandwidth of the launch: (read + write) / duration
+            val = lambda k: float(r[h.index(k)].replace(",", "")) * SCALE[units[h.index(k)]]
+            gbs = (val("dram__bytes_read.sum") + val("dram__bytes_write.sum")) / val("gpu__time_duration.sum") / 1e9
+            d["DRAM GB/s (read + write / duration)"] = f"{gbs:.0f}"
+        except (ValueError, KeyError):
+            pass
         stalls = [(h[i], r[i]) for i in range(len(h)) if h[i].startswith("smsp__pcsamp_warps_issue_stalled_")
                   and not h[i].endswith("_not_issued")]
         stalls = sorted(((float(v.replace(",", "") or 0), k.split("stalled_")[-1]) for k, v in stalls), reverse=True)
