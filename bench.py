@@ -17,6 +17,7 @@ reported in the "pga" object.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import math
 import os
@@ -77,6 +78,25 @@ def _cpu_info():
 
 
 # ----------------------------------------------------------------------------- CPU (oracle) legs
+@contextlib.contextmanager
+def _host_threads():
+    """Every host core this process may run on for the CPU legs: BLAS threads and
+    scipy.fft workers (torchrun sets OMP_NUM_THREADS=1 per rank; the CPU legs run on
+    rank 0 alone, so they take the whole host)."""
+    n = len(os.sched_getaffinity(0))
+    with contextlib.ExitStack() as st:
+        try:
+            from threadpoolctl import threadpool_limits
+
+            st.enter_context(threadpool_limits(limits=n))
+        except Exception:
+            pass
+        import scipy.fft
+
+        st.enter_context(scipy.fft.set_workers(n))
+        yield
+
+
 def cpu_lproduct(steps: int, warmup: int, budget_s: float | None = None):
     """The reference algorithm (oracle port) on the host cores, seconds per product."""
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -725,10 +745,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+    with _host_threads() if (args.impl == "reference" or int(os.environ.get("WORLD_SIZE", "1")) == 1) \
+            else contextlib.nullcontext():
+        if args.impl == "reference":
+            run_reference(args)
+        else:
+            run_ours(args)
 
 
 if __name__ == "__main__":
