@@ -35,6 +35,10 @@ sys.path.insert(0, str(ROOT))
 CFG2 = dict(a=(256, 128, 3, 32), b=(128, 256, 3, 32), kind="dct")
 CFG3 = dict(shape=(144, 176, 3, 100), rank=10, sr=0.2, iters=200)
 GFLOP_CFG2 = 2_491_416_576
+# the `config` object both arms print (identical, so the driver can pair the lines)
+CONFIG2 = {"workload": "config2 l_product A 256x128x3x32 * B 128x256x3x32, DCT modes 3,4",
+           "flop_per_step": GFLOP_CFG2}
+L2_NOTE = "flushed (512 MiB write) before every timed step"
 
 
 def _peaks():
@@ -163,17 +167,16 @@ def run_reference(args):
         "metric": "*_L-product GFLOP/s",
         "value": value,
         "unit": "GFLOP/s",
-        "n_gpus": ws,
+        "n_gpus": args.gpus,
         "steps": len(times),
         "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic N(0,1) seed 0 (BASELINE config 2 shapes)",
-        "config": {"workload": "config2 l_product A 256x128x3x32 * B 128x256x3x32, DCT modes 3,4",
-                   "flop_per_step": GFLOP_CFG2},
+        "config": dict(CONFIG2),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": info["blas_threads"], "kind": "port",
                          "sample": f"{len(times)} full config-2 products (oracle/ltensor_oracle.py, numpy/scipy "
                                    f"OpenBLAS), {info.get('cpu', '?')}"},
@@ -231,9 +234,11 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- our arm
 def run_ours_dist(args):
-    """N > 1: the row-sharded *_L product of SURVEY.md §8(e) (weak scaling).  Rank g holds 256
-    rows of A (global I1 = 256 N) and 128/N rows of B; B-hat is all-gathered over NCCL; each
-    rank produces its 256 rows of C.  Time = max over ranks of the device (CUDA-event) step time."""
+    """N > 1: config 2 strong-scaled with the row-sharded *_L product of SURVEY.md section 8(e).
+    The global operands are the fixed config-2 tensors (the same workload at every N): rank g
+    holds the i1-row block R_g of A (256/N rows) and the l-row block K_g of B (128/N rows);
+    B-hat is all-gathered over NCCL (the only collective); each rank produces its rows of C.
+    Time = max over ranks of the device (CUDA-event) step time."""
     import torch
     import torch.distributed as dist
 
@@ -247,18 +252,22 @@ def run_ours_dist(args):
     nat.set_device(local)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    spec = L.make_spec("dct", (256 * ws, 256, 3, 32))
+    spec = L.make_spec("dct", (256, 256, 3, 32))
     eng = DeviceEngine(spec, (3, 32))
-    a_h, b_full = _cfg2_inputs(seed=rank)
-    _, b_full = _cfg2_inputs(seed=0)  # B is one global operand, row-sharded
+    a_full, b_full = _cfg2_inputs(seed=0)
+    r0, r1 = blocks(256, ws)[rank]
     k0, k1 = blocks(128, ws)[rank]
+    a_h = np.ascontiguousarray(a_full[r0:r1])
+    b_h = np.ascontiguousarray(b_full[k0:k1])
     a = torch.from_numpy(a_h).cuda()
-    b = torch.from_numpy(np.ascontiguousarray(b_full[k0:k1])).cuda()
+    b = torch.from_numpy(b_h).cuda()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    E_a, E_b, E_c = 256 * 128 * 96, 128 * 256 * 96, 256 * 256 * 96
-    flops_job = ws * (2 * 256 * 128 * 256 * 96 + 70 * (E_a + E_c)) + 70 * E_b
     plan = DistLProductPlan(a.shape, b.shape, eng, torch.float32, a.device)
     c = torch.empty(plan.c_shape, dtype=torch.float32, device="cuda")
+    # parity gate: this rank's rows of C against the oracle on a bounded row sample
+    plan.run(a, b, out=c)
+    torch.cuda.synchronize()
+    gate = _parity_gate(c.cpu().numpy(), a_h, b_full)
     # the two compute phases are CUDA graphs; the B-hat all-gather runs between their replays
     l0 = nat.launch_count()
     step = plan.graphed(a, b, c, stream)
@@ -277,10 +286,10 @@ def run_ours_dist(args):
             if i >= args.warmup:
                 times.append(e0.elapsed_time(e1) / 1e3)
         launches = launches_per_step * args.steps
-        # e2e: each rank's operands from pinned host memory and its rows of C back to pinned host
-        # memory, copies inside the timed region (device time, max over ranks)
+        # e2e: each rank's operand rows from pinned host memory and its rows of C back to pinned
+        # host memory, copies inside the timed region (device time, max over ranks)
         a_pin = torch.from_numpy(a_h).pin_memory()
-        b_pin = torch.from_numpy(np.ascontiguousarray(b_full[k0:k1])).pin_memory()
+        b_pin = torch.from_numpy(b_h).pin_memory()
         c_pin = torch.empty(tuple(c.shape), dtype=torch.float32).pin_memory()
         e2e_times = []
         for i in range(args.warmup + args.steps):
@@ -294,29 +303,33 @@ def run_ours_dist(args):
             e1.synchronize()
             if i >= args.warmup:
                 e2e_times.append(e0.elapsed_time(e1) / 1e3)
-    pga = None if args.skip_extras else bench_pga_dist(L, torch, dist, eng_cls=DeviceEngine, args=args)
-    t = torch.tensor([sum(times), sum(e2e_times)], dtype=torch.float64, device="cuda")
+    pga = None if (args.skip_extras or args.skip_pga) else bench_pga_dist(L, torch, dist, eng_cls=DeviceEngine,
+                                                                          args=args)
+    t = torch.tensor([sum(times), sum(e2e_times), gate["rel_err"]], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_step = float(t[0].item())
-    t_e2e = float(t[1].item())
+    t_step, t_e2e, worst = float(t[0].item()), float(t[1].item()), float(t[2].item())
+    gate = {"rows_checked_per_rank": gate["rows_checked"], "rel_err_max_over_ranks": worst,
+            "tol": 1e-4, "ok": worst < 1e-4}
     hbm_peak, _, peak_src = _peaks()
-    alg_bytes = 4 * (E_a + E_b // ws + E_c)
+    E_a, E_b, E_c = 256 * 128 * 96, 128 * 256 * 96, 256 * 256 * 96
+    # per rank: its A rows and C rows once, its B block once plus the gathered B-hat once
+    alg_bytes = 4 * ((r1 - r0) * 128 * 96 + (k1 - k0) * 256 * 96 + E_b + (r1 - r0) * 256 * 96)
     achieved = alg_bytes * args.steps / t_step / 1e9
     line = {
-        "metric": "*_L-product GFLOP/s", "value": flops_job * args.steps / t_step / 1e9, "unit": "GFLOP/s",
+        "metric": "*_L-product GFLOP/s", "value": GFLOP_CFG2 * args.steps / t_step / 1e9, "unit": "GFLOP/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_step / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic N(0,1) (BASELINE config 2 shapes per rank), seeds = rank",
-        "config": {"workload": f"config2 l_product, A rows sharded: A {256 * ws}x128x3x32 * B 128x256x3x32, DCT modes 3,4",
-                   "flop_per_step": flops_job, "l2": "flushed (512 MiB write) before every timed step",
-                   "parallelism": f"row-sharded x{ws}, B-hat all-gather (NCCL)"},
-        "roofline": {"kernel": "whole sharded step", "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": achieved / hbm_peak, "peak_source": f"{peak_src} HBM copy",
-                     "traffic": None},
-        "e2e": {"value": flops_job * args.steps / t_e2e / 1e9, "unit": "GFLOP/s",
-                "h2d_bytes_per_step": int(a_pin.numel() * 4 + b_pin.numel() * 4),
-                "d2h_bytes_per_step": int(c_pin.numel() * 4),
-                "api": "distributed.DistLProductPlan.run per rank, pinned host operands in / rows of C out"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic N(0,1) seed 0 (BASELINE config 2 shapes)",
+        "config": dict(CONFIG2), "l2": L2_NOTE,
+        "parallelism": f"A rows / B rows sharded x{ws}, B-hat all-gather (NCCL)",
+        "parity_gate": gate,
+        "roofline": {"kernel": "whole sharded step (rank-local bytes)", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "peak_source": f"{peak_src} HBM copy", "traffic": None},
+        "e2e": {"value": GFLOP_CFG2 * args.steps / t_e2e / 1e9, "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(E_a * 4 + E_b * 4), "d2h_bytes_per_step": int(E_c * 4),
+                "api": "distributed.DistLProductPlan per rank, pinned host operand rows in / rows of C out "
+                       "(bytes summed over ranks)"},
         "gpu_launches": int(launches), "clocks": clocks.summary(),
     }
     if pga is not None:
@@ -324,6 +337,18 @@ def run_ours_dist(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def _parity_gate(c_rows: np.ndarray, a_rows: np.ndarray, b: np.ndarray, nrows: int = 8) -> dict:
+    """Bounded correctness gate of a bench run: the first `nrows` rows of C (rows of A *_L B
+    depend only on the same rows of A) against the oracle in float64, relative Frobenius."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import ltensor_oracle as O
+
+    r = min(nrows, a_rows.shape[0])
+    ref = O.l_product(a_rows[:r].astype(np.float64), b.astype(np.float64), O.ospec("dct", (r,) + b.shape[1:]))
+    err = float(np.linalg.norm((c_rows[:r] - ref).ravel()) / np.linalg.norm(ref.ravel()))
+    return {"rows_checked": r, "rel_err": err, "tol": 1e-4, "ok": err < 1e-4}
 
 
 def bench_pga_dist(L, torch, dist, eng_cls, args):
@@ -386,9 +411,10 @@ def run_ours(args):
     c = nat.DeviceArray(plan.c_shape, np.float32)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
-    # ---- correctness gate (first product vs the oracle on a bounded check)
+    # ---- correctness gate: the first product's leading rows of C against the oracle (float64)
     plan.run(a, b, c)
     torch.cuda.synchronize()
+    gate = _parity_gate(c.numpy(), a_h, b_h)
 
     def barrier():
         if ws > 1:
@@ -469,6 +495,17 @@ def run_ours(args):
             dt = time.perf_counter() - t0
             if i >= args.warmup:
                 e2e_t.append(dt)
+        # the drop-in call exactly as a reference user makes it: plain (pageable) numpy arrays in,
+        # a new numpy array out, no `out=` (the library stages pageable buffers through pinned memory)
+        e2e_pg = []
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = L.l_product(a_h, b_h, spec)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                e2e_pg.append(dt)
+        gate_e2e = _parity_gate(res, a_h, b_h)
         pga = None if args.skip_pga else bench_pga(L, nat, torch, args)
         extras = None if args.skip_extras else bench_extras(L, nat, torch, args, cpu=not args.no_cpu_baseline)
 
@@ -519,16 +556,22 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": 1e3 * t_step / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic N(0,1) (BASELINE config 2 shapes), seed = rank",
-        "config": {"workload": "config2 l_product A 256x128x3x32 * B 128x256x3x32, DCT modes 3,4",
-                   "flop_per_step": GFLOP_CFG2, "l2": "flushed (512 MiB write) before every timed step",
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "config": dict(CONFIG2),
+        "l2": L2_NOTE,
+        "parallelism": "single GPU",
+        "parity_gate": {"device_step": gate, "e2e_pageable": gate_e2e, "ok": gate["ok"] and gate_e2e["ok"]},
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(a_h.nbytes + b_h.nbytes),
                 "d2h_bytes_per_step": int(out.nbytes), "api": "paper_2202_02870_b200.l_product(numpy, numpy, spec, out=numpy) on pinned host arrays"},
+        "e2e_pageable": {"value": GFLOP_CFG2 * len(e2e_pg) / sum(e2e_pg) / 1e9, "unit": "GFLOP/s",
+                         "h2d_bytes_per_step": int(a_h.nbytes + b_h.nbytes), "d2h_bytes_per_step": int(res.nbytes),
+                         "ms_per_step": 1e3 * sum(e2e_pg) / len(e2e_pg),
+                         "api": "paper_2202_02870_b200.l_product(a, b, spec) on plain pageable numpy arrays, "
+                                "new numpy result (the reference's own signature)"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
@@ -618,8 +661,15 @@ def bench_pga(L, nat, torch, args):
             "k3_ms": t_k3 * 1e3,
             "iteration_ceiling_it_s": 2466, "iteration_frac": (n_done / dt) / 2466,
             "ceiling_source": "SURVEY.md §8(d): max(HBM 305.1 MB, 26.67 GFLOP) per iteration"}
+    # the same run at the reference's precision (completion.py:154 computes in float64), the
+    # like-for-like pair of the float64 CPU baseline
+    _run_pga(L, nat, torch, m, mask, spec, "fp64", 3)
+    fp64 = {"value": _run_pga(L, nat, torch, m, mask, spec, "fp64", args.pga_iters), "unit": "it/s",
+            "dtype": "f64", "iterations": args.pga_iters,
+            "note": "precision='fp64': float64 transforms, Jacobi SVT and recomposition (the reference's precision)"}
     return {"metric": "PGA completion iters/sec", "value": n_done / dt, "unit": "it/s", "iterations": n_done,
-            "seconds": dt, "dtype": "f32", "jacobi_sweeps_per_slice": sweeps / max(slices, 1), "roofline": roof,
+            "seconds": dt, "dtype": "f32", "fp64": fp64,
+            "jacobi_sweeps_per_slice": sweeps / max(slices, 1), "roofline": roof,
             "config": {"workload": "config3 144x176x3x100 rank-10 DCT(modes 3,4), Bernoulli(0.2), tol 1e-300",
                        "data": "synthetic stand-in for the paper's colour videos (not in this container)"},
             "rse_vs_m": float(np.linalg.norm(x - m) ** 2 / max(np.linalg.norm(x) ** 2, 1e-300))}
@@ -728,6 +778,26 @@ def bench_extras(L, nat, torch, args, cpu):
     return out
 
 
+def _self_launch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) of this script under
+    torch.distributed.run on 127.0.0.1 and return its exit code.  Fails loudly when fewer than
+    N GPUs are visible instead of printing a 1-GPU line."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-extras", action="store_true")
@@ -745,6 +815,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    in_torchrun = "WORLD_SIZE" in os.environ
+    if in_torchrun and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}", file=sys.stderr)
+        sys.exit(2)
+    if args.impl == "ours" and args.gpus > 1 and not in_torchrun:
+        sys.exit(_self_launch(args))
     with _host_threads() if (args.impl == "reference" or int(os.environ.get("WORLD_SIZE", "1")) == 1) \
             else contextlib.nullcontext():
         if args.impl == "reference":

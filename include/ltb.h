@@ -71,6 +71,9 @@ const char* ltb_ctx_last_error(const ltb_ctx* ctx);
 /* adopt an external cudaStream_t (e.g. torch.cuda.current_stream()); NULL = own stream */
 int ltb_ctx_set_stream(ltb_ctx* ctx, void* stream);
 int ltb_ctx_synchronize(ltb_ctx* ctx);
+/* make ctx's device the calling host thread's current CUDA device (contexts of several
+ * devices may coexist in one process; each call runs on the current device) */
+int ltb_ctx_make_current(ltb_ctx* ctx);
 /* number of ltb kernels launched on this context since creation */
 int64_t ltb_ctx_launch_count(const ltb_ctx* ctx);
 /* device-side counters (3 entries): h_out[0] = Jacobi slices solved, h_out[1] = Jacobi sweeps run,

@@ -201,6 +201,25 @@ def t_svd(a, spec):
     return u, s, v, norms
 
 
+def truncate(u, s, v, k, spec):
+    """linalg.py:121-129: u(:,1:k) *_L s(1:k,1:k) *_L v(:,1:k)^T (spec shape-agnostic here)."""
+    return l_product(l_product(u[:, :k], s[:k, :k], spec), l_transpose(v[:, :k], spec), spec)
+
+
+def inner_product(a, b):
+    """core.py:26-35: vdot, conjugate-linear in the first argument."""
+    out = np.vdot(np.asarray(a), np.asarray(b))
+    return float(out.real) if np.isrealobj(a) and np.isrealobj(b) else complex(out)
+
+
+def is_orthogonal(q, spec, tol=1e-10):
+    """linalg.py:62-72."""
+    q = np.asarray(q)
+    eye = identity_tensor(q.shape[0], q.shape[2:], spec)
+    qt = l_transpose(q, spec)
+    return fro(l_product(q, qt, spec) - eye) < tol and fro(l_product(qt, q, spec) - eye) < tol
+
+
 def singular_values(a, spec):
     """compute_uv=False path of linalg.py:137,157,164, (P, min(I1,I2)) in reference p-order."""
     return np.linalg.svd(to_stack(forward(np.asarray(a), spec)), compute_uv=False)

@@ -43,6 +43,7 @@ _SIGNATURES = {
     "ltb_ctx_last_error": ([_vp], C.c_char_p),
     "ltb_ctx_set_stream": ([_vp, _vp], _int),
     "ltb_ctx_synchronize": ([_vp], _int),
+    "ltb_ctx_make_current": ([_vp], _int),
     "ltb_ctx_launch_count": ([_vp], _i64),
     "ltb_ctx_stats": ([_vp, C.POINTER(_i64), _int], _int),
     "ltb_malloc": ([_vp, _i64, C.POINTER(_vp)], _int),
@@ -88,7 +89,6 @@ EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
 _lock = threading.RLock()
 _lib = None
-_ctx = None
 _device = 0
 
 
@@ -114,36 +114,51 @@ def load_library(path: Path | str | None = None):
 
 
 def set_device(device: int) -> None:
-    """Select the CUDA device used by subsequent calls (default 0)."""
-    global _device, _ctx
+    """Select the CUDA device used by subsequent calls (default 0).
+
+    Every device gets its own ltb_ctx, created on first use and kept for the life of
+    the process: buffers and spec handles stay bound to the context (and device) that
+    made them and are released through it, so switching devices never leaves a live
+    object pointing at a destroyed context."""
+    global _device
     with _lock:
-        if _ctx is not None and device != _device:
-            load_library().ltb_ctx_destroy(_ctx)
-            _ctx = None
         _device = int(device)
 
 
+_ctxs: dict = {}
+_tls = threading.local()
+
+
 def context():
-    """The process-wide ltb_ctx (created on first use)."""
-    global _ctx
+    """The ltb_ctx of the selected device (created on first use)."""
     with _lock:
-        if _ctx is None:
+        ctx = _ctxs.get(_device)
+        if ctx is None:
             lib = load_library()
             out = _vp()
             st = lib.ltb_ctx_create(_device, C.byref(out))
             if st != 0:
                 raise DeviceError(f"could not create a CUDA context on device {_device} (status {st}); "
                                   "a B200 is required — there is no CPU fallback")
-            _ctx = out
-        return _ctx
+            ctx = _ctxs[_device] = out
+        dev = _device
+    if getattr(_tls, "device", None) != dev:  # the CUDA current device is per host thread
+        load_library().ltb_ctx_make_current(ctx)
+        _tls.device = dev
+    return ctx
+
+
+def current_device() -> int:
+    return _device
 
 
 def check(status: int) -> None:
     if status == 0:
         return
     msg = ""
-    if _ctx is not None:
-        raw = load_library().ltb_ctx_last_error(_ctx)
+    ctx = _ctxs.get(_device)
+    if ctx is not None:
+        raw = load_library().ltb_ctx_last_error(ctx)
         msg = raw.decode() if raw else ""
     raise STATUS_TO_ERROR.get(status, DeviceError)(msg or f"libltb status {status}")
 
@@ -185,7 +200,7 @@ def real_of(dt) -> np.dtype:
 class DeviceArray:
     """A device buffer (ltb_malloc) with a numpy-like shape/dtype."""
 
-    __slots__ = ("ptr", "nbytes", "shape", "dtype", "_owner", "_base")
+    __slots__ = ("ptr", "nbytes", "shape", "dtype", "_owner", "_base", "_ctx")
 
     def __init__(self, shape, dtype, ptr=None, owner=True):
         self._base = None
@@ -193,9 +208,11 @@ class DeviceArray:
         self.dtype = np.dtype(dtype)
         self.nbytes = int(np.prod(self.shape, dtype=np.int64)) * self.dtype.itemsize
         self._owner = owner
+        self._ctx = None
         if ptr is None:
             out = _vp()
-            check(lib().ltb_malloc(context(), max(self.nbytes, 16), C.byref(out)))
+            self._ctx = context()
+            check(lib().ltb_malloc(self._ctx, max(self.nbytes, 16), C.byref(out)))
             self.ptr = out
         else:
             self.ptr = _vp(ptr) if not isinstance(ptr, _vp) else ptr
@@ -211,8 +228,8 @@ class DeviceArray:
 
     def __del__(self):
         try:
-            if self._owner and self.ptr and _lib is not None and _ctx is not None:
-                _lib.ltb_free(_ctx, self.ptr)
+            if self._owner and self.ptr and _lib is not None and self._ctx is not None:
+                _lib.ltb_free(self._ctx, self.ptr)
         except Exception:  # interpreter shutdown
             pass
 

@@ -53,15 +53,17 @@ class _ByteBuffer:
         data = np.ascontiguousarray(data, dtype=np.uint8)
         self.nbytes = int(data.nbytes)
         out = C.c_void_p()
-        nat.check(nat.lib().ltb_malloc(nat.context(), max(self.nbytes, 16), C.byref(out)))
+        self.ptr = None
+        self._ctx = nat.context()
+        nat.check(nat.lib().ltb_malloc(self._ctx, max(self.nbytes, 16), C.byref(out)))
         self.ptr = out
         if self.nbytes:
-            nat.check(nat.lib().ltb_memcpy_h2d(nat.context(), self.ptr, data.ctypes.data_as(C.c_void_p), self.nbytes))
+            nat.check(nat.lib().ltb_memcpy_h2d(self._ctx, self.ptr, data.ctypes.data_as(C.c_void_p), self.nbytes))
 
     def __del__(self):
         try:
-            if self.ptr and nat._lib is not None and nat._ctx is not None:
-                nat._lib.ltb_free(nat._ctx, self.ptr)
+            if self.ptr and nat._lib is not None:
+                nat._lib.ltb_free(self._ctx, self.ptr)
         except Exception:
             pass
 

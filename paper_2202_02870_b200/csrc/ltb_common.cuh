@@ -137,6 +137,9 @@ struct ltb_ctx {
   // pageable host copies: two pinned staging buffers and their DMA events (first use)
   void* h_stage[2] = {nullptr, nullptr};
   cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  // pinned staging of whole pageable operands (host-to-host l_product), grown on demand
+  void* h_big = nullptr;
+  size_t h_big_bytes = 0;
 };
 
 struct ltb_spec {
@@ -224,6 +227,14 @@ template <typename K> inline int ensure_smem(ltb_ctx* ctx, K kern, size_t smem, 
 }
 // cached cudaOccupancyMaxActiveBlocksPerMultiprocessor
 int ltb_occupancy(const void* kern, int threads, size_t smem);
+
+// host side of pageable copies (ltb_ctx.cu): pinned test, multi-threaded memcpy, and a
+// per-context pinned scratch buffer grown on demand
+extern "C" {
+bool ltb_is_pinned(const void* p);
+void ltb_host_copy(void* dst, const void* src, size_t n);
+int ltb_pinned_scratch(ltb_ctx* ctx, size_t bytes, void** out);
+}
 
 // stream-ordered scratch allocation
 int ltb_ws_alloc(ltb_ctx* ctx, size_t bytes, void** out);

@@ -130,6 +130,7 @@ void ltb_ctx_destroy(ltb_ctx* ctx) {
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
   if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
+  if (ctx->h_big) cudaFreeHost(ctx->h_big);
   for (int b = 0; b < 2; ++b) {
     if (ctx->h_stage[b]) cudaFreeHost(ctx->h_stage[b]);
     if (ctx->ev_stage[b]) cudaEventDestroy(ctx->ev_stage[b]);
@@ -141,6 +142,11 @@ const char* ltb_ctx_last_error(const ltb_ctx* ctx) { return ctx ? ctx->last_erro
 
 int ltb_ctx_set_stream(ltb_ctx* ctx, void* stream) {
   ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return LTB_OK;
+}
+
+int ltb_ctx_make_current(ltb_ctx* ctx) {
+  LTB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   return LTB_OK;
 }
 
@@ -170,7 +176,12 @@ int ltb_malloc(ltb_ctx* ctx, int64_t bytes, void** d_out) {
 }
 
 int ltb_free(ltb_ctx* ctx, void* d_ptr) {
+  // the buffer may belong to a context other than the calling thread's current device
+  int cur = ctx->device;
+  cudaGetDevice(&cur);
+  if (cur != ctx->device) cudaSetDevice(ctx->device);
   ltb_ws_free(ctx, d_ptr);
+  if (cur != ctx->device) cudaSetDevice(cur);
   return LTB_OK;
 }
 
@@ -265,6 +276,27 @@ CopyPool& copy_pool() {
   return *pool;
 }
 
+}  // namespace
+
+bool ltb_is_pinned(const void* p) { return is_pinned(p); }
+void ltb_host_copy(void* dst, const void* src, size_t n) { copy_pool().copy((char*)dst, (const char*)src, n); }
+
+int ltb_pinned_scratch(ltb_ctx* ctx, size_t bytes, void** out) {
+  if (bytes > ctx->h_big_bytes) {
+    if (ctx->h_big) {
+      LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+      cudaFreeHost(ctx->h_big);
+      ctx->h_big = nullptr;
+      ctx->h_big_bytes = 0;
+    }
+    LTB_CUDA_TRY(ctx, cudaHostAlloc(&ctx->h_big, bytes, cudaHostAllocDefault));
+    ctx->h_big_bytes = bytes;
+  }
+  *out = ctx->h_big;
+  return LTB_OK;
+}
+
+namespace {
 int ensure_stage(ltb_ctx* ctx) {
   for (int b = 0; b < 2; ++b) {
     if (!ctx->h_stage[b]) LTB_CUDA_TRY(ctx, cudaHostAlloc(&ctx->h_stage[b], kStageBytes, cudaHostAllocDefault));

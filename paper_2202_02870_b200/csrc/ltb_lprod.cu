@@ -7,8 +7,13 @@
 //   copy_in  : B, then A chunk 0, 1, ...                      (host -> device)
 //   compute  : K1(B); per chunk K1(A_c) -> K2 -> K1'(C_c)     (ctx->stream)
 //   copy_out : C chunk 0, 1, ...                              (device -> host)
-// With pinned host buffers the end-to-end time approaches max(in, out) + one
-// chunk; with pageable buffers the copies serialise but stay correct.
+// Pinned host buffers go straight to the DMA engines.  A pageable buffer (a
+// plain numpy array, what the drop-in receives) is staged through a pinned
+// per-context buffer: the host thread copies the next chunk in (8 threads)
+// while the DMA of the previous one runs, and copies C out chunk by chunk as
+// the device finishes it.  Every return path waits for both copy streams
+// before releasing the workspace, so no DMA touches caller memory after the
+// call returns, error or not.
 #include <algorithm>
 
 #include "ltb_dispatch.cuh"
@@ -36,6 +41,34 @@ struct EventPool {  // events of one call, destroyed on exit
 
 }  // namespace
 
+namespace {
+// Resources of one call.  The destructor runs on every return path: it waits for the
+// copy streams (they may still read the caller's A / B or write C) and only then
+// releases the stream-ordered workspace.
+struct HostCall {
+  ltb_ctx* ctx;
+  void* ws[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  EventPool pool;
+  explicit HostCall(ltb_ctx* c) : ctx(c) {}
+  ~HostCall() {
+    if (ctx->copy_in) cudaStreamSynchronize(ctx->copy_in);
+    if (ctx->copy_out) cudaStreamSynchronize(ctx->copy_out);
+    for (void* p : ws) ltb_ws_free(ctx, p);
+  }
+};
+
+// host -> device of [off, off + n) of one operand: straight from pinned memory, else a
+// multi-threaded copy into the pinned stage followed by the DMA from there
+int copy_in_range(ltb_ctx* ctx, char* d, const char* h, char* stage, size_t off, size_t n) {
+  if (stage) {
+    ltb_host_copy(stage + off, h + off, n);
+    h = stage;
+  }
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(d + off, h + off, n, cudaMemcpyHostToDevice, ctx->copy_in));
+  return LTB_OK;
+}
+}  // namespace
+
 int g_lprod_chunks = 8;  // maximum row chunks (test / tuning hook)
 extern "C" void ltb_debug_set_lprod_chunks(int v) { g_lprod_chunks = v < 1 ? 1 : v; }
 
@@ -48,29 +81,51 @@ extern "C" int ltb_l_product_host(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1
   const int64_t P = spec->P;
   if (I1 == 0 || I2 == 0 || P == 0) return LTB_OK;
   const size_t es = dtype == LTB_F32 ? 4 : 8;
+  const size_t bytes_a = es * I1 * L * P, bytes_b = es * L * I2 * P, bytes_c = es * I1 * I2 * P;
   LTB_TRY(ensure_copy_streams(ctx));
+  HostCall call(ctx);
+  // pageable operands: one pinned stage region each
+  const bool pin_a = ltb_is_pinned(h_a), pin_b = ltb_is_pinned(h_b), pin_c = ltb_is_pinned(h_c);
+  const size_t need = (pin_a ? 0 : bytes_a) + (pin_b ? 0 : bytes_b) + (pin_c ? 0 : bytes_c);
+  char *st_a = nullptr, *st_b = nullptr, *st_c = nullptr;
+  if (need) {
+    void* base = nullptr;
+    LTB_TRY(ltb_pinned_scratch(ctx, need, &base));
+    char* q = (char*)base;
+    if (!pin_a) st_a = q, q += bytes_a;
+    if (!pin_b) st_b = q, q += bytes_b;
+    if (!pin_c) st_c = q;
+  }
   // row chunks of A / C: up to 8, at least 32 rows each (the tensor-core GEMM tile side)
   const int64_t nch = std::max<int64_t>(1, std::min<int64_t>(g_lprod_chunks, I1 / 32));
   const int64_t rows = (I1 + nch - 1) / nch;
-  void *dA = nullptr, *dB = nullptr, *hA = nullptr, *hB = nullptr, *hC = nullptr, *dC = nullptr;
-  LTB_TRY(ltb_ws_alloc(ctx, es * I1 * L * P + 16, &dA));
-  LTB_TRY(ltb_ws_alloc(ctx, es * L * I2 * P + 16, &dB));
-  LTB_TRY(ltb_ws_alloc(ctx, es * I1 * L * P + 16, &hA));
-  LTB_TRY(ltb_ws_alloc(ctx, es * L * I2 * P + 16, &hB));
-  LTB_TRY(ltb_ws_alloc(ctx, es * I1 * I2 * P + 16, &hC));
-  LTB_TRY(ltb_ws_alloc(ctx, es * I1 * I2 * P + 16, &dC));
-  EventPool pool;
+  void *&dA = call.ws[0], *&dB = call.ws[1], *&hA = call.ws[2], *&hB = call.ws[3], *&hC = call.ws[4],
+       *&dC = call.ws[5];
+  LTB_TRY(ltb_ws_alloc(ctx, bytes_a + 16, &dA));
+  LTB_TRY(ltb_ws_alloc(ctx, bytes_b + 16, &dB));
+  LTB_TRY(ltb_ws_alloc(ctx, bytes_a + 16, &hA));
+  LTB_TRY(ltb_ws_alloc(ctx, bytes_b + 16, &hB));
+  LTB_TRY(ltb_ws_alloc(ctx, bytes_c + 16, &hC));
+  LTB_TRY(ltb_ws_alloc(ctx, bytes_c + 16, &dC));
+  EventPool& pool = call.pool;
   cudaEvent_t ready = pool.make();  // the stream-ordered allocations above are usable everywhere
   if (!ready) return ltb_set_error(ctx, LTB_ECUDA, "l_product: event creation failed");
   LTB_CUDA_TRY(ctx, cudaEventRecord(ready, ctx->stream));
   LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_in, ready, 0));
   LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_out, ready, 0));
-  // B in, K1(B)
+  // B in (in quarters when staged, so the host copy of one overlaps the DMA of the last), K1(B)
   cudaEvent_t eb = pool.make();
-  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(dB, h_b, es * L * I2 * P, cudaMemcpyHostToDevice, ctx->copy_in));
+  {
+    const int nb = st_b ? 4 : 1;
+    const size_t per = ((bytes_b + nb - 1) / nb + 4095) & ~size_t(4095);
+    for (size_t off = 0; off < bytes_b; off += per)
+      LTB_TRY(copy_in_range(ctx, (char*)dB, (const char*)h_b, st_b, off, std::min(per, bytes_b - off)));
+  }
   LTB_CUDA_TRY(ctx, cudaEventRecord(eb, ctx->copy_in));
   LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, eb, 0));
   LTB_TRY(ltb_transform_impl(ctx, spec, L * I2, 0, dtype, LTB_TUBE_MAJOR, dB, dtype, LTB_SLICE_MAJOR, hB, nullptr));
+  cudaEvent_t c_done[64];
+  int64_t issued = 0;
   for (int64_t c = 0; c < nch; ++c) {
     const int64_t r0 = c * rows, r = std::min(rows, I1 - r0);
     if (r <= 0) break;
@@ -80,8 +135,7 @@ extern "C" int ltb_l_product_host(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1
     char* ha_c = (char*)hA + es * r0 * L * P;  // chunk-major: chunk c's slice stack (P x r x L)
     char* hc_c = (char*)hC + es * r0 * I2 * P;
     char* c_c = (char*)dC + es * r0 * I2 * P;
-    LTB_CUDA_TRY(ctx, cudaMemcpyAsync(a_c, (const char*)h_a + es * r0 * L * P, es * r * L * P,
-                                      cudaMemcpyHostToDevice, ctx->copy_in));
+    LTB_TRY(copy_in_range(ctx, (char*)dA, (const char*)h_a, st_a, es * r0 * L * P, es * r * L * P));
     LTB_CUDA_TRY(ctx, cudaEventRecord(ea, ctx->copy_in));
     LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ea, 0));
     LTB_TRY(ltb_transform_impl(ctx, spec, r * L, 0, dtype, LTB_TUBE_MAJOR, a_c, dtype, LTB_SLICE_MAJOR, ha_c,
@@ -92,16 +146,30 @@ extern "C" int ltb_l_product_host(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1
                                nullptr));
     LTB_CUDA_TRY(ctx, cudaEventRecord(ec, ctx->stream));
     LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->copy_out, ec, 0));
-    LTB_CUDA_TRY(ctx, cudaMemcpyAsync((char*)h_c + es * r0 * I2 * P, c_c, es * r * I2 * P, cudaMemcpyDeviceToHost,
+    char* dst = st_c ? st_c : (char*)h_c;
+    LTB_CUDA_TRY(ctx, cudaMemcpyAsync(dst + es * r0 * I2 * P, c_c, es * r * I2 * P, cudaMemcpyDeviceToHost,
                                       ctx->copy_out));
+    if (st_c) {
+      c_done[c] = pool.make();
+      if (!c_done[c]) return ltb_set_error(ctx, LTB_ECUDA, "l_product: event creation failed");
+      LTB_CUDA_TRY(ctx, cudaEventRecord(c_done[c], ctx->copy_out));
+    }
+    issued = c + 1;
   }
-  // join the copy streams back into the compute stream, release, wait for the host copy
+  // staged C: copy each chunk out of the pinned stage as soon as its DMA lands
+  if (st_c) {
+    for (int64_t c = 0; c < issued; ++c) {
+      const int64_t r0 = c * rows, r = std::min(rows, I1 - r0);
+      LTB_CUDA_TRY(ctx, cudaEventSynchronize(c_done[c]));
+      ltb_host_copy((char*)h_c + es * r0 * I2 * P, st_c + es * r0 * I2 * P, es * r * I2 * P);
+    }
+  }
+  // join the copy streams back into the compute stream (the workspace is released behind them)
   cudaEvent_t done_in = pool.make(), done_out = pool.make();
   LTB_CUDA_TRY(ctx, cudaEventRecord(done_in, ctx->copy_in));
   LTB_CUDA_TRY(ctx, cudaEventRecord(done_out, ctx->copy_out));
   LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, done_in, 0));
   LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, done_out, 0));
-  for (void* p : {dA, dB, hA, hB, hC, dC}) ltb_ws_free(ctx, p);
   LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return LTB_OK;
 }

@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
+from .core import mode_n_product  # noqa: F401  (re-exported as in the reference module)
 from .errors import NumericConsistencyError, ParameterError, TransformError
 
 INV_TOL = 1e-10
@@ -256,7 +257,7 @@ def hermitian_rows(m: np.ndarray, tol: float = 1e-12) -> np.ndarray:
 def device_spec(spec: TransformSpec, trailing: tuple):
     """ltb_spec handle for tensors whose trailing dims are `trailing` (cached on the spec)."""
     trailing = tuple(int(d) for d in trailing)
-    key = trailing
+    key = (trailing, nat.current_device())  # a handle lives on the device (context) that made it
     cache = spec._device
     if key in cache:
         return cache[key]
@@ -314,11 +315,11 @@ _LAYOUT_SPECS: dict = {}
 
 def layout_spec(trailing: tuple):
     """Identity spec (no modes) used for pure layout changes (tube <-> slice major)."""
-    trailing = tuple(int(d) for d in trailing)
-    if trailing not in _LAYOUT_SPECS:
+    key = (tuple(int(d) for d in trailing), nat.current_device())
+    if key not in _LAYOUT_SPECS:
         z = np.zeros(1)
-        _LAYOUT_SPECS[trailing] = _create_spec(trailing, [], False, z, z)
-    return _LAYOUT_SPECS[trailing]
+        _LAYOUT_SPECS[key] = _create_spec(key[0], [], False, z, z)
+    return _LAYOUT_SPECS[key]
 
 
 def transform_device(x: nat.DeviceArray, handle, ntubes: int, inverse: bool, layout_in: int, out_dtype,

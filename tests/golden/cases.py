@@ -74,6 +74,10 @@ def svd_cases():
     c["s_rankdef"] = dict(kind="fft", x=x, tau=0.2)
     c["s_dct_f32"] = dict(kind="dct", x=r.standard_normal((8, 6, 2, 2, 3)).astype(np.float32), tau=0.5)
     c["s_fft_wide"] = dict(kind="fft", x=r.standard_normal((3, 7, 5)), tau=0.4)
+    # round 2: complex input, a wide 5th-order DCT, a tall fp32 slice stack
+    c["s_fft_cplx"] = dict(kind="fft", x=r.standard_normal((5, 4, 3)) + 1j * r.standard_normal((5, 4, 3)), tau=0.6)
+    c["s_dct5_wide"] = dict(kind="dct", x=r.standard_normal((4, 9, 2, 3, 2)), tau=0.5)
+    c["s_dct_f32_tall"] = dict(kind="dct", x=r.standard_normal((40, 24, 3, 4)).astype(np.float32), tau=0.8)
     for v in c.values():
         v["spec_shape"] = v["x"].shape
     return c
@@ -132,4 +136,34 @@ def btph_cases():
                            "b_cprod_tube": ((1, 1, 6), (1, 1, 6))}.items():
         c[name] = dict(kind="cprod", a=r.standard_normal(sa), b=r.standard_normal(sb),
                        spec_shape=(sa[0], sb[1]) + tuple(sa[2:]))
+    return c
+
+
+def algebra_cases():
+    """*_L algebra beyond the product (linalg.py:46-72,121-129; core.py:26-36,110-122)."""
+    r = np.random.default_rng(55)
+    c = {}
+    for kind, shape, k in (("dct", (6, 5, 3, 2), 2), ("fft", (5, 7, 4), 3), ("fft", (4, 4, 2, 3), 1)):
+        c[f"a_truncate_{kind}{len(shape)}_{k}"] = dict(kind=kind, x=r.standard_normal(shape), k=k, spec_shape=shape)
+    c["a_inner_real"] = dict(kind="dct", a=r.standard_normal((4, 3, 5)), b=r.standard_normal((4, 3, 5)),
+                             spec_shape=(4, 3, 5))
+    c["a_inner_cplx"] = dict(kind="dct", a=r.standard_normal((3, 2, 4)) + 1j * r.standard_normal((3, 2, 4)),
+                             b=r.standard_normal((3, 2, 4)) - 2j * r.standard_normal((3, 2, 4)),
+                             spec_shape=(3, 2, 4))
+    # orthogonal tensors: the u factor of a t-SVD under dct / fft
+    c["a_orth_dct"] = dict(kind="dct", x=r.standard_normal((5, 5, 3, 2)), spec_shape=(5, 5, 3, 2))
+    c["a_orth_fft"] = dict(kind="fft", x=r.standard_normal((4, 4, 6)), spec_shape=(4, 4, 6))
+    return c
+
+
+def mode_product_cases():
+    """mode_n_product on real shapes (core.py:110-122; the reference's test_core.py:103-119 recipes)."""
+    r = np.random.default_rng(66)
+    c = {}
+    x = r.standard_normal((4, 3, 5, 2))
+    for n in (1, 2, 3, 4):
+        c[f"n_mode{n}"] = dict(x=x, u=r.standard_normal((6, x.shape[n - 1])), n=n)
+    x = r.standard_normal((3, 4, 6))
+    c["n_cplx_u"] = dict(x=x, u=r.standard_normal((5, 6)) + 1j * r.standard_normal((5, 6)), n=3)
+    c["n_f32"] = dict(x=r.standard_normal((8, 7, 5)).astype(np.float32), u=r.standard_normal((3, 7)), n=2)
     return c

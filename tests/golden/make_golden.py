@@ -75,6 +75,8 @@ def main():
         out[f"{name}/x"] = case["x"]
         f = ref.t_svd(case["x"], spec)
         out[f"{name}/s"] = f.s
+        out[f"{name}/u"] = f.u
+        out[f"{name}/v"] = f.v
         out[f"{name}/tube_norms"] = f.tube_norms
         out[f"{name}/sv"] = np.linalg.svd(ref.core.as_rep_stack(ref.apply_l(case["x"], spec)), compute_uv=False)
         if spec.unitary_scaled:
@@ -104,6 +106,26 @@ def main():
         if case.get("gt") is not None:
             out[f"{name}/rse"] = np.array([r.rse for r in trace.records])
             out[f"{name}/psnr"] = np.array([r.psnr for r in trace.records])
+    for name, case in cases.algebra_cases().items():
+        spec = spec_of(case)
+        put_meta(out, name, case, **({"k": case["k"]} if "k" in case else {}))
+        if name.startswith("a_truncate"):
+            out[f"{name}/x"] = case["x"]
+            out[f"{name}/out"] = ref.truncate(ref.t_svd(case["x"], spec), case["k"])
+        elif name.startswith("a_inner"):
+            out[f"{name}/a"] = case["a"]
+            out[f"{name}/b"] = case["b"]
+            out[f"{name}/value"] = np.array(ref.inner_product(case["a"], case["b"]))
+        else:
+            q = ref.t_svd(case["x"], spec).u
+            out[f"{name}/q"] = q
+            out[f"{name}/orth"] = np.array(ref.is_orthogonal(q, spec))
+            out[f"{name}/nonorth"] = np.array(ref.is_orthogonal(case["x"], spec))
+    for name, case in cases.mode_product_cases().items():
+        out[f"{name}/x"] = case["x"]
+        out[f"{name}/u"] = case["u"]
+        out[f"{name}/n"] = np.array(case["n"])
+        out[f"{name}/out"] = ref.mode_n_product(case["x"], case["u"], case["n"])
     for name, (dims, sr, seed) in cases.mask_cases().items():
         out[f"{name}/meta"] = np.array(json.dumps({"dims": list(dims), "sr": sr, "seed": seed}))
         out[f"{name}/mask"] = ref.sample_mask(dims, sr, seed)

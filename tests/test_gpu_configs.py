@@ -1,6 +1,8 @@
 """BASELINE.json configurations at (or near) full size on the GPU, checked against the CPU
-oracle run here on the same seeded inputs (the oracle is the checker only), and through
-size-independent properties where the oracle would be too slow.  Tolerances (north_star):
+oracle run here on the same seeded inputs (the oracle is the checker only), against compact
+fixtures of the reference's own outputs where the host run is too slow for the test session
+(tests/golden/configs.npz, tests/golden/make_config_fixtures.py), and through size-independent
+properties.  Tolerances (north_star):
 1e-4 relative Frobenius for float32 work, 1e-10 for float64."""
 
 import numpy as np
@@ -9,10 +11,23 @@ import pytest
 import ltensor_oracle as O
 import paper_2202_02870_b200 as L
 from paper_2202_02870_b200 import core
-from conftest import rel_err
+from config_recipes import NSAMPLE, config3_inputs, config5_input, sample_index
+from ltb_testutil import ROOT, factor_parity, rel_err
+
+CONFIGS = ROOT / "tests" / "golden" / "configs.npz"
 
 pytestmark = pytest.mark.gpu
 
+
+def sha(x):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def cfx():
+    return np.load(CONFIGS)
 
 def cfg2_inputs():
     rng = np.random.default_rng(0)
@@ -164,3 +179,80 @@ def test_config3_recipe_long_run_fp32_carry():
     fin = np.isfinite(rr)
     np.testing.assert_array_equal(np.isfinite(rc), fin)  # x_next == 0 (inf) on the same iterations
     assert np.max(np.abs(rc[fin] - rr[fin]) / np.maximum(rr[fin], 1e-12)) < 1e-2
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+def test_config3_pga_200_iterations_vs_reference(cfx, precision, tol):
+    """The full config-3 run (144x176x3x100, 200 iterations, defaults, tol 1e-300) against the
+    reference's own trajectory (tests/golden/configs.npz, made by make_config_fixtures.py):
+    mu / t bit-exact, the per-iteration relative change, and the final iterate through its norm
+    and a seeded sample of 65,536 entries."""
+    m, mask = config3_inputs(O.l_product, O.ospec)
+    assert sha(m) == str(cfx["cfg3/m_sha"]) and sha(mask) == str(cfx["cfg3/mask_sha"])
+    spec = L.make_spec("dct", m.shape)
+    x, trace = L.pga_complete(m, mask, L.CompletionConfig(spec=spec, tol=1e-300, max_iters=200), precision=precision)
+    assert trace.iterations == 200
+    assert [r.mu for r in trace.records] == list(cfx["cfg3/mu"])
+    assert [r.t for r in trace.records] == list(cfx["cfg3/t"])
+    idx = sample_index(x.size, NSAMPLE, seed=3)
+    assert rel_err(x.ravel()[idx], cfx["cfg3/x_sample"]) < tol
+    assert abs(np.linalg.norm(x.ravel()) - float(cfx["cfg3/x_norm"])) < tol * float(cfx["cfg3/x_norm"])
+    rc = np.array([r.rel_change for r in trace.records])
+    rr = cfx["cfg3/rel"]
+    fin = np.isfinite(rr)
+    np.testing.assert_array_equal(np.isfinite(rc), fin)
+    np.testing.assert_allclose(rc[fin], rr[fin], rtol=1e-2 if precision == "fp32" else 1e-6)
+
+
+@pytest.mark.parametrize("n", [256, 512])
+def test_config5_vs_reference(cfx, n):
+    """Config 5 at n = 256 / 512 (512 slices, DCT over modes 3-5): svt at the reference's tau and
+    the transform-domain singular values against the reference (configs.npz)."""
+    key = f"cfg5_{n}"
+    a = config5_input(n)
+    assert sha(a) == str(cfx[f"{key}/a_sha"])
+    spec = L.make_spec("dct", a.shape)
+    tau = float(cfx[f"{key}/tau"])
+    out = L.svt(a, tau, spec)
+    assert out.dtype == np.float32
+    idx = sample_index(out.size, NSAMPLE, seed=n)
+    assert rel_err(out.ravel()[idx], cfx[f"{key}/svt_sample"]) < 1e-4
+    nrm = float(cfx[f"{key}/svt_norm"])
+    assert abs(float(np.linalg.norm(out.ravel().astype(np.float64))) - nrm) < 1e-4 * nrm
+    sv = L.linalg._singular_values(a, spec)[core.slice_order_permutation(a.shape[2:])]
+    assert rel_err(sv, cfx[f"{key}/sv"]) < 1e-4
+
+
+def test_config5_n256_tsvd_factors():
+    """t_svd at n = 256: S against the singular values and U, V up to sign against LAPACK's on
+    the same transform-domain stack (oracle, f64)."""
+    a = config5_input(256)
+    spec = L.make_spec("dct", a.shape)
+    ospec = O.ospec("dct", a.shape)
+    f = L.t_svd(a, spec)
+    uh, sv, vh = np.linalg.svd(O.to_stack(O.forward(a.astype(np.float64), ospec)), full_matrices=True)
+    for ours, ref in ((f.u, uh), (f.v, np.conj(np.swapaxes(vh, 1, 2)))):
+        err, count = factor_parity(O.to_stack(O.forward(ours.astype(np.float64), ospec)), ref, sv)
+        assert count > 0.8 * sv.size and err < 1e-4, (err, count)
+    diag = O.to_stack(O.forward(f.s.astype(np.float64), ospec))
+    assert rel_err(np.diagonal(diag, axis1=1, axis2=2), sv) < 1e-4
+
+
+def test_config4_reduced_pga_50_iterations():
+    """Config 4 recipe at 128 x 128 x 3 x 64 for the full 50 iterations:
+    explicit Q (x) F64, complex64 transform domain, Bernoulli(0.3), against the fp64 oracle."""
+    rng = np.random.default_rng(0)
+    q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    f = L.build_fourier_matrix(64)
+    a = rng.standard_normal((128, 20, 3, 64), dtype=np.float32)
+    b = rng.standard_normal((20, 128, 3, 64), dtype=np.float32)
+    spec = L.make_spec("explicit", (128, 128, 3, 64), matrices={3: q, 4: f})
+    ospec = O.ospec("explicit", (128, 128, 3, 64), matrices={3: q, 4: f})
+    m = O.l_product(a.astype(np.float64), b.astype(np.float64), ospec).astype(np.float32)
+    mask = rng.random(m.shape) < 0.3
+    x, trace = L.pga_complete(m, mask, L.CompletionConfig(spec=spec, tol=1e-300, max_iters=50))
+    # the oracle computes in float64 on the same (float32-valued) observations, as the reference would
+    ref, recs, _ = O.pga_complete(m.astype(np.float64), mask, ospec, tol=1e-300, max_iters=50)
+    assert trace.iterations == 50
+    assert [r.mu for r in trace.records] == [r[1] for r in recs]
+    assert rel_err(x, ref) < 1e-4

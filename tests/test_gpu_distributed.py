@@ -14,7 +14,7 @@ import torch.distributed as dist
 import paper_2202_02870_b200 as L
 from paper_2202_02870_b200.distributed import (DeviceEngine, DistLProductPlan, dist_l_product, dist_pga_complete,
                                                dist_svt)
-from conftest import rel_err
+from ltb_testutil import rel_err
 
 pytestmark = pytest.mark.gpu
 

@@ -9,7 +9,7 @@ import pytest
 
 import paper_2202_02870_b200 as L
 from paper_2202_02870_b200 import core
-from conftest import build_spec, case_names, meta, rel_err
+from ltb_testutil import build_spec, case_names, meta, rel_err
 
 pytestmark = pytest.mark.gpu
 

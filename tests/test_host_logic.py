@@ -18,7 +18,7 @@ from paper_2202_02870_b200.errors import (
     TransformError,
     UnsupportedSpecError,
 )
-from conftest import ROOT, case_names, meta, random_shape
+from ltb_testutil import ROOT, case_names, meta, random_shape
 
 
 # ----------------------------------------------------------------- C ABI surface
@@ -280,9 +280,39 @@ def test_public_names_match_reference_surface():
         "build_dct_matrix", "build_fourier_matrix", "make_spec", "LFactors", "RankReport", "identity_tensor",
         "is_orthogonal", "l_product", "l_transpose", "nuclear_norm", "ranks", "spectral_norm", "svt", "t_svd",
         "truncate", "CompletionConfig", "CompletionTrace", "pga_complete", "project_omega", "psnr", "rse",
-        "sample_mask",
+        "sample_mask", "export_ppm_dir", "import_ppm_dir", "read_container", "write_container",
     }
     assert expected <= set(L.__all__)
+
+
+REF_SRC = Path("/root/reference/pkg/src/ltensor")
+SUBMODULES = ("core", "transforms", "linalg", "completion", "errors", "io", "cli")
+
+
+def _public_defs(path: Path, imports: bool = False) -> set:
+    """Top-level public functions / classes (and relative imports) of a module, by AST (no import)."""
+    import ast
+
+    names = set()
+    for node in ast.parse(path.read_text()).body:
+        if isinstance(node, (ast.FunctionDef, ast.ClassDef)):
+            names.add(node.name)
+        elif imports and isinstance(node, ast.ImportFrom) and node.level == 1:
+            names.update(a.asname or a.name for a in node.names)
+    return {n for n in names if not n.startswith("_")}
+
+
+@pytest.mark.skipif(not REF_SRC.is_dir(), reason="reference tree not present (GPU box)")
+def test_public_names_cover_reference_modules():
+    """Every public name of the reference package and of each of its modules the
+    drop-in replaces exists under the same module here (pkg/src/ltensor/__init__.py:3-45)."""
+    import importlib
+
+    assert _public_defs(REF_SRC / "__init__.py", imports=True) <= set(dir(L))
+    for mod in SUBMODULES:
+        ours = importlib.import_module(f"paper_2202_02870_b200.{mod}")
+        missing = _public_defs(REF_SRC / f"{mod}.py") - set(dir(ours))
+        assert not missing, f"{mod}: {sorted(missing)}"
 
 
 def test_no_oracle_in_product_package():

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import ltensor_oracle as O
-from conftest import build_spec, case_names, meta, rel_err
+from ltb_testutil import build_spec, case_names, meta, rel_err
 
 
 @pytest.mark.parametrize("name", case_names("t_"))
@@ -86,3 +86,34 @@ def test_oracle_cprod_equals_btph(golden, name):
     spec = build_spec(O, golden, name)
     c = O.l_product(golden[f"{name}/a"], golden[f"{name}/b"], spec)
     assert rel_err(c, golden[f"{name}/c"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", case_names("s_"))
+def test_svd_factors(golden, name):
+    """The oracle's t_svd factors are the reference's (same LAPACK call on the same stack)."""
+    spec = build_spec(O, golden, name)
+    x = golden[f"{name}/x"]
+    u, s, v, _ = O.t_svd(x, spec)
+    tol = 1e-6 if x.dtype == np.float32 else 1e-12
+    assert rel_err(u, golden[f"{name}/u"]) < tol and rel_err(v, golden[f"{name}/v"]) < tol
+
+
+@pytest.mark.parametrize("name", case_names("a_"))
+def test_algebra(golden, name):
+    spec = build_spec(O, golden, name)
+    if name.startswith("a_truncate"):
+        u, s, v, _ = O.t_svd(golden[f"{name}/x"], spec)
+        out = O.truncate(u, s, v, meta(golden, name)["k"], spec)
+        assert rel_err(out, golden[f"{name}/out"]) < 1e-12
+    elif name.startswith("a_inner"):
+        assert O.inner_product(golden[f"{name}/a"], golden[f"{name}/b"]) == golden[f"{name}/value"][()]
+    else:
+        assert O.is_orthogonal(golden[f"{name}/q"], spec) == bool(golden[f"{name}/orth"])
+        assert bool(golden[f"{name}/orth"]) and not bool(golden[f"{name}/nonorth"])
+
+
+@pytest.mark.parametrize("name", case_names("n_"))
+def test_mode_products(golden, name):
+    out = O.mode_product(golden[f"{name}/x"], golden[f"{name}/u"], int(golden[f"{name}/n"]))
+    assert out.dtype == golden[f"{name}/out"].dtype
+    np.testing.assert_array_equal(out, golden[f"{name}/out"])

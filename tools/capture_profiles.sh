@@ -8,23 +8,23 @@ python bench.py > gpurun_out/prof/${R}_bench.json 2> gpurun_out/prof/${R}_bench.
 python bench.py --steps 3 --warmup 3 --skip-extras --no-cpu-baseline --pga-iters 60 > /dev/null 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/${R}_launches.csv \
     python bench.py --steps 3 --warmup 3 --skip-extras --no-cpu-baseline --pga-iters 60 > /dev/null 2>&1
-python tools/pdl_ab.py > /dev/null 2>&1 && \
+python tools/experiments/pdl_ab.py > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:tc3_kernel -c 3 -o gpurun_out/prof/${R}_tc3 \
-    python tools/pdl_ab.py > /dev/null 2>&1
-python tools/prof_pga_late.py 120 2 > /dev/null 2>&1 && \
+    python tools/experiments/pdl_ab.py > /dev/null 2>&1
+python tools/experiments/prof_pga_late.py 120 2 > /dev/null 2>&1 && \
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:jacobi_qr_kernel -c 1 \
-    -o gpurun_out/prof/${R}_jacobi_qr python tools/prof_pga_late.py 120 2 > /dev/null 2>&1
+    -o gpurun_out/prof/${R}_jacobi_qr python tools/experiments/prof_pga_late.py 120 2 > /dev/null 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:xform_tile_kernel -c 2 \
-    -o gpurun_out/prof/${R}_xform_pga python tools/prof_pga_late.py 120 2 > /dev/null 2>&1
-python tools/svd_blocked_prof.py 1024 > /dev/null 2>&1 && \
+    -o gpurun_out/prof/${R}_xform_pga python tools/experiments/prof_pga_late.py 120 2 > /dev/null 2>&1
+python tools/experiments/svd_blocked_prof.py 1024 > /dev/null 2>&1 && \
 ncu --set full --clock-control none -k regex:jacobi_block_kernel -s 20 -c 1 -o gpurun_out/prof/${R}_jacobi_block \
-    python tools/svd_blocked_prof.py 1024 > /dev/null 2>&1
-python tools/pga_kernel_breakdown.py 120 5 > gpurun_out/prof/${R}_pga_breakdown.txt 2>&1
+    python tools/experiments/svd_blocked_prof.py 1024 > /dev/null 2>&1
+python tools/experiments/pga_kernel_breakdown.py 120 5 > gpurun_out/prof/${R}_pga_breakdown.txt 2>&1
 ls -la gpurun_out/prof
 # summaries on the box (the .ncu-rep files together exceed what gpurun copies back): markdown,
 # raw CSV per report, then drop the reports themselves
 P=gpurun_out/prof
-python tools/ncu_summary.py $P/${R}_ncu_summary.md \
+python tools/experiments/ncu_summary.py $P/${R}_ncu_summary.md \
     $P/${R}_tc3.ncu-rep:"config-2 l_product tcgen05 kernels (paired forward K1, slice GEMM K2, inverse K1')" \
     $P/${R}_jacobi_qr.ncu-rep:"config-3 PGA K3 (Cholesky-preconditioned Jacobi, warm iteration 121)" \
     $P/${R}_xform_pga.ncu-rep:"config-3 PGA fused transforms (K1 + K4 prologue, K1' + norms epilogue)" \
