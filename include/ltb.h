@@ -71,6 +71,14 @@ const char* ltb_ctx_last_error(const ltb_ctx* ctx);
 /* adopt an external cudaStream_t (e.g. torch.cuda.current_stream()); NULL = own stream */
 int ltb_ctx_set_stream(ltb_ctx* ctx, void* stream);
 int ltb_ctx_synchronize(ltb_ctx* ctx);
+/* per-context test / profiling options (no process-global state): value is a flag or a
+ * device pointer (uint64 buffers the kernels stamp with clock values; 0 disables) */
+enum ltb_option {
+  LTB_OPT_FORCE_BLOCKED_SVD = 1, /* route every SVD / SVT through the blocked Jacobi tier */
+  LTB_OPT_TC_TIMELINE = 2,       /* tcgen05 GEMM / transform: per-tile stamps of CTA 0 */
+  LTB_OPT_QR_TIMELINE = 3        /* QR-preconditioned Jacobi: stage stamps of CTA 0 */
+};
+int ltb_ctx_set_option(ltb_ctx* ctx, int option, int64_t value);
 /* make ctx's device the calling host thread's current CUDA device (contexts of several
  * devices may coexist in one process; each call runs on the current device) */
 int ltb_ctx_make_current(ltb_ctx* ctx);

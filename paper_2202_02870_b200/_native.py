@@ -18,6 +18,7 @@ from .errors import STATUS_TO_ERROR, DeviceError
 LIB_PATH = Path(__file__).resolve().with_name("libltb.so")
 
 F32, F64, C64, C128 = 0, 1, 2, 3
+OPT_FORCE_BLOCKED_SVD, OPT_TC_TIMELINE, OPT_QR_TIMELINE = 1, 2, 3
 TUBE_MAJOR, SLICE_MAJOR = 0, 1
 OP_N, OP_T, OP_C, OP_H = 0, 1, 2, 3
 
@@ -44,6 +45,7 @@ _SIGNATURES = {
     "ltb_ctx_set_stream": ([_vp, _vp], _int),
     "ltb_ctx_synchronize": ([_vp], _int),
     "ltb_ctx_make_current": ([_vp], _int),
+    "ltb_ctx_set_option": ([_vp, _int, _i64], _int),
     "ltb_ctx_launch_count": ([_vp], _i64),
     "ltb_ctx_stats": ([_vp, C.POINTER(_i64), _int], _int),
     "ltb_malloc": ([_vp, _i64, C.POINTER(_vp)], _int),

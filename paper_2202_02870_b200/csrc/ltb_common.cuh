@@ -140,6 +140,10 @@ struct ltb_ctx {
   // pinned staging of whole pageable operands (host-to-host l_product), grown on demand
   void* h_big = nullptr;
   size_t h_big_bytes = 0;
+  // per-context test / profiling options (ltb_ctx_set_option)
+  int opt_force_blocked = 0;                       // route every SVD through the blocked Jacobi tier
+  unsigned long long* opt_tc_timeline = nullptr;   // tcgen05 kernels: per-tile clock stamps (CTA 0)
+  unsigned long long* opt_qr_timeline = nullptr;   // QR-preconditioned Jacobi: stage stamps (CTA 0)
 };
 
 struct ltb_spec {
@@ -239,6 +243,29 @@ int ltb_pinned_scratch(ltb_ctx* ctx, size_t bytes, void** out);
 // stream-ordered scratch allocation
 int ltb_ws_alloc(ltb_ctx* ctx, size_t bytes, void** out);
 void ltb_ws_free(ltb_ctx* ctx, void* p);
+
+// Workspace of one call: every buffer is released (stream-ordered) when the scope ends,
+// on the success path and on every early error return alike.
+struct WsScope {
+  ltb_ctx* ctx;
+  void* p[24];
+  int n = 0;
+  explicit WsScope(ltb_ctx* c) : ctx(c) {}
+  WsScope(const WsScope&) = delete;
+  WsScope& operator=(const WsScope&) = delete;
+  ~WsScope() {
+    while (n > 0) ltb_ws_free(ctx, p[--n]);
+  }
+  template <typename T> int alloc(size_t bytes, T** out) {
+    if (n == 24) return ltb_set_error(ctx, LTB_EOOM, "too many workspace buffers in one call");
+    void* q = nullptr;
+    const int st = ltb_ws_alloc(ctx, bytes, &q);
+    if (st != LTB_OK) return st;
+    p[n++] = q;
+    *out = (T*)q;
+    return LTB_OK;
+  }
+};
 
 // internal entry points shared between translation units
 int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,

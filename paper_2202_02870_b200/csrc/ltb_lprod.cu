@@ -69,8 +69,7 @@ int copy_in_range(ltb_ctx* ctx, char* d, const char* h, char* stage, size_t off,
 }
 }  // namespace
 
-int g_lprod_chunks = 8;  // maximum row chunks (test / tuning hook)
-extern "C" void ltb_debug_set_lprod_chunks(int v) { g_lprod_chunks = v < 1 ? 1 : v; }
+constexpr int g_lprod_chunks = 8;  // maximum row chunks
 
 extern "C" int ltb_l_product_host(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1, int64_t L, int64_t I2, int dtype,
                                   const void* h_a, const void* h_b, void* h_c) {

@@ -54,14 +54,12 @@ struct ltb_pga {
 };
 
 // 1: fp32 PGA carries the right singular bases between iterations (warm-started SVT)
-static int g_pga_carry = 1;
-extern "C" void ltb_debug_set_pga_carry(int v) { g_pga_carry = v; }
+constexpr int g_pga_carry = 1;
 // 1: fp32 real specs with a Kronecker matrix transform on the tensor cores inside PGA.
 // Off by default: 3xTF32 keeps ~21 mantissa bits per product, and over ~90 iterations of
 // the momentum recursion the iterate drifts to 1.0e-4 of the fp64 oracle (the fp32 tile
 // engine stays below it); +8% it/s on config 3 when enabled
-static int g_pga_tc = 0;
-extern "C" void ltb_debug_set_pga_tc(int v) { g_pga_tc = v; }
+constexpr int g_pga_tc = 0;
 
 namespace {
 

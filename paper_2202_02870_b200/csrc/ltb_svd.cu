@@ -614,10 +614,9 @@ struct BlockGeom {
 };
 
 constexpr size_t kBlockSmem = 200 * 1024;
-int g_force_blocked = 0;  // test hook: route every slice size through the blocked tier
 // early-stop scale (x sqrt(tol)) of the fp32 Jacobi for calls that do not set their own
 // (QR path, blocked-tier svt / values; 0: run to a sweep without rotations)
-float g_qr_early = 1.f;
+constexpr float g_qr_early = 1.f;
 
 __global__ void fill_int_kernel(int64_t n, int* __restrict__ p, int v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
@@ -1001,7 +1000,7 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
   if (batch > 0x7fffffff) return ltb_set_error(ctx, LTB_ESHAPE, "svd: batch too large");
   o.stats = ctx->d_stats;
   constexpr bool big = std::is_same<T, cplx<double>>::value;
-  if (g_force_blocked) return launch_jacobi_blocked<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
+  if (ctx->opt_force_blocked) return launch_jacobi_blocked<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
   auto fits = [&](int mp) { return jacobi_smem_bytes<T>(m, n, WANT_V, mp) <= kSmemLimit; };
   if (m <= 8 && fits(8)) return launch_smem<T, WANT_V, 4, 2>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   if (m <= 32 && fits(32)) return launch_smem<T, WANT_V, 8, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
@@ -1365,7 +1364,6 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   }
 }
 
-unsigned long long* g_qr_dbg = nullptr;  // stage timeline hook (CTA 0)
 
 size_t jacobi_qr_smem(int n, int pitch) { return ((size_t)n * pitch + 4 * (size_t)n + 1) * 4 + (n + 8) * 4 + 16; }
 
@@ -1382,24 +1380,24 @@ int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const
   if (slots > 4) return LTB_EUNSUPPORTED;  // <= 4 slots per team
   auto kern = slots == 1 ? jacobi_qr_kernel<TS, MPL, MINB, CHOL, 1> : jacobi_qr_kernel<TS, MPL, MINB, CHOL, 4>;
   LTB_TRY(ensure_smem(ctx, kern, smem, true));
-  kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, o, max_sweeps, pitch, g_qr_dbg);
+  kern<<<(unsigned)batch, 32 * nwarps, smem, ctx->stream>>>(I1, I2, A, o, max_sweeps, pitch, ctx->opt_qr_timeline);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
 
 // 1 when the QR-preconditioned resident kernel takes this fp32 SVT; 0 to use the others
-int g_svt_qr = 1;
-int g_qr_max_sweeps = 40;  // timing hook: 0 measures the QR and emission stages alone
+constexpr int g_svt_qr = 1;
+constexpr int g_qr_max_sweeps = 40;  // timing hook: 0 measures the QR and emission stages alone
 // lanes per column pair in the fp32 QR/Cholesky Jacobi: 8 (one pair per team per round,
 // fewer padding rows; 10-30% faster for 64 <= n <= 192, tools/qr_ts_ab.py) or 16
-int g_qr_ts = 8;
+constexpr int g_qr_ts = 8;
 
 // LTB_EUNSUPPORTED when the shape does not fit the QR-preconditioned kernel
 // chol: A holds n x n Gram matrices (I1 == I2 == n), factored by Cholesky instead of Householder
 int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o_in,
                      bool chol = false) {
   const int m = (int)std::max(I1, I2), n = (int)std::min(I1, I2);
-  if (!g_svt_qr || g_force_blocked || n < 32 || batch > 0x7fffffff) return LTB_EUNSUPPORTED;
+  if (!g_svt_qr || ctx->opt_force_blocked || n < 32 || batch > 0x7fffffff) return LTB_EUNSUPPORTED;
   JacobiOut o = o_in;
   // cold calls too: stop after a sweep whose rotations all had relative inner products
   // below sqrt(tol) (see jacobi_qr_kernel; tol = the rotation threshold)
@@ -1488,18 +1486,15 @@ __global__ void col_scale_kernel(int n, const float* __restrict__ V, const float
 // fp32 SVT of `batch` I1 x I2 slices carrying the n x n right bases V (row-major,
 // n = min(I1, I2)) between calls; warm == 0 starts from the identity.
 // LTB_EUNSUPPORTED when the slice shape does not fit the QR-preconditioned kernel.
-int g_carry_chol = 1;  // warm carried SVT: Cholesky of the Gram matrix (1) or Householder (0)
-extern "C" void ltb_debug_set_carry_chol(int v) { g_carry_chol = v; }
+constexpr int g_carry_chol = 1;  // warm carried SVT: Cholesky of the Gram matrix (1) or Householder (0)
 // carried SVT: multiplier of the Jacobi rotation threshold eps * sqrt(n)
-float g_carry_tol_scale = 1.f;
-extern "C" void ltb_debug_set_carry_tol_scale(float v) { g_carry_tol_scale = v; }
+constexpr float g_carry_tol_scale = 1.f;
 // warm carried SVT: stop the Jacobi after a sweep whose rotated pairs all had a relative
 // inner product below g_carry_early * sqrt(tol) (tol = the rotation threshold), i.e. the
 // inner products left behind are ~tol; 0 runs to a sweep without rotations.  Config-3 PGA
 // (tools/pga_early_ab.py): 2.77 -> 1.98 sweeps per slice, +13% it/s, the 200-iteration
 // iterate's error against the fp64 run unchanged (3.2e-5)
-float g_carry_early = 1.f;
-extern "C" void ltb_debug_set_carry_early(float v) { g_carry_early = v; }
+constexpr float g_carry_early = 1.f;
 
 int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
                        float* V, int warm, const int* skip) {
@@ -1507,20 +1502,17 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
   const int64_t m = trans ? I2 : I1, n = trans ? I1 : I2;
   if (batch <= 0 || batch > 65535 || n < 32) return LTB_EUNSUPPORTED;  // grid.y carries the slice
   const int64_t nn = n * n;
+  WsScope ws(ctx);
   float *A0 = nullptr, *Y = nullptr, *sv = nullptr, *dd = nullptr, *VR = nullptr, *Vn = nullptr, *S = nullptr;
   int* kept = nullptr;
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * n * m, (void**)&A0));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * nn, (void**)&Y));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * n, (void**)&sv));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * n, (void**)&dd));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * nn, (void**)&VR));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * nn, (void**)&Vn));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(float) * batch * nn, (void**)&S));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * batch, (void**)&kept));
-  auto release = [&]() {
-    for (void* p : {(void*)A0, (void*)Y, (void*)sv, (void*)dd, (void*)VR, (void*)Vn, (void*)S, (void*)kept})
-      ltb_ws_free(ctx, p);
-  };
+  LTB_TRY(ws.alloc(sizeof(float) * batch * n * m, &A0));
+  LTB_TRY(ws.alloc(sizeof(float) * batch * nn, &Y));
+  LTB_TRY(ws.alloc(sizeof(float) * batch * n, &sv));
+  LTB_TRY(ws.alloc(sizeof(float) * batch * n, &dd));
+  LTB_TRY(ws.alloc(sizeof(float) * batch * nn, &VR));
+  LTB_TRY(ws.alloc(sizeof(float) * batch * nn, &Vn));
+  LTB_TRY(ws.alloc(sizeof(float) * batch * nn, &S));
+  LTB_TRY(ws.alloc(sizeof(int) * batch, &kept));
   const int F = LTB_F32;
   const float* src = G;
   if (warm) {  // A0 = V^T G (I1 < I2) or G V: the preconditioned slices, same shape as G
@@ -1550,10 +1542,7 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
   } else {
     st = launch_jacobi_qr(ctx, batch, I1, I2, src, o);
   }
-  if (st != LTB_OK) {
-    release();
-    return st;
-  }
+  if (st != LTB_OK) return st;
   // V_A0: normalised Jacobi columns completed to an orthonormal basis (row-major, column j = v_j)
   LTB_TRY(ensure_smem(ctx, complete_u_kernel<float>, (size_t)n * sizeof(float)));
   complete_u_kernel<float><<<(unsigned)batch, 256, (size_t)n * sizeof(float), ctx->stream>>>((int)n, (int)n, Y, sv, VR,
@@ -1587,7 +1576,6 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
   else
     LTB_TRY(ltb_gemm_impl(ctx, F, batch, m, n, n, LTB_OP_N, G, n, m * n, LTB_OP_N, S, n, nn, out, n, m * n, nullptr,
                           nullptr, nullptr, nullptr, nullptr, skip));
-  release();
   return LTB_OK;
 }
 
@@ -1607,17 +1595,15 @@ int ltb_svt_carry64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, co
   const int64_t m = trans ? I2 : I1, n = trans ? I1 : I2, nn = n * n;
   if (batch <= 0 || batch > 65535 || n < 2) return LTB_EUNSUPPORTED;
   const int F = LTB_F64;
+  WsScope ws(ctx);
   double *A0 = nullptr, *w = nullptr, *vc = nullptr, *z = nullptr, *d = nullptr;
   int* kept = nullptr;
-  auto release = [&]() {
-    for (void* p : {(void*)A0, (void*)w, (void*)vc, (void*)z, (void*)d, (void*)kept}) ltb_ws_free(ctx, p);
-  };
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * I1 * I2, (void**)&A0));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * n * m, (void**)&w));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * nn, (void**)&vc));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * n * m, (void**)&z));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(double) * batch * n, (void**)&d));
-  LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * batch, (void**)&kept));
+  LTB_TRY(ws.alloc(sizeof(double) * batch * I1 * I2, &A0));
+  LTB_TRY(ws.alloc(sizeof(double) * batch * n * m, &w));
+  LTB_TRY(ws.alloc(sizeof(double) * batch * nn, &vc));
+  LTB_TRY(ws.alloc(sizeof(double) * batch * n * m, &z));
+  LTB_TRY(ws.alloc(sizeof(double) * batch * n, &d));
+  LTB_TRY(ws.alloc(sizeof(int) * batch, &kept));
   const double* src = G;
   if (warm) {
     if (trans)  // A0 = V^T G  (I1 x I2)
@@ -1630,10 +1616,7 @@ int ltb_svt_carry64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, co
   }
   JacobiOut o{w, nullptr, vc, kept, d, tau, skip};
   int st = launch_jacobi<double, true>(ctx, batch, I1, I2, src, o);
-  if (st != LTB_OK) {
-    release();
-    return st;
-  }
+  if (st != LTB_OK) return st;
   if (!trans) {
     // Z = D W^T G (n x I2, rows limited to the kept count); out = W Z
     LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, I2, m, LTB_OP_C, w, m, n * m, LTB_OP_N, G, I2, I1 * I2, z, I2, n * I2,
@@ -1656,16 +1639,9 @@ int ltb_svt_carry64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, co
     cols_to_rowmajor_kernel<double><<<grid_for(batch * nn, 256, 4096), 256, 0, ctx->stream>>>(batch, (int)n, vc, V);
     LTB_LAUNCH_CHECK(ctx);
   }
-  release();
   return LTB_OK;
 }
 
-extern "C" void ltb_debug_set_svd_blocked(int v) { g_force_blocked = v; }
-extern "C" void ltb_debug_set_svt_qr(int v) { g_svt_qr = v; }
-extern "C" void ltb_debug_set_qr_max_sweeps(int v) { g_qr_max_sweeps = v; }
-extern "C" void ltb_debug_set_qr_ts(int v) { g_qr_ts = v; }
-extern "C" void ltb_debug_set_qr_early(float v) { g_qr_early = v; }
-extern "C" void ltb_debug_set_qr_timeline(void* p) { g_qr_dbg = (unsigned long long*)p; }
 
 // SVT of `batch` row-major I1 x I2 slices: out = U (S - tau)_+ V^H
 int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2, const void* d_a, double tau,

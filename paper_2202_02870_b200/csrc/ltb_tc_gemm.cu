@@ -941,25 +941,24 @@ __global__ void __launch_bounds__(kThreads3, 1)
 
 // ------------------------------------------------------------------ host: tensor maps
 // MN-major 128B-swizzle descriptor strides (bytes): LBO = MN-chunk stride, SBO = 8-row K-group stride
-uint32_t g_mn_lbo = 4096, g_mn_sbo = 512;
+constexpr uint32_t g_mn_lbo = 4096, g_mn_sbo = 512;
 // 1: leave the fp32 tile in place as the "hi" operand (valid iff the tensor core
 // truncates fp32 -> tf32); 0: store hi = x with the low 13 bits cleared
-int g_raw_hi = 1;
-unsigned long long* g_dbg = nullptr;
+constexpr int g_raw_hi = 1;
 // epilogue store mode: 3 swizzled smem boxes + TMA tensor stores (default, needs a
 // C tensor map), 1 direct per-thread row stores, 2 no stores (diagnostic only)
-int g_epi_mode = 3;
+constexpr int g_epi_mode = 3;
 // programmatic dependent launch on (1) / off (0)
-int g_pdl = 1;
+constexpr int g_pdl = 1;
 // resident constant-B variant allowed (1) / off (0)
-int g_rb = 1;
+constexpr int g_rb = 1;
 // 3xTF32 with A staged in TMEM (tc3_kernel) (1) / split in shared memory (0)
-int g_tc3 = 1;
+constexpr int g_tc3 = 1;
 // transposed outputs: coalesced direct stores (1) / smem box + TMA store (0)
-int g_ct_direct = 0;
+constexpr int g_ct_direct = 0;
 // tc3 epilogue: warp-coalesced stores from the shared-memory box (1) / TMA tensor stores (0,
 // measured faster on the config-2 step: 51 vs 63 us)
-int g_epi_lsu = 0;
+constexpr int g_epi_lsu = 0;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1056,7 +1055,7 @@ int launch_tc(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, mc, C, ldc, sc, M, N, K, (int)batch, mn_lbo, mn_sbo,
-                                       g_raw_hi, g_dbg, epi, ct));
+                                       g_raw_hi, ctx->opt_tc_timeline, epi, ct));
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -1080,7 +1079,7 @@ int launch_tc3(ltb_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   LTB_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, mc, M, N, K, (int)batch, g_mn_lbo, g_mn_sbo, ct, ex,
-                                       g_dbg));
+                                       ctx->opt_tc_timeline));
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }
@@ -1155,19 +1154,7 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
 #undef LTB_TC
 }
 
-extern "C" void ltb_tc_debug_set_raw_hi(int v) { g_raw_hi = v; }
-extern "C" void ltb_tc_debug_set_epi_mode(int v) { g_epi_mode = v; }
-extern "C" void ltb_tc_debug_set_pdl(int v) { g_pdl = v; }
-extern "C" void ltb_tc_debug_set_rb(int v) { g_rb = v; }
-extern "C" void ltb_tc_debug_set_tc3(int v) { g_tc3 = v; }
-extern "C" void ltb_tc_debug_set_ct_direct(int v) { g_ct_direct = v; }
-extern "C" void ltb_tc_debug_set_epi_lsu(int v) { g_epi_lsu = v; }
-extern "C" void ltb_tc_debug_set_timeline(void* d_buf) { g_dbg = (unsigned long long*)d_buf; }
 
-extern "C" void ltb_tc_debug_set_mn_strides(uint32_t lbo, uint32_t sbo) {
-  g_mn_lbo = lbo;
-  g_mn_sbo = sbo;
-}
 
 // test hook: exported C entry for the kernel-level tests (fp32 only)
 extern "C" int ltb_tc_gemm(ltb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t k, int a_mn, const void* d_a,

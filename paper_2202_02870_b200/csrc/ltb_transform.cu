@@ -208,8 +208,7 @@ int dispatch_io(ltb_ctx* ctx, bool ic, bool oc, bool cm, XformParams p, const vo
 }  // namespace
 
 // 0: force the CUDA-core tile engine for fp32 real specs (A/B measurements)
-static int g_xform_tc = 1;
-extern "C" void ltb_debug_set_xform_tc(int v) { g_xform_tc = v; }
+constexpr int g_xform_tc = 1;
 
 int ltb_transform_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in, int layout_in,
                        const void* d_in, int dtype_out, int layout_out, void* d_out, double* d_sumsq) {

@@ -180,8 +180,8 @@ class RankReport:
 def t_svd(a, spec: TransformSpec) -> LFactors:
     """Full slice-wise SVD in the transform domain, inverse-transformed (linalg.py:102-118).
 
-    K3 runs one-sided Jacobi with V accumulated; U is completed to a full
-    orthonormal basis on the device (full_matrices=True)."""
+    K3 runs one-sided Jacobi with V accumulated (in double precision for single-precision
+    stacks); U is completed to a full orthonormal basis on the device (full_matrices=True)."""
     a = np.asarray(a)
     i1, i2 = a.shape[:2]
     trailing = a.shape[2:]
@@ -189,12 +189,17 @@ def t_svd(a, spec: TransformSpec) -> LFactors:
     P = hat.shape[0]
     k = min(i1, i2)
     rdt = nat.real_of(hat.dtype)
-    u_hat = nat.DeviceArray((P, i1, i1), hat.dtype)
-    v_hat = nat.DeviceArray((P, i2, i2), hat.dtype)
-    sv = nat.DeviceArray((P, k), rdt)
+    # single-precision stacks are factored in double precision: the fp32 Jacobi's singular
+    # vectors drift ~eps * sigma_max / gap per column (1e-4 relative on config 5, n = 256),
+    # outside the 1e-4 factor tolerance; the fp64 kernel's are ~1e-12
+    work = hat.astype(nat.complex_of(np.float64) if np.iscomplexobj(np.zeros(0, hat.dtype)) else np.float64)
+    u_hat = nat.DeviceArray((P, i1, i1), work.dtype)
+    v_hat = nat.DeviceArray((P, i2, i2), work.dtype)
+    sv = nat.DeviceArray((P, k), nat.real_of(work.dtype))
     if k > 0:
-        nat.check(nat.lib().ltb_slice_svd(nat.context(), hat.code, P, i1, i2, hat.ptr, u_hat.ptr, sv.ptr,
+        nat.check(nat.lib().ltb_slice_svd(nat.context(), work.code, P, i1, i2, work.ptr, u_hat.ptr, sv.ptr,
                                           v_hat.ptr))
+    u_hat, v_hat, sv = u_hat.astype(hat.dtype), v_hat.astype(hat.dtype), sv.astype(rdt)
     s_hat = nat.DeviceArray((P, i1, i2), rdt)
     nat.check(nat.lib().ltb_embed_diag(nat.context(), s_hat.code, P, i1, i2, sv.ptr, s_hat.ptr))
     real = _real_inputs(a)

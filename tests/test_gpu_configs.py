@@ -192,7 +192,7 @@ def test_config3_pga_200_iterations_vs_reference(cfx, precision, tol):
     spec = L.make_spec("dct", m.shape)
     x, trace = L.pga_complete(m, mask, L.CompletionConfig(spec=spec, tol=1e-300, max_iters=200), precision=precision)
     assert trace.iterations == 200
-    assert [r.mu for r in trace.records] == list(cfx["cfg3/mu"])
+    np.testing.assert_allclose([r.mu for r in trace.records], cfx["cfg3/mu"], rtol=1e-14)
     assert [r.t for r in trace.records] == list(cfx["cfg3/t"])
     idx = sample_index(x.size, NSAMPLE, seed=3)
     assert rel_err(x.ravel()[idx], cfx["cfg3/x_sample"]) < tol
@@ -254,5 +254,7 @@ def test_config4_reduced_pga_50_iterations():
     # the oracle computes in float64 on the same (float32-valued) observations, as the reference would
     ref, recs, _ = O.pga_complete(m.astype(np.float64), mask, ospec, tol=1e-300, max_iters=50)
     assert trace.iterations == 50
-    assert [r.mu for r in trace.records] == [r[1] for r in recs]
+    # mu_0 = nu ||M||_F: a device reduction vs numpy's norm, equal to the last bits
+    np.testing.assert_allclose([r.mu for r in trace.records], [r[1] for r in recs], rtol=1e-14)
+    assert [r.t for r in trace.records] == [r[2] for r in recs]
     assert rel_err(x, ref) < 1e-4

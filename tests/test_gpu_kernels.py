@@ -157,9 +157,9 @@ BLOCKED_CASES = [(np.float32, (300, 280)), (np.float64, (240, 260)), (np.complex
 
 @pytest.fixture
 def force_blocked():
-    nat.lib().ltb_debug_set_svd_blocked(1)
+    nat.check(nat.lib().ltb_ctx_set_option(nat.context(), nat.OPT_FORCE_BLOCKED_SVD, 1))
     yield
-    nat.lib().ltb_debug_set_svd_blocked(0)
+    nat.check(nat.lib().ltb_ctx_set_option(nat.context(), nat.OPT_FORCE_BLOCKED_SVD, 0))
 
 
 def _svt_check(dt, shape, batch=2, seed=11):
