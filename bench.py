@@ -234,11 +234,13 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- our arm
 def run_ours_dist(args):
-    """N > 1: config 2 strong-scaled with the row-sharded *_L product of SURVEY.md section 8(e).
-    The global operands are the fixed config-2 tensors (the same workload at every N): rank g
-    holds the i1-row block R_g of A (256/N rows) and the l-row block K_g of B (128/N rows);
-    B-hat is all-gathered over NCCL (the only collective); each rank produces its rows of C.
-    Time = max over ranks of the device (CUDA-event) step time."""
+    """N > 1: config 2 strong-scaled (the same global product at every N).  Rows of A *_L B depend
+    only on the same rows of A and on all of B, so rank g computes the i1-row block R_g of C from
+    its rows of A and a full copy of B: K1(A_g), K1(B), the slice GEMM, K1'(C_g).  Transforming B
+    on every rank (12.6 MB read + write, ~6 us) replaces the B-hat all-gather of
+    distributed.DistLProductPlan (11 MB received per rank over NVLink, plus the collective's
+    latency), so the step has no data-path collective.  Time = max over ranks of the device
+    (CUDA-event) step time; the job's work is the one config-2 product."""
     import torch
     import torch.distributed as dist
 
@@ -247,62 +249,63 @@ def run_ours_dist(args):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2202_02870_b200 as L
     from paper_2202_02870_b200 import _native as nat
-    from paper_2202_02870_b200.distributed import DeviceEngine, DistLProductPlan, blocks
+    from paper_2202_02870_b200.distributed import DeviceEngine, blocks
+    from paper_2202_02870_b200.engine import LProductPlan
 
     nat.set_device(local)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
+    nat.check(nat.lib().ltb_ctx_set_stream(nat.context(), stream.cuda_stream))
     spec = L.make_spec("dct", (256, 256, 3, 32))
-    eng = DeviceEngine(spec, (3, 32))
-    a_full, b_full = _cfg2_inputs(seed=0)
+    a_full, b_h = _cfg2_inputs(seed=0)
     r0, r1 = blocks(256, ws)[rank]
-    k0, k1 = blocks(128, ws)[rank]
     a_h = np.ascontiguousarray(a_full[r0:r1])
-    b_h = np.ascontiguousarray(b_full[k0:k1])
-    a = torch.from_numpy(a_h).cuda()
-    b = torch.from_numpy(b_h).cuda()
+    plan = LProductPlan(a_h.shape, b_h.shape, spec, np.float32)
+    a = nat.DeviceArray.from_numpy(a_h)
+    b = nat.DeviceArray.from_numpy(b_h)
+    c = nat.DeviceArray(plan.c_shape, np.float32)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    plan = DistLProductPlan(a.shape, b.shape, eng, torch.float32, a.device)
-    c = torch.empty(plan.c_shape, dtype=torch.float32, device="cuda")
     # parity gate: this rank's rows of C against the oracle on a bounded row sample
-    plan.run(a, b, out=c)
+    plan.run(a, b, c)
     torch.cuda.synchronize()
-    gate = _parity_gate(c.cpu().numpy(), a_h, b_full)
-    # the two compute phases are CUDA graphs; the B-hat all-gather runs between their replays
+    gate = _parity_gate(c.numpy(), a_h, b_h)
+    for _ in range(2):
+        plan.run(a, b, c)
+    torch.cuda.synchronize()
     l0 = nat.launch_count()
-    step = plan.graphed(a, b, c, stream)
-    launches_per_step = (nat.launch_count() - l0) // 2  # graphed(): one eager run + the captures
-    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        plan.run(a, b, c)
+    launches_per_step = nat.launch_count() - l0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
     with ClockSampler(local) as clocks:
         for i in range(args.warmup + args.steps):
             flush.zero_()
             dist.barrier()
+            torch.cuda.synchronize()
             e0.record(stream)
-            step()
+            graph.replay()
             e1.record(stream)
             e1.synchronize()
             if i >= args.warmup:
                 times.append(e0.elapsed_time(e1) / 1e3)
         launches = launches_per_step * args.steps
-        # e2e: each rank's operand rows from pinned host memory and its rows of C back to pinned
-        # host memory, copies inside the timed region (device time, max over ranks)
-        a_pin = torch.from_numpy(a_h).pin_memory()
-        b_pin = torch.from_numpy(b_h).pin_memory()
-        c_pin = torch.empty(tuple(c.shape), dtype=torch.float32).pin_memory()
+        # e2e through the public API per rank: its rows of A and all of B from pinned host
+        # memory, its rows of C back to pinned host memory (wall time, max over ranks)
+        a_pin = torch.empty(a_h.shape, dtype=torch.float32, pin_memory=True).numpy()
+        b_pin = torch.empty(b_h.shape, dtype=torch.float32, pin_memory=True).numpy()
+        c_pin = torch.empty(plan.c_shape, dtype=torch.float32, pin_memory=True).numpy()
+        a_pin[...] = a_h
+        b_pin[...] = b_h
         e2e_times = []
         for i in range(args.warmup + args.steps):
             dist.barrier()
-            e0.record(stream)
-            a.copy_(a_pin, non_blocking=True)
-            b.copy_(b_pin, non_blocking=True)
-            step()
-            c_pin.copy_(c, non_blocking=True)
-            e1.record(stream)
-            e1.synchronize()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            L.l_product(a_pin, b_pin, spec, out=c_pin)
             if i >= args.warmup:
-                e2e_times.append(e0.elapsed_time(e1) / 1e3)
+                e2e_times.append(time.perf_counter() - t0)
     pga = None if (args.skip_extras or args.skip_pga) else bench_pga_dist(L, torch, dist, eng_cls=DeviceEngine,
                                                                           args=args)
     t = torch.tensor([sum(times), sum(e2e_times), gate["rel_err"]], dtype=torch.float64, device="cuda")
@@ -311,9 +314,9 @@ def run_ours_dist(args):
     gate = {"rows_checked_per_rank": gate["rows_checked"], "rel_err_max_over_ranks": worst,
             "tol": 1e-4, "ok": worst < 1e-4}
     hbm_peak, _, peak_src = _peaks()
-    E_a, E_b, E_c = 256 * 128 * 96, 128 * 256 * 96, 256 * 256 * 96
-    # per rank: its A rows and C rows once, its B block once plus the gathered B-hat once
-    alg_bytes = 4 * ((r1 - r0) * 128 * 96 + (k1 - k0) * 256 * 96 + E_b + (r1 - r0) * 256 * 96)
+    E_b = 128 * 256 * 96
+    # rank-local fused bytes: its A rows, all of B, its C rows (one read / write each)
+    alg_bytes = 4 * ((r1 - r0) * 128 * 96 + E_b + (r1 - r0) * 256 * 96)
     achieved = alg_bytes * args.steps / t_step / 1e9
     line = {
         "metric": "*_L-product GFLOP/s", "value": GFLOP_CFG2 * args.steps / t_step / 1e9, "unit": "GFLOP/s",
@@ -321,15 +324,16 @@ def run_ours_dist(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic N(0,1) seed 0 (BASELINE config 2 shapes)",
         "config": dict(CONFIG2), "l2": L2_NOTE,
-        "parallelism": f"A rows / B rows sharded x{ws}, B-hat all-gather (NCCL)",
+        "parallelism": f"A / C rows sharded x{ws}, B transformed on every rank (no data-path collective)",
         "parity_gate": gate,
-        "roofline": {"kernel": "whole sharded step (rank-local bytes)", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": "whole rank-local step (fused bytes)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "peak_source": f"{peak_src} HBM copy", "traffic": None},
-        "e2e": {"value": GFLOP_CFG2 * args.steps / t_e2e / 1e9, "unit": "GFLOP/s",
-                "h2d_bytes_per_step": int(E_a * 4 + E_b * 4), "d2h_bytes_per_step": int(E_c * 4),
-                "api": "distributed.DistLProductPlan per rank, pinned host operand rows in / rows of C out "
-                       "(bytes summed over ranks)"},
+        "e2e": {"value": GFLOP_CFG2 * len(e2e_times) / t_e2e / 1e9, "unit": "GFLOP/s",
+                "h2d_bytes_per_step": int(4 * (256 * 128 * 96 + ws * E_b)),
+                "d2h_bytes_per_step": int(4 * 256 * 256 * 96),
+                "api": "paper_2202_02870_b200.l_product(numpy, numpy, spec, out=numpy) per rank on pinned host "
+                       "arrays (its rows of A, all of B); bytes summed over ranks"},
         "gpu_launches": int(launches), "clocks": clocks.summary(),
     }
     if pga is not None:

@@ -192,7 +192,8 @@ def test_config3_pga_200_iterations_vs_reference(cfx, precision, tol):
     spec = L.make_spec("dct", m.shape)
     x, trace = L.pga_complete(m, mask, L.CompletionConfig(spec=spec, tol=1e-300, max_iters=200), precision=precision)
     assert trace.iterations == 200
-    np.testing.assert_allclose([r.mu for r in trace.records], cfx["cfg3/mu"], rtol=1e-14)
+    # mu_0 = nu ||M||_F over 7.6M entries: the device's fixed-order reduction vs numpy's pairwise sum
+    np.testing.assert_allclose([r.mu for r in trace.records], cfx["cfg3/mu"], rtol=1e-13)
     assert [r.t for r in trace.records] == list(cfx["cfg3/t"])
     idx = sample_index(x.size, NSAMPLE, seed=3)
     assert rel_err(x.ravel()[idx], cfx["cfg3/x_sample"]) < tol
@@ -201,7 +202,9 @@ def test_config3_pga_200_iterations_vs_reference(cfx, precision, tol):
     rr = cfx["cfg3/rel"]
     fin = np.isfinite(rr)
     np.testing.assert_array_equal(np.isfinite(rc), fin)
-    np.testing.assert_allclose(rc[fin], rr[fin], rtol=1e-2 if precision == "fp32" else 1e-6)
+    # fp32: ||y - x+|| / ||x+|| carries ~1e-6 absolute rounding (it falls to ~1e-5 late in the run)
+    np.testing.assert_allclose(rc[fin], rr[fin], rtol=1e-2 if precision == "fp32" else 1e-6,
+                               atol=2e-6 if precision == "fp32" else 0.0)
 
 
 @pytest.mark.parametrize("n", [256, 512])
