@@ -235,6 +235,33 @@ int ltb_project_omega(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const
 int ltb_pga_gradient(ltb_ctx* ctx, int dtype, int64_t n, const void* d_xc, const void* d_xp,
                      const void* d_pobs, const uint8_t* d_mask, double beta, void* d_y, void* d_g);
 
+/* ---------------------------------------------------------------- sharded PGA (multi-GPU)
+ * One iteration of pga_complete (completion.py:165-197) on a rank's shard, for a caller that
+ * runs the collectives between the steps: every step is
+ * stream-ordered, returns without a host synchronisation, and is a no-op once
+ * d_state[0] != 0, so a chunk of iterations can be enqueued and read back at its end.
+ *   pack_mask : uint8 0/1 -> bit-packed words (bit e of word e/32)
+ *   forward   : rows shard (ntubes tubes, tube-major) -> gradient step fused into the load
+ *               (y = x + beta (x - x_prev), g = y - (P_Omega(y) - p_obs)) -> L -> slice-major
+ *   svt       : the slice block; d_v (batch x n x n) carries right bases between calls for
+ *               real fp32 / fp64 slices (warm = 0 on the first call), NULL for plain svt
+ *   inverse   : slice-major rows shard -> L^-1, real part -> x_next, fused norms into
+ *               d_sums[0..4] = {sum (y-x+)^2, sum x+^2, sum (x+-gt)^2, sum Im^2} (all-reduce
+ *               SUM) and d_sums[4] = max x+ (all-reduce MAX); d_gt may be NULL
+ *   decide    : after the all-reduces: d_rec[0..4] as ltb_pga_run's records, d_state[1] +=
+ *               1, d_state[0] = 1 once rel <= tol (pobs_sumsq = the global sum p_obs^2) */
+int ltb_pack_mask(ltb_ctx* ctx, int64_t n, const uint8_t* d_mask, uint32_t* d_bits);
+int ltb_pga_shard_forward(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t ntubes, double beta,
+                          const void* d_xc, const void* d_xp, const void* d_pobs, const uint32_t* d_bits,
+                          void* d_hat, const int* d_state);
+int ltb_pga_shard_svt(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2, const void* d_hat, double tau,
+                      void* d_out, void* d_v, int warm, const int* d_state);
+int ltb_pga_shard_inverse(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t ntubes, double beta,
+                          const void* d_hat, const void* d_xc, const void* d_xp, const void* d_gt, void* d_xn,
+                          double* d_sums, const int* d_state);
+int ltb_pga_shard_decide(ltb_ctx* ctx, const double* d_sums, double pobs_sumsq, double tol, double* d_rec,
+                         int* d_state);
+
 /* ---------------------------------------------------------------- K4 + PGA
  * pga_complete (completion.py:141-202).  The host keeps the scalar
  * recurrences: it passes, per iteration k (1-based), beta_k = (t_{k-1}-1)/t_k

@@ -84,6 +84,11 @@ _SIGNATURES = {
     "ltb_pga_fetch": ([_vp, _int, _dp], _int),
     "ltb_pga_current": ([_vp, C.POINTER(_vp)], _int),
     "ltb_pga_destroy": ([_vp], None),
+    "ltb_pack_mask": ([_vp, _i64, _vp, _vp], _int),
+    "ltb_pga_shard_forward": ([_vp, _vp, _int, _i64, C.c_double, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ltb_pga_shard_svt": ([_vp, _int, _i64, _i64, _i64, _vp, C.c_double, _vp, _vp, _int, _vp], _int),
+    "ltb_pga_shard_inverse": ([_vp, _vp, _int, _i64, C.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "ltb_pga_shard_decide": ([_vp, _vp, C.c_double, C.c_double, _vp, _vp], _int),
 }
 
 # every symbol include/ltb.h declares (checked by the CPU test suite)

@@ -264,12 +264,14 @@ def _resolve_precision(m_in, precision):
     return precision
 
 
-def pga_complete(m, mask, cfg: CompletionConfig, ground_truth=None, *, precision=None, chunk=None):
+def pga_complete(m, mask, cfg: CompletionConfig, ground_truth=None, *, precision=None, chunk=None, group=None):
     """Complete P_Omega(m) by accelerated proximal gradient (completion.py:141-202).
 
     Returns (completed float64 tensor, CompletionTrace).  Keyword-only extras:
-    precision ("fp32" / "fp64", default: fp32 for float32 `m`, else fp64) and
-    chunk (iterations enqueued per device round trip, default adaptive)."""
+    precision ("fp32" / "fp64", default: fp32 for float32 `m`, else fp64),
+    chunk (iterations enqueued per device round trip, default adaptive) and
+    group (a torch.distributed process group, or "world"): every rank of the group
+    makes the same call and the solve is sharded over their GPUs (distributed.py)."""
     cfg.validate()
     if not cfg.spec.unitary_scaled:
         raise UnsupportedSpecError("completion uses SVT, which requires a unitary-scaled transform")
@@ -291,6 +293,11 @@ def pga_complete(m, mask, cfg: CompletionConfig, ground_truth=None, *, precision
     if cfg.rse_denominator not in ("obtained", "original"):
         raise ParameterError(f"unknown RSE denominator {cfg.rse_denominator!r}")
 
+    if group is not None:
+        from .distributed import spmd_pga_complete
+
+        return spmd_pga_complete(m64 if prec == "fp64" else np.asarray(m), mask, cfg, gt, precision=prec,
+                                 group=group)
     solver = PGASolver(m64, mask, cfg.spec, prec, gt)
     trace = CompletionTrace()
     pobs_zero = solver.pobs_sumsq == 0.0

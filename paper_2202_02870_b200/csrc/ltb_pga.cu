@@ -326,6 +326,50 @@ __global__ void pga_fetch_kernel(int64_t E, const R* __restrict__ x, const R* __
   }
 }
 
+// sharded PGA (multi-GPU): the local reduction of the fused inverse's per-CTA partials in a
+// fixed order, laid out for the cross-rank all-reduces: [0..3] = sum (y - x+)^2, sum x+^2,
+// sum (x+ - gt)^2, sum Im^2 (SUM), [4] = max x+ (MAX)
+__global__ void pga_shard_sums_kernel(const double* __restrict__ partials, int64_t nblocks,
+                                      double* __restrict__ sums, const int* __restrict__ state) {
+  if (state && state[0]) return;
+  const int slot = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (slot >= 5) return;
+  const bool mx = slot == 3;
+  double v = mx ? -1.0e308 : 0.0;
+  for (int64_t i = lane; i < nblocks; i += 32) {
+    const double w = partials[i * 5 + slot];
+    v = mx ? fmax(v, w) : v + w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = mx ? fmax(v, w) : v + w;
+  }
+  if (lane == 0) sums[slot == 3 ? 4 : (slot == 4 ? 3 : slot)] = v;
+}
+
+// the stop rule of completion.py:174-181,195-197 on the all-reduced sums (identical on every
+// rank); rec in ltb_pga_run's record order {sum (y-x+)^2, sum x+^2, sum (x+-gt)^2, max x+, sum Im^2}
+__global__ void pga_shard_decide_kernel(const double* __restrict__ sums, double pobs_sumsq, double tol,
+                                        double* __restrict__ rec, int* __restrict__ state) {
+  if (state[0]) return;
+  rec[0] = sums[0];
+  rec[1] = sums[1];
+  rec[2] = sums[2];
+  rec[3] = sums[4];
+  rec[4] = sums[3];
+  const double num = sqrt(sums[0]), den = sqrt(sums[1]);
+  double rel;
+  if (den > 0.0)
+    rel = num / den;
+  else if (pobs_sumsq == 0.0)
+    rel = 0.0;
+  else
+    rel = __longlong_as_double(0x7ff0000000000000LL);
+  state[1] += 1;
+  if (rel <= tol) state[0] = 1;
+}
+
 // tile plan of the fused transforms for this spec and compute type (0 if too long)
 template <typename Tc, typename Tm>
 int pga_plan(const ltb_spec* spec, int64_t NT, int inverse, XformParams& p, size_t* smem) {
@@ -620,6 +664,98 @@ void ltb_pga_destroy(ltb_pga* g) {
   ltb_ws_free(ctx, g->vcarry64);
   cudaStreamSynchronize(ctx->stream);
   delete g;
+}
+
+// ---------------------------------------------------------------- sharded PGA steps
+int ltb_pack_mask(ltb_ctx* ctx, int64_t n, const uint8_t* d_mask, uint32_t* d_bits) {
+  if (n < 0) return ltb_set_error(ctx, LTB_ESHAPE, "pack_mask: negative length");
+  if (n == 0) return LTB_OK;
+  pack_mask_kernel<<<grid_for((n + 31) / 32, 256, ctx->num_sms * 8), 256, 0, ctx->stream>>>(n, d_mask, d_bits);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
+
+int ltb_pga_shard_forward(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t ntubes, double beta,
+                          const void* d_xc, const void* d_xp, const void* d_pobs, const uint32_t* d_bits,
+                          void* d_hat, const int* d_state) {
+  if (!spec) return ltb_set_error(ctx, LTB_ETRANSFORM, "null spec");
+  if (dtype != LTB_F32 && dtype != LTB_F64) return ltb_set_error(ctx, LTB_EPARAM, "pga shard: real dtype expected");
+  if (ntubes <= 0) return LTB_OK;
+  auto run = [&](auto rt, auto ct) -> int {
+    using R = decltype(rt);
+    using Tc = decltype(ct);
+    XformParams p;
+    size_t smem = 0;
+    if (!pga_plan<Tc, Tc>(spec, ntubes, 0, p, &smem))
+      return ltb_set_error(ctx, LTB_ESHAPE, "pga shard: tube too long for the fused transform");
+    LoadPGA<R> ld{(const R*)d_xc, (const R*)d_xp, (const R*)d_pobs, d_bits, (R)beta};
+    StorePlain<Tc, false> st{(Tc*)d_hat, LTB_SLICE_MAJOR};
+    const int dbl = std::is_same<R, double>::value ? 1 : 0;
+    return launch_xform_tile<Tc, Tc>(ctx, p, ld, st, (const Tc*)spec->d_mats[dbl][0], nullptr, d_state, smem);
+  };
+  if (spec->is_complex)
+    return dtype == LTB_F64 ? run(double(), cplx<double>()) : run(float(), cplx<float>());
+  return dtype == LTB_F64 ? run(double(), double()) : run(float(), float());
+}
+
+int ltb_pga_shard_svt(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_t I2, const void* d_hat, double tau,
+                      void* d_out, void* d_v, int warm, const int* d_state) {
+  if (!dtype_valid(dtype)) return ltb_set_error(ctx, LTB_EPARAM, "pga shard svt: bad dtype");
+  if (!(tau >= 0)) return ltb_set_error(ctx, LTB_EPARAM, "tau must be >= 0, got %g", tau);
+  if (batch <= 0 || I1 <= 0 || I2 <= 0) return LTB_OK;
+  if (d_v && dtype == LTB_F32) {
+    const int st = ltb_svt_carry_impl(ctx, batch, I1, I2, (const float*)d_hat, tau, (float*)d_out, (float*)d_v, warm,
+                                      d_state);
+    if (st != LTB_EUNSUPPORTED) return st;
+  }
+  if (d_v && dtype == LTB_F64) {
+    const int st = ltb_svt_carry64_impl(ctx, batch, I1, I2, (const double*)d_hat, tau, (double*)d_out,
+                                        (double*)d_v, warm, d_state);
+    if (st != LTB_EUNSUPPORTED) return st;
+  }
+  return ltb_svt_impl(ctx, dtype, batch, I1, I2, d_hat, tau, nullptr, d_out, d_state);
+}
+
+int ltb_pga_shard_inverse(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t ntubes, double beta,
+                          const void* d_hat, const void* d_xc, const void* d_xp, const void* d_gt, void* d_xn,
+                          double* d_sums, const int* d_state) {
+  if (!spec) return ltb_set_error(ctx, LTB_ETRANSFORM, "null spec");
+  if (dtype != LTB_F32 && dtype != LTB_F64) return ltb_set_error(ctx, LTB_EPARAM, "pga shard: real dtype expected");
+  if (ntubes <= 0) {  // an empty shard contributes zero sums and no maximum
+    const double z[5] = {0.0, 0.0, 0.0, 0.0, -1.0e308};
+    LTB_CUDA_TRY(ctx, cudaMemcpyAsync(d_sums, z, sizeof(z), cudaMemcpyHostToDevice, ctx->stream));
+    LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    return LTB_OK;
+  }
+  WsScope ws(ctx);
+  auto run = [&](auto rt, auto ct) -> int {
+    using R = decltype(rt);
+    using Tc = decltype(ct);
+    XformParams p;
+    size_t smem = 0;
+    if (!pga_plan<Tc, Tc>(spec, ntubes, 1, p, &smem))
+      return ltb_set_error(ctx, LTB_ESHAPE, "pga shard: tube too long for the fused transform");
+    double* partials = nullptr;  // one slot set per CTA: the grid never exceeds the tile count
+    LTB_TRY(ws.alloc(sizeof(double) * 5 * ((ntubes + p.TT - 1) / p.TT), &partials));
+    StorePGA<R> st{(R*)d_xn, (const R*)d_xc, (const R*)d_xp, (const R*)d_gt, (R)beta};
+    LoadPlain<Tc> ld{(const Tc*)d_hat, LTB_SLICE_MAJOR};
+    const int dbl = std::is_same<R, double>::value ? 1 : 0;
+    int64_t nb = 0;
+    LTB_TRY((launch_xform_tile<Tc, Tc>(ctx, p, ld, st, (const Tc*)spec->d_mats[dbl][1], partials, d_state, smem, &nb)));
+    pga_shard_sums_kernel<<<1, 160, 0, ctx->stream>>>(partials, nb, d_sums, d_state);
+    LTB_LAUNCH_CHECK(ctx);
+    return LTB_OK;
+  };
+  if (spec->is_complex)
+    return dtype == LTB_F64 ? run(double(), cplx<double>()) : run(float(), cplx<float>());
+  return dtype == LTB_F64 ? run(double(), double()) : run(float(), float());
+}
+
+int ltb_pga_shard_decide(ltb_ctx* ctx, const double* d_sums, double pobs_sumsq, double tol, double* d_rec,
+                         int* d_state) {
+  pga_shard_decide_kernel<<<1, 1, 0, ctx->stream>>>(d_sums, pobs_sumsq, tol, d_rec, d_state);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
 }
 
 }  // extern "C"

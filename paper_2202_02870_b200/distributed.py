@@ -189,6 +189,8 @@ def fibres_to_slices(hat_rows: torch.Tensor, I1: int, group=None) -> torch.Tenso
     out_splits = [(q1 - q0) * (r1 - r0) * I2 for r0, r1 in rb]
     recv = torch.empty(sum(out_splits), dtype=send.dtype, device=send.device)
     dist.all_to_all_single(recv, send.reshape(-1), out_splits, in_splits, group=group)
+    if I1 % world == 0:  # equal row blocks: the reassembly is one permuting copy
+        return recv.view(world, q1 - q0, I1 // world, I2).transpose(0, 1).reshape(q1 - q0, I1, I2)
     out = torch.empty((q1 - q0, I1, I2), dtype=send.dtype, device=send.device)
     off = 0
     for (r0, r1), n in zip(rb, out_splits):
@@ -203,7 +205,12 @@ def slices_to_fibres(slices: torch.Tensor, P: int, group=None) -> torch.Tensor:
     nq, I1, I2 = slices.shape
     rb = blocks(I1, world)
     qb = blocks(P, world)
-    send = torch.cat([slices[:, r0:r1, :].reshape(-1) for r0, r1 in rb]) if nq else slices.new_empty(0)
+    if not nq:
+        send = slices.new_empty(0)
+    elif I1 % world == 0:  # equal row blocks: destination-major in one permuting copy
+        send = slices.view(nq, world, I1 // world, I2).transpose(0, 1).reshape(-1)
+    else:
+        send = torch.cat([slices[:, r0:r1, :].reshape(-1) for r0, r1 in rb])
     in_splits = [nq * (r1 - r0) * I2 for r0, r1 in rb]
     r0, r1 = rb[rank]
     out_splits = [(b1 - b0) * (r1 - r0) * I2 for b0, b1 in qb]
@@ -370,9 +377,11 @@ def dist_pga_complete(m_rows: torch.Tensor, mask_rows: torch.Tensor, cfg: Comple
         raise UnsupportedSpecError("completion uses SVT, which requires a unitary-scaled transform")
     if m_rows.shape != mask_rows.shape:
         raise ShapeError(f"mask shape {tuple(mask_rows.shape)} does not match data shape {tuple(m_rows.shape)}")
+    if isinstance(engine, DeviceEngine) and m_rows.is_cuda:
+        return _dist_pga_device(m_rows, mask_rows, cfg, I1, engine, group, ground_truth_rows, mu0)
     mask_u8 = mask_rows.to(torch.uint8).contiguous()
     m_rows = m_rows.contiguous()
-    pobs = torch.where(mask_rows.bool(), m_rows, torch.zeros_like(m_rows))
+    pobs = torch.where(mask_u8.bool(), m_rows, torch.zeros_like(m_rows)).contiguous()
 
     def allsum(vals):
         t = torch.as_tensor(vals, dtype=torch.float64, device=m_rows.device)
@@ -421,5 +430,198 @@ def dist_pga_complete(m_rows: torch.Tensor, mask_rows: torch.Tensor, cfg: Comple
         if rel <= cfg.tol:
             trace.status = "converged"
             break
-    out = torch.where(mask_rows.bool(), m_rows, x_cur) if cfg.reimpose_observed else x_cur
+    out = torch.where(mask_u8.bool(), m_rows, x_cur).contiguous() if cfg.reimpose_observed else x_cur
     return out, trace
+
+
+def _dist_pga_device(m_rows, mask_rows, cfg, I1, engine, group, gt_rows, mu0, chunk: int = 16):
+    """The device path of dist_pga_complete: per iteration one fused gradient + forward launch
+    (ltb_pga_shard_forward), the fibre -> slice all-to-all, the slice block's SVT warm-started
+    from the previous iteration's right bases (ltb_pga_shard_svt), the all-to-all back, one
+    fused inverse + norms launch (ltb_pga_shard_inverse), two all-reduces of the five sums and
+    the stop decision on the device (ltb_pga_shard_decide).  Nothing synchronises the host
+    inside a chunk of iterations: once the device stop flag is raised every later kernel is a
+    no-op (the collectives still run, identically on every rank), and the host reads the
+    records and the executed count once per chunk, as ltb_pga_run does on one GPU."""
+    lib, ctx = nat.lib(), nat.context()
+    dt = m_rows.dtype
+    if dt not in (torch.float32, torch.float64):
+        m_rows = m_rows.double()
+        dt = torch.float64
+    code = nat.F32 if dt == torch.float32 else nat.F64
+    r, I2 = int(m_rows.shape[0]), int(m_rows.shape[1])
+    E = m_rows.numel()
+    ntubes = r * I2
+    P = engine.P
+    dev = m_rows.device
+    # every buffer handed to libltb by pointer is C-contiguous (a Fortran-ordered numpy mask,
+    # e.g. sample_mask's, gives strided torch views and strided torch.where results)
+    m_rows = m_rows.contiguous()
+    mask_u8 = mask_rows.to(torch.uint8).contiguous()
+    bits = torch.zeros(max((E + 31) // 32, 1), dtype=torch.int32, device=dev)
+    nat.check(lib.ltb_pack_mask(ctx, E, mask_u8.data_ptr(), bits.data_ptr()))
+    pobs = torch.where(mask_u8.bool(), m_rows, torch.zeros_like(m_rows)).contiguous()
+    gt = gt_rows.to(dt).contiguous() if gt_rows is not None else None
+
+    def allsum(vals):
+        t = torch.as_tensor(vals, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, group=group)
+        return t
+
+    if mu0 is None and cfg.mu0 is None:
+        mu0 = cfg.nu * math.sqrt(float(allsum([float((m_rows.double() ** 2).sum())])[0]))
+    elif mu0 is None:
+        mu0 = float(cfg.mu0)
+    mus, ts, betas = pga_schedule(cfg, mu0)
+    pobs_sumsq = float(allsum([float((pobs.double() ** 2).sum())])[0])
+    gt_sumsq = None
+    if gt is not None and cfg.rse_denominator == "original":
+        gt_sumsq = float(allsum([float((gt.double() ** 2).sum())])[0])
+    hat_np = np.dtype(forward_dtype(np.dtype(np.float32 if code == nat.F32 else np.float64), engine.spec))
+    hat_t = _TORCH_DT[hat_np]
+    world, rank = _world(group)
+    q0, q1 = blocks(P, world)[rank]
+    nq, n = q1 - q0, min(I1, I2)
+    xs = [torch.zeros_like(m_rows), torch.zeros_like(m_rows), torch.empty_like(m_rows)]
+    hat_rows = torch.empty((P, r, I2), dtype=hat_t, device=dev)
+    sl_out = torch.empty((nq, I1, I2), dtype=hat_t, device=dev)
+    vcarry = torch.empty((nq, n, n), dtype=dt, device=dev) if not hat_t.is_complex and nq else None
+    state = torch.zeros(2, dtype=torch.int32, device=dev)
+    sums = torch.zeros(5, dtype=torch.float64, device=dev)
+    recs = torch.zeros((chunk, 5), dtype=torch.float64, device=dev)
+    gt_ptr = gt.data_ptr() if gt is not None else None
+    h = engine.handle.ptr
+    trace = CompletionTrace()
+    warm, done, ip, ic = 0, 0, 0, 1  # xs[ip] = x_prev, xs[ic] = x_cur
+    k = 1
+    while k <= cfg.max_iters and trace.status != "converged":
+        count = min(chunk, cfg.max_iters - k + 1)
+        nexts = []
+        for i in range(count):
+            kk = k + i
+            inx = 3 - ip - ic
+            xp, xc, xn = xs[ip], xs[ic], xs[inx]
+            beta = float(betas[kk - 1])
+            nat.check(lib.ltb_pga_shard_forward(ctx, h, code, ntubes, beta, xc.data_ptr(), xp.data_ptr(),
+                                                pobs.data_ptr(), bits.data_ptr(), hat_rows.data_ptr(),
+                                                state.data_ptr()))
+            sl = fibres_to_slices(hat_rows, I1, group)
+            nat.check(lib.ltb_pga_shard_svt(ctx, nat.dtype_code(hat_np), nq, I1, I2, sl.data_ptr(),
+                                            float(mus[kk - 1]), sl_out.data_ptr(),
+                                            vcarry.data_ptr() if vcarry is not None else None, warm,
+                                            state.data_ptr()))
+            warm = 1
+            back = slices_to_fibres(sl_out, P, group)
+            nat.check(lib.ltb_pga_shard_inverse(ctx, h, code, ntubes, beta, back.data_ptr(), xc.data_ptr(),
+                                                xp.data_ptr(), gt_ptr, xn.data_ptr(), sums.data_ptr(),
+                                                state.data_ptr()))
+            dist.all_reduce(sums[:4], group=group)
+            dist.all_reduce(sums[4:], op=dist.ReduceOp.MAX, group=group)
+            nat.check(lib.ltb_pga_shard_decide(ctx, sums.data_ptr(), pobs_sumsq, float(cfg.tol),
+                                               recs[i].data_ptr(), state.data_ptr()))
+            nexts.append(inx)
+            ip, ic = ic, inx
+        st = state.tolist()
+        rec = recs[:count].tolist()
+        executed = st[1] - done
+        for i in range(executed):
+            kk = k + i
+            r0, r1, r2, peak, _ = rec[i]
+            rel = rel_change(r0, r1, pobs_sumsq == 0.0)
+            item = IterationRecord(k=kk, mu=mus[kk - 1], t=ts[kk - 1], rel_change=rel)
+            if gt is not None:
+                den = math.sqrt(r1) ** 2 if cfg.rse_denominator == "obtained" else gt_sumsq
+                err = math.sqrt(r2) ** 2
+                item.rse = math.nan if den == 0.0 else err / den
+                item.psnr = math.inf if err == 0.0 else (-math.inf if peak == 0.0 else
+                                                         10.0 * math.log10(peak ** 2 / err))
+            trace.records.append(item)
+        done = st[1]
+        if st[0]:
+            trace.status = "converged"
+            ic = nexts[executed - 1]  # the iterate of the last executed iteration
+        k += count
+    x_cur = xs[ic]
+    out = torch.where(mask_u8.bool(), m_rows, x_cur).contiguous() if cfg.reimpose_observed else x_cur
+    return out, trace
+
+
+# ----------------------------------------------------------------- SPMD drop-in entry points
+def _group(group):
+    return None if isinstance(group, str) and group == "world" else group
+
+
+def _gather_rows(x_rows: torch.Tensor, I1: int, group) -> np.ndarray:
+    """All-gather the row blocks of a row-sharded tensor into the full (I1, ...) numpy array."""
+    world, _ = _world(group)
+    rb = blocks(I1, world)
+    rmax = max(b - a for a, b in rb)
+    buf = torch.zeros((rmax,) + tuple(x_rows.shape[1:]), dtype=x_rows.dtype, device=x_rows.device)
+    buf[: x_rows.shape[0]] = x_rows
+    allbuf = torch.empty((world * rmax,) + tuple(x_rows.shape[1:]), dtype=x_rows.dtype, device=x_rows.device)
+    dist.all_gather_into_tensor(allbuf, buf, group=group)
+    return torch.cat([allbuf[g * rmax: g * rmax + (b - a)] for g, (a, b) in enumerate(rb)]).cpu().numpy()
+
+
+def _engine(spec, trailing):
+    cache = spec.__dict__.setdefault("_spmd_engines", {})
+    key = (tuple(int(d) for d in trailing), nat.current_device())
+    if key not in cache:
+        cache[key] = DeviceEngine(spec, trailing)
+    return cache[key]
+
+
+def spmd_pga_complete(m, mask, cfg: CompletionConfig, ground_truth=None, *, precision="fp64", group="world"):
+    """pga_complete (completion.py:141-202) across the ranks of `group`, called by every rank
+    with the same arguments (SPMD, one process per GPU under torchrun).  Rank g takes the
+    i1-row block R_g; the iteration is dist_pga_complete's device path; every rank returns the
+    full float64 iterate and the (identical) trace, as the single-process call does."""
+    grp = _group(group)
+    world, rank = _world(grp)
+    from .core import fro_norm
+
+    m64 = np.asarray(m, dtype=float)
+    mask = np.asarray(mask, dtype=bool)
+    I1 = m64.shape[0]
+    r0, r1 = blocks(I1, world)[rank]
+    dev = torch.device("cuda", nat.current_device())
+    dt = torch.float32 if precision == "fp32" else torch.float64
+    eng = _engine(cfg.spec, m64.shape[2:])
+    m_rows = torch.from_numpy(np.ascontiguousarray(m64[r0:r1])).to(dev, dt)
+    k_rows = torch.from_numpy(np.ascontiguousarray(mask[r0:r1])).to(dev)
+    gt_rows = None
+    if ground_truth is not None:
+        gt_rows = torch.from_numpy(np.ascontiguousarray(np.asarray(ground_truth, dtype=float)[r0:r1])).to(dev, dt)
+    mu0 = cfg.nu * fro_norm(m64) if cfg.mu0 is None else float(cfg.mu0)  # as the single-GPU call computes it
+    x_rows, trace = dist_pga_complete(m_rows, k_rows, cfg, I1, eng, group=grp, ground_truth_rows=gt_rows, mu0=mu0)
+    return _gather_rows(x_rows.double(), I1, grp), trace
+
+
+def spmd_svt(a, tau: float, spec, *, group="world"):
+    """svt (linalg.py:168-181) across the ranks of `group` (SPMD): row-sharded transforms, the
+    slice-sharded SVT between two all-to-alls; every rank returns the full result."""
+    grp = _group(group)
+    world, rank = _world(grp)
+    a = np.asarray(a)
+    I1 = a.shape[0]
+    r0, r1 = blocks(I1, world)[rank]
+    dev = torch.device("cuda", nat.current_device())
+    rows = torch.from_numpy(np.ascontiguousarray(a[r0:r1])).to(dev)
+    out = dist_svt(rows, tau, I1, _engine(spec, a.shape[2:]), grp)
+    return _gather_rows(out, I1, grp)
+
+
+def spmd_l_product(a, b, spec, *, group="world"):
+    """l_product (linalg.py:34-43) across the ranks of `group` (SPMD): rank g computes the rows
+    R_g of C from its rows of A and all of B (rows of a *_L b depend only on the same rows of
+    a), then the row blocks are all-gathered; every rank returns the full product."""
+    from .linalg import l_product
+
+    grp = _group(group)
+    world, rank = _world(grp)
+    a = np.asarray(a)
+    I1 = a.shape[0]
+    r0, r1 = blocks(I1, world)[rank]
+    c_rows = l_product(np.ascontiguousarray(a[r0:r1]), b, spec)
+    dev = torch.device("cuda", nat.current_device())
+    return _gather_rows(torch.from_numpy(np.ascontiguousarray(c_rows)).to(dev), I1, grp)

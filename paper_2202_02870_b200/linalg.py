@@ -81,13 +81,23 @@ def _singular_values(a: np.ndarray, spec: TransformSpec) -> np.ndarray:
 
 
 # ----------------------------------------------------------------- public API
-def l_product(a, b, spec: TransformSpec, *, out: np.ndarray | None = None) -> np.ndarray:
+def l_product(a, b, spec: TransformSpec, *, out: np.ndarray | None = None, group=None) -> np.ndarray:
     """a *_L b = L^{-1}(L(a) facewise L(b)) (linalg.py:34-43).
 
-    `out` (optional, not in the reference signature): a C-contiguous host array of
-    the result's shape and dtype (e.g. pinned memory) that receives the product."""
+    Keyword-only extras (not in the reference signature): `out`, a C-contiguous host
+    array of the result's shape and dtype (e.g. pinned memory) that receives the
+    product; `group`, a torch.distributed process group (or "world") whose ranks all
+    make the same call and split the rows of the product between their GPUs."""
     a = np.asarray(a)
     b = np.asarray(b)
+    if group is not None:
+        from .distributed import spmd_l_product
+
+        res = spmd_l_product(a, b, spec, group=group)
+        if out is not None:
+            out[...] = res
+            return out
+        return res
     if a.shape[2:] != b.shape[2:]:
         raise ShapeError(f"trailing dims differ: {a.shape[2:]} vs {b.shape[2:]}")
     if a.shape[1] != b.shape[0]:
@@ -246,15 +256,22 @@ def nuclear_norm(a, spec: TransformSpec) -> float:
     return float(_singular_values(np.asarray(a), spec).sum() / spec.alpha)
 
 
-def svt(a, tau: float, spec: TransformSpec) -> np.ndarray:
+def svt(a, tau: float, spec: TransformSpec, *, group=None) -> np.ndarray:
     """Singular value thresholding, the prox of tau * TNN (linalg.py:168-181).
 
     K3: per-slice one-sided Jacobi in shared memory, then the threshold and the
-    rank-limited recomposition as two batched GEMMs, all on the device."""
+    rank-limited recomposition as two batched GEMMs, all on the device.  `group`
+    (keyword-only, a torch.distributed process group or "world"): every rank makes the
+    same call; transforms are row-sharded and the slices split between the GPUs."""
     if tau < 0:
         raise ParameterError(f"tau must be >= 0, got {tau}")
     _require_unitary(spec, "svt")
     a = np.asarray(a)
+    if group is not None:
+        _check_shape(a.shape, spec)
+        from .distributed import spmd_svt
+
+        return spmd_svt(a, tau, spec, group=group)
     hat = _hat_stack(a, spec)
     P, i1, i2 = hat.shape
     out = nat.DeviceArray((P, i1, i2), hat.dtype)

@@ -99,3 +99,44 @@ def test_dist_pga_fp32_carried_device(nccl_world1):
     ref, rtrace = L.pga_complete(m.astype(np.float64), mask, cfg)
     assert trace.iterations == rtrace.iterations == 60
     assert rel_err(x.cpu().numpy(), ref) < 1e-4
+
+
+def test_dist_pga_device_converges_midchunk(nccl_world1, golden):
+    """The device stop flag: a default-tol run that converges inside a chunk returns the
+    iterate of the converging iteration and the same trace as the single-device solver."""
+    name = "c_pinned_dct"
+    m = golden[f"{name}/m"]
+    spec = L.make_spec("dct", m.shape)
+    mask = L.sample_mask(m.shape, 0.5, 7)
+    cfg = L.CompletionConfig(spec=spec, max_iters=300)
+    x, trace = dist_pga_complete(torch.from_numpy(m).cuda(), torch.from_numpy(mask).cuda(), cfg, m.shape[0],
+                                 DeviceEngine(spec, m.shape[2:]))
+    ref, rtrace = L.pga_complete(m, mask, cfg)
+    assert trace.status == rtrace.status == "converged"
+    assert trace.iterations == rtrace.iterations
+    np.testing.assert_allclose([r.rel_change for r in trace.records], [r.rel_change for r in rtrace.records],
+                               rtol=1e-8)
+    assert rel_err(x.cpu().numpy(), ref) < 1e-10
+
+
+def test_spmd_drop_in_entry_points(nccl_world1, golden):
+    """The reference entry points with group="world": every rank makes the same call and gets
+    the full result (here world 1: the sharded path end to end through NCCL)."""
+    m = golden["c_gt/m"]
+    mask = golden["c_gt/mask"]
+    spec = L.make_spec("fft", m.shape)
+    cfg = L.CompletionConfig(spec=spec, max_iters=15, tol=1e-12, reimpose_observed=True)
+    x, trace = L.pga_complete(m, mask, cfg, ground_truth=m, group="world")
+    ref, rtrace = L.pga_complete(m, mask, cfg, ground_truth=m)
+    assert x.dtype == np.float64 and x.shape == m.shape
+    assert trace.iterations == rtrace.iterations
+    np.testing.assert_allclose([r.rse for r in trace.records], [r.rse for r in rtrace.records], rtol=1e-8)
+    assert rel_err(x, ref) < 1e-10
+    rng = np.random.default_rng(21)
+    a = rng.standard_normal((30, 7, 3, 4))
+    b = rng.standard_normal((7, 20, 3, 4))
+    pspec = L.make_spec("dct", (30, 20, 3, 4))
+    assert rel_err(L.l_product(a, b, pspec, group="world"), L.l_product(a, b, pspec)) < 1e-12
+    xs = rng.standard_normal((18, 14, 5))
+    sspec = L.make_spec("fft", xs.shape)
+    assert rel_err(L.svt(xs, 0.7, sspec, group="world"), L.svt(xs, 0.7, sspec)) < 1e-10
