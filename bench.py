@@ -266,16 +266,16 @@ def run_ours_dist(args):
     c = nat.DeviceArray(plan.c_shape, np.float32)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     # parity gate: this rank's rows of C against the oracle on a bounded row sample
-    plan.run(a, b, c)
+    plan.run_fused(a, b, c)
     torch.cuda.synchronize()
     gate = _parity_gate(c.numpy(), a_h, b_h)
     for _ in range(2):
-        plan.run(a, b, c)
+        plan.run_fused(a, b, c)
     torch.cuda.synchronize()
     l0 = nat.launch_count()
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
-        plan.run(a, b, c)
+        plan.run_fused(a, b, c)
     launches_per_step = nat.launch_count() - l0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
@@ -427,18 +427,24 @@ def run_ours(args):
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     step_ms = []
-    # the step (K1(A), K1(B), K2, K1') is captured once as ONE CUDA graph and
-    # replayed (no per-kernel host enqueue cost; kernels run back to back); each
-    # phase is also captured as its own graph for the per-kernel breakdown
-    # (CUDA events recorded between phase replays on the launching stream)
+    # the step is the product path: ONE persistent tcgen05 kernel (forward transforms, slice
+    # GEMMs, inverse transform; ltb_l_product_device, csrc/ltb_lprod_fused.cuh) captured as a
+    # CUDA graph and replayed.  The four-launch path (K1(A,B), K2, K1') is timed beside it, as a
+    # whole and per phase (one graph per phase, CUDA events between the replays)
     for _ in range(2):
-        plan.run(a, b, c)  # settle kernel attributes / tensor-map caches before capture
+        plan.run_fused(a, b, c)  # settle kernel attributes / tensor-map caches before capture
+        plan.run(a, b, c)
     torch.cuda.synchronize()
+    gate_fused = _parity_gate(c.numpy(), a_h, b_h)
     l0 = nat.launch_count()
     full = torch.cuda.CUDAGraph()
     with torch.cuda.graph(full, stream=stream):
-        plan.run(a, b, c)
+        plan.run_fused(a, b, c)
     launches_per_step = nat.launch_count() - l0
+    four = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(four, stream=stream):
+        plan.run(a, b, c)
+    four_ms = []
     # per-phase graphs (K1 of A and B is one launch when the plan pairs them)
     E_a, E_b, E_c = 256 * 128 * 96, 128 * 256 * 96, 256 * 256 * 96
     phase_defs = {0: ("transform_fwd_A", 8 * E_a, 70 * E_a, "one f32 read + one write of A"),
@@ -479,6 +485,13 @@ def run_ours(args):
             ev[1].synchronize()
             step_ms.append(ev[0].elapsed_time(ev[1]))
         barrier()
+        for _ in range(args.steps):
+            flush.zero_()
+            ev[0].record(stream)
+            four.replay()
+            ev[1].record(stream)
+            ev[1].synchronize()
+            four_ms.append(ev[0].elapsed_time(ev[1]))
         for _ in range(args.steps):
             flush.zero_()
             phases(lambda i: ev[i].record(stream))
@@ -526,30 +539,26 @@ def run_ours(args):
     value = ws * GFLOP_CFG2 * args.steps / t_step / 1e9
     e2e_value = ws * GFLOP_CFG2 * len(e2e_t) / e2e_total / 1e9
 
-    # roofline of the dominant kernel of the step (per-phase CUDA events on the launching stream)
+    # roofline of the step's one kernel: the whole product's algorithmic bytes (one read of A
+    # and B, one write of C: SURVEY.md section 8(d), 50,331,648 B) over its device time (CUDA
+    # events on the launching stream around the graph, which holds only that kernel)
+    t_kernel = t_step / args.steps
+    fused_bytes = 4 * (E_a + E_b + E_c)
+    achieved = fused_bytes / t_kernel / 1e9
+    roof = {"kernel": "lprod_fused_kernel (the whole product, one launch)", "bound": "hbm", "achieved": achieved,
+            "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "peak_source": f"{peak_src} HBM copy (MEASURED_PEAKS.json)",
+            "alg_per_launch": f"{fused_bytes} B (A and B read once, C written once)",
+            "traffic": _ncu_traffic("lprod_fused_kernel"),
+            # the three-phase algorithm moves every transform-domain stack through memory:
+            # A, B, A-hat, B-hat, C-hat, C once each = 151 MB ("unfused")
+            "phase_level_bytes": 4 * 3 * (E_a + E_b + E_c),
+            "phase_level_frac": 4 * 3 * (E_a + E_b + E_c) / t_kernel / 1e9 / hbm_peak}
     names = [phase_defs[i][0] for i in phase_ids]
-    alg_bytes = [phase_defs[i][1] for i in phase_ids]
-    alg_flops = [phase_defs[i][2] for i in phase_ids]
-    alg_desc = [phase_defs[i][3] for i in phase_ids]
     phase_avg = phase_ms / args.steps
-    dom = int(np.argmax(phase_avg))
-    # each phase's roofline is the binding resource at its arithmetic intensity:
-    # t_min = max(flop / tensor peak, bytes / HBM peak)
-    t_flop = alg_flops[dom] / (tf_peak * 1e12)
-    t_byte = alg_bytes[dom] / (hbm_peak * 1e9)
-    if t_flop > t_byte:
-        achieved = alg_flops[dom] / (phase_avg[dom] / 1e3) / 1e12
-        roof = {"kernel": names[dom], "bound": "tensor", "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s",
-                "frac": achieved / tf_peak, "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
-                "alg_per_launch": f"{alg_flops[dom]} flop"}
-    else:
-        achieved = alg_bytes[dom] / (phase_avg[dom] / 1e3) / 1e9
-        roof = {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "peak_source": f"{peak_src} HBM copy (MEASURED_PEAKS.json)",
-                "alg_per_launch": f"{alg_bytes[dom]} B ({alg_desc[dom]})",
-                "arith_intensity_flop_per_byte": alg_flops[dom] / alg_bytes[dom]}
-    roof["traffic"] = _ncu_traffic(names[dom])
-    roof["phase_ms"] = dict(zip(names, [round(float(x), 5) for x in phase_avg]))
+    four_phase = {"ms_per_step": float(np.mean(four_ms)),
+                  "phase_ms": dict(zip(names, [round(float(x), 5) for x in phase_avg])),
+                  "note": "the four-launch path (K1(A,B) paired, K2, K1') on the same buffers, for comparison"}
 
     line = {
         "metric": "*_L-product GFLOP/s",
@@ -567,8 +576,10 @@ def run_ours(args):
         "config": dict(CONFIG2),
         "l2": L2_NOTE,
         "parallelism": "single GPU",
-        "parity_gate": {"device_step": gate, "e2e_pageable": gate_e2e, "ok": gate["ok"] and gate_e2e["ok"]},
+        "parity_gate": {"device_step": gate_fused, "four_phase": gate, "e2e_pageable": gate_e2e,
+                        "ok": gate["ok"] and gate_fused["ok"] and gate_e2e["ok"]},
         "roofline": roof,
+        "four_phase": four_phase,
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": int(a_h.nbytes + b_h.nbytes),
                 "d2h_bytes_per_step": int(out.nbytes), "api": "paper_2202_02870_b200.l_product(numpy, numpy, spec, out=numpy) on pinned host arrays"},
         "e2e_pageable": {"value": GFLOP_CFG2 * len(e2e_pg) / sum(e2e_pg) / 1e9, "unit": "GFLOP/s",

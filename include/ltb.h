@@ -235,6 +235,19 @@ int ltb_project_omega(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const
 int ltb_pga_gradient(ltb_ctx* ctx, int dtype, int64_t n, const void* d_xc, const void* d_xp,
                      const void* d_pobs, const uint8_t* d_mask, double beta, void* d_y, void* d_g);
 
+/* l_product (linalg.py:34-43) on device buffers (A: I1 x L x trailing, B: L x I2 x trailing,
+ * C: I1 x I2 x trailing, C-order, real dtype of a real spec).  fused != 0 runs the fp32 product
+ * as ONE persistent tcgen05 kernel (forward transforms, slice GEMMs and inverse transform
+ * overlapped through per-group completion counters) when the shape fits (I1 % 128 == 0,
+ * P <= 96); otherwise K1(A), K1(B), K2, K1'.  d_ws: ltb_l_product_ws_bytes() bytes.
+ * fused == 3: as 1, and the caller guarantees that d_ws was zero-filled once and has since
+ * been used only by completed fused calls (the kernel leaves its counters zeroed), which
+ * saves the per-call counter reset (a memset node in a CUDA graph).
+ * Stream-ordered, no host synchronisation (CUDA-graph capturable). */
+int64_t ltb_l_product_ws_bytes(const ltb_spec* spec, int64_t I1, int64_t L, int64_t I2, int dtype);
+int ltb_l_product_device(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1, int64_t L, int64_t I2, int dtype,
+                         const void* d_a, const void* d_b, void* d_c, void* d_ws, int64_t ws_bytes, int fused);
+
 /* ---------------------------------------------------------------- sharded PGA (multi-GPU)
  * One iteration of pga_complete (completion.py:165-197) on a rank's shard, for a caller that
  * runs the collectives between the steps: every step is

@@ -85,6 +85,8 @@ _SIGNATURES = {
     "ltb_pga_current": ([_vp, C.POINTER(_vp)], _int),
     "ltb_pga_destroy": ([_vp], None),
     "ltb_pack_mask": ([_vp, _i64, _vp, _vp], _int),
+    "ltb_l_product_ws_bytes": ([_vp, _i64, _i64, _i64, _int], _i64),
+    "ltb_l_product_device": ([_vp, _vp, _i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _i64, _int], _int),
     "ltb_pga_shard_forward": ([_vp, _vp, _int, _i64, C.c_double, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "ltb_pga_shard_svt": ([_vp, _int, _i64, _i64, _i64, _vp, C.c_double, _vp, _vp, _int, _vp], _int),
     "ltb_pga_shard_inverse": ([_vp, _vp, _int, _i64, C.c_double, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),

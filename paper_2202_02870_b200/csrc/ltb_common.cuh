@@ -181,6 +181,12 @@ int ltb_tc_gemm_f32(ltb_ctx* ctx, int64_t batch, int64_t M, int64_t N, int64_t K
                     const int* klim = nullptr, const float* rscale = nullptr, const float* cscale = nullptr,
                     const int* skip = nullptr);
 
+// fused one-launch fp32 *_L product (ltb_lprod_fused.cuh): workspace bytes, and the launch
+// (LTB_EUNSUPPORTED when the shape / spec does not fit; the caller then runs three launches)
+int64_t ltb_lprod_fused_ws_bytes(int64_t P, int64_t I1, int64_t L, int64_t I2);
+int ltb_lprod_fused_f32(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1, int64_t L, int64_t I2, const float* A,
+                        const float* B, float* C, void* ws, bool ws_clean);
+
 // ------------------------------------------------------------------ errors
 int ltb_set_error(ltb_ctx* ctx, int code, const char* fmt, ...);
 

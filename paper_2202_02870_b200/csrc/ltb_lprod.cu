@@ -172,3 +172,46 @@ extern "C" int ltb_l_product_host(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1
   LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return LTB_OK;
 }
+
+// ---------------------------------------------------------------- device-resident product
+// l_product (linalg.py:34-43) on device buffers: the fused one-launch kernel for fp32 real
+// specs (ltb_lprod_fused.cuh), otherwise K1(A), K1(B), K2, K1' through the workspace.
+extern "C" int64_t ltb_l_product_ws_bytes(const ltb_spec* spec, int64_t I1, int64_t L, int64_t I2, int dtype) {
+  if (!spec || I1 < 0 || L < 0 || I2 < 0) return 0;
+  const int64_t P = spec->P;
+  const int64_t hs = dtype_size(spec->is_complex ? (dtype_is_double(dtype) ? LTB_C128 : LTB_C64) : dtype);
+  const int64_t three = hs * P * (I1 * L + L * I2 + I1 * I2) + 256;
+  return std::max<int64_t>(three, dtype == LTB_F32 ? ltb_lprod_fused_ws_bytes(P, I1, L, I2) : 0);
+}
+
+extern "C" int ltb_l_product_device(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1, int64_t L, int64_t I2, int dtype,
+                                    const void* d_a, const void* d_b, void* d_c, void* d_ws, int64_t ws_bytes,
+                                    int fused) {
+  if (!spec) return ltb_set_error(ctx, LTB_ETRANSFORM, "null spec");
+  if (I1 < 0 || L < 0 || I2 < 0) return ltb_set_error(ctx, LTB_ESHAPE, "l_product: negative dimension");
+  if (dtype != LTB_F32 && dtype != LTB_F64) return ltb_set_error(ctx, LTB_EPARAM, "l_product: real dtype expected");
+  if (spec->is_complex) return LTB_EUNSUPPORTED;  // complex transform domains: the generic path
+  if (ws_bytes < ltb_l_product_ws_bytes(spec, I1, L, I2, dtype))
+    return ltb_set_error(ctx, LTB_EPARAM, "l_product: workspace too small");
+  const int64_t P = spec->P;
+  if (I1 == 0 || I2 == 0 || P == 0) return LTB_OK;
+  if ((fused & 1) && dtype == LTB_F32) {
+    const int st = ltb_lprod_fused_f32(ctx, spec, I1, L, I2, (const float*)d_a, (const float*)d_b, (float*)d_c, d_ws,
+                                       (fused & 2) != 0);
+    if (st != LTB_EUNSUPPORTED) return st;
+  }
+  const size_t es = dtype == LTB_F32 ? 4 : 8;
+  char* hA = (char*)d_ws;
+  char* hB = hA + es * P * I1 * L;
+  char* hC = hB + es * P * L * I2;
+  if (I1 * L == L * I2)
+    LTB_TRY(ltb_transform_pair_impl(ctx, spec, I1 * L, 0, dtype, LTB_TUBE_MAJOR, d_a, d_b, dtype, LTB_SLICE_MAJOR, hA,
+                                    hB));
+  else {
+    LTB_TRY(ltb_transform_impl(ctx, spec, I1 * L, 0, dtype, LTB_TUBE_MAJOR, d_a, dtype, LTB_SLICE_MAJOR, hA, nullptr));
+    LTB_TRY(ltb_transform_impl(ctx, spec, L * I2, 0, dtype, LTB_TUBE_MAJOR, d_b, dtype, LTB_SLICE_MAJOR, hB, nullptr));
+  }
+  LTB_TRY(ltb_gemm_impl(ctx, dtype, P, I1, I2, L, LTB_OP_N, hA, L, I1 * L, LTB_OP_N, hB, I2, L * I2, hC, I2, I1 * I2,
+                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr));
+  return ltb_transform_impl(ctx, spec, I1 * I2, 1, dtype, LTB_SLICE_MAJOR, hC, dtype, LTB_TUBE_MAJOR, d_c, nullptr);
+}

@@ -1325,3 +1325,6 @@ extern "C" int ltb_tc_debug_mma_rate(int bn, int pattern, int iters, unsigned lo
     default: return LTB_EPARAM;
   }
 }
+
+// the fused one-launch *_L product (shares this file's helpers)
+#include "ltb_lprod_fused.cuh"

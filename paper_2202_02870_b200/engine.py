@@ -39,6 +39,12 @@ class LProductPlan:
         self._sums = (C.c_double * 2)()
         # K1(A) and K1(B) as one call (one tensor-core launch) when the tube counts match
         self.paired = self.m * self.k == self.k * self.n
+        # whole-product entry (ltb_l_product_device): one persistent kernel for fp32 real specs
+        self.real_spec = not np.iscomplexobj(np.zeros(0, self.hat_dtype))
+        code = nat.dtype_code(self.src_dtype)
+        self.ws_bytes = int(nat.lib().ltb_l_product_ws_bytes(self.handle.ptr, self.m, self.k, self.n, code))
+        # zero-filled once: the fused kernel leaves its counters zeroed after every launch
+        self.ws = nat.DeviceArray.zeros((max(self.ws_bytes, 16),), np.uint8) if self.real_spec else None
 
     def flops(self) -> int:
         """Algorithmic flop count: slice GEMM + separable real transforms."""
@@ -50,6 +56,16 @@ class LProductPlan:
         """Minimal fused HBM traffic: read A, B, write C."""
         s = nat.real_of(self.hat_dtype).itemsize
         return s * (self.m * self.k + self.k * self.n + self.m * self.n) * self.P
+
+    def run_fused(self, a: nat.DeviceArray, b: nat.DeviceArray, c: nat.DeviceArray, fused: bool = True):
+        """The whole product through ltb_l_product_device: one persistent tcgen05 kernel (forward
+        transforms, slice GEMMs and inverse transform overlapped) when the shape fits, else the
+        four phases; real transform domains only."""
+        if not self.real_spec:
+            return self.run(a, b, c)
+        nat.check(nat.lib().ltb_l_product_device(nat.context(), self.handle.ptr, self.m, self.k, self.n, a.code, a.ptr,
+                                                 b.ptr, c.ptr, self.ws.ptr, self.ws_bytes, 3 if fused else 0))
+        return c
 
     def run(self, a: nat.DeviceArray, b: nat.DeviceArray, c: nat.DeviceArray, marks=None, check_real=False,
             phases=(0, 1, 2, 3)):

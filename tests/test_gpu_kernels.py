@@ -5,6 +5,7 @@ both slice orientations, the layout-only transform, reductions."""
 import ctypes as C
 
 import numpy as np
+import paper_2202_02870_b200 as L
 import pytest
 
 from paper_2202_02870_b200 import _native as nat
@@ -305,3 +306,35 @@ def test_host_device_copies_pageable_and_pinned(nbytes):
     np.testing.assert_array_equal(pin.view(np.uint32), x.view(np.uint32))
     d2 = nat.DeviceArray.from_numpy(pin)
     np.testing.assert_array_equal(d2.numpy().view(np.uint32), x.view(np.uint32))
+
+
+@pytest.mark.parametrize("i1,l,i2,trail", [
+    (256, 128, 256, (3, 32)),   # BASELINE config 2
+    (128, 40, 384, (3, 32)),    # L not a multiple of 32 (partial GEMM k-block), three column blocks
+    (384, 64, 128, (4, 8)),     # P = 32: one k-block, three row blocks
+    (128, 16, 128, (3, 8)),     # P = 24: partial transform k-block (zero-filled)
+    (128, 40, 200, (3, 32)),    # I2 % 128 != 0: the four-launch path
+])
+def test_lprod_fused_kernel(i1, l, i2, trail):
+    """The one-launch persistent *_L product (ltb_lprod_fused.cuh) against the fp64 oracle
+    and against the four-launch path on the same buffers."""
+    import ltensor_oracle as O
+    from paper_2202_02870_b200.engine import LProductPlan
+
+    rng = np.random.default_rng(i1 + l + i2)
+    a_h = rng.standard_normal((i1, l) + trail, dtype=np.float32)
+    b_h = rng.standard_normal((l, i2) + trail, dtype=np.float32)
+    spec = L.make_spec("dct", (i1, i2) + trail)
+    plan = LProductPlan(a_h.shape, b_h.shape, spec, np.float32)
+    a = nat.DeviceArray.from_numpy(a_h)
+    b = nat.DeviceArray.from_numpy(b_h)
+    c = nat.DeviceArray(plan.c_shape, np.float32)
+    c4 = nat.DeviceArray(plan.c_shape, np.float32)
+    for _ in range(2):  # counters are reset per launch
+        plan.run_fused(a, b, c)
+    plan.run_fused(a, b, c4, fused=False)
+    ref = O.l_product(a_h.astype(np.float64), b_h.astype(np.float64), O.ospec("dct", (i1, i2) + trail))
+    got = c.numpy()
+    assert np.isfinite(got).all()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-4
+    assert np.linalg.norm(got - c4.numpy()) / np.linalg.norm(ref) < 1e-5
