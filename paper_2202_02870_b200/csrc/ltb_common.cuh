@@ -144,6 +144,7 @@ struct ltb_ctx {
   int opt_force_blocked = 0;                       // route every SVD through the blocked Jacobi tier
   unsigned long long* opt_tc_timeline = nullptr;   // tcgen05 kernels: per-tile clock stamps (CTA 0)
   unsigned long long* opt_qr_timeline = nullptr;   // QR-preconditioned Jacobi: stage stamps (CTA 0)
+  int opt_jacobi_pairs = 0;  // warm Cholesky Jacobi: 0 four-column blocks, 1 one pair per team, 2 two-column blocks
 };
 
 struct ltb_spec {

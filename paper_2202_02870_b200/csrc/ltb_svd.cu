@@ -1032,8 +1032,294 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
 // scaled Gram matrix is well conditioned, and much shorter than the Householder QR.
 // SLOTS: most pairs per team per round (1 when the teams cover every pair: the slot
 // arrays then stay in registers instead of spilling to local memory)
-template <int TS, int MPL, int MINB, bool CHOL = false, int SLOTS = 4>
-__global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
+// rotation parameters of one Jacobi pair (fp32, MUFU): on return c, sn, sg and tt describe
+// the rotation w_p' = c w_p - sn sg w_q, w_q' = sn w_p + c sg w_q and the analytic norm
+// update alpha' = alpha - tt |g|, beta' = beta + tt |g|; a pair below the threshold (or with
+// norms / inner product below FLT_MIN) gets the identity (c = 1, sn = tt = 0, sg = 1), which
+// leaves both columns bit-identical.  Returns whether the pair rotates; rel = |g| / sqrt(ab).
+__device__ __forceinline__ bool jacobi_pair_params(float g, float al, float be, float tol, float& c, float& sn,
+                                                   float& sg, float& tt, float& gabs, float& rel) {
+  gabs = fabsf(g);
+  const float sab = sqrt_apx(al) * sqrt_apx(be);
+  const bool doit = (gabs > tol * sab) && (fminf(fminf(al, be), gabs) >= FLT_MIN);
+  const float zeta = (be - al) * (0.5f * rcp_apx(gabs));
+  const float az = fabsf(zeta);
+  const float den = az < 1e18f ? az + sqrt_apx(fmaf(az, az, 1.f)) : 2.f * az;
+  tt = copysignf(rcp_apx(den), zeta);
+  const float x1 = fmaf(tt, tt, 1.f);
+  float cc = rsqrt_apx(x1);
+  cc = cc * fmaf(-0.5f * x1 * cc, cc, 1.5f);
+  rel = doit ? gabs * rcp_apx(sab) : 0.f;
+  c = doit ? cc : 1.f;
+  sn = doit ? cc * tt : 0.f;
+  tt = doit ? tt : 0.f;
+  sg = (doit && g < 0.f) ? -1.f : 1.f;
+  gabs = doit ? gabs : 0.f;  // (a NaN inner product must not reach the norm updates)
+  return doit;
+}
+
+// Block-pair one-sided Jacobi sweeps over the n columns of W (n rows each, n % 4 == 0,
+// blockDim.x == 2 n): the columns form n / 2 blocks of two, the circle method pairs the
+// blocks (n / 2 - 1 rounds of n / 4 block pairs), and one 8-lane team takes one block pair
+// per round: it loads the four columns into registers (MPL rows per lane, two rows per
+// 8-byte access), rotates the four cross pairs in two steps of two disjoint pairs (plus the
+// two within-block pairs in the sweep's first round), and stores the four columns back.
+// Against one pair per team per round this halves the rounds, the barriers and the
+// shared-memory traffic per rotation (the one-pair kernel is bound by that traffic,
+// ~1.4 us per round on a config-3 slice); the four columns need ~72 registers per thread,
+// which the 288-thread CTAs (two per SM) allow.  Same rotations, thresholds, analytic norm
+// updates and stopping rules as the one-pair path.  Returns the number of sweeps run.
+template <int MPL>
+__device__ int jacobi_block_sweeps(float* W, int pitch, int n, float* nrm, int* flags, int* smax, float tol,
+                                   int max_sweeps, float early_stop) {
+  constexpr int H = MPL / 2;  // float2 per lane per column
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int team = tid >> 3, tl = tid & 7;
+  const int nbk = n >> 1, m1 = nbk - 1;
+  float* const Wc = W + 2 * tl;
+  int sweeps_done = 0;
+  for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
+    int* rot = &flags[sweep & 1];
+    for (int j = warp; j < n; j += nwarps) {
+      const float* wj = W + (size_t)j * pitch;
+      float s2 = 0.f;
+      for (int i = lane; i < n; i += 32) s2 += wj[i] * wj[i];
+      s2 = warp_sum(s2);
+      if (lane == 0) nrm[j] = s2;
+    }
+    __syncthreads();
+    int P = team == 0 ? m1 : team, Q = team == 0 ? 0 : m1 - team;
+    for (int r = 0; r < m1; ++r) {
+      const int col[4] = {2 * P, 2 * P + 1, 2 * Q, 2 * Q + 1};
+      float2 X[4][H];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < H; ++h) X[k][h] = *reinterpret_cast<const float2*>(Wc + (size_t)col[k] * pitch + 16 * h);
+      float nr[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nr[k] = nrm[col[k]];
+      bool any = false;
+      float worst = 0.f;
+      // steps: (0,1)(2,3) within the blocks on the first round; then (0,2)(1,3), (0,3)(1,2)
+#pragma unroll
+      for (int st = 0; st < 3; ++st) {
+        if (st == 0 && r != 0) continue;
+        const int a0 = 0, b0 = st == 0 ? 1 : (st == 1 ? 2 : 3);
+        const int a1 = st == 0 ? 2 : 1, b1 = st == 0 ? 3 : (st == 1 ? 3 : 2);
+        float2 u0 = make_float2(0.f, 0.f), u1 = u0, v0 = u0, v1 = u0;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          if (h & 1) {
+            u1 = __ffma2_rn(X[a0][h], X[b0][h], u1);
+            v1 = __ffma2_rn(X[a1][h], X[b1][h], v1);
+          } else {
+            u0 = __ffma2_rn(X[a0][h], X[b0][h], u0);
+            v0 = __ffma2_rn(X[a1][h], X[b1][h], v0);
+          }
+        }
+        float g0 = (u0.x + u1.x) + (u0.y + u1.y), g1 = (v0.x + v1.x) + (v0.y + v1.y);
+#pragma unroll
+        for (int off = 4; off > 0; off >>= 1) {
+          g0 += __shfl_xor_sync(0xffffffffu, g0, off);
+          g1 += __shfl_xor_sync(0xffffffffu, g1, off);
+        }
+        float c0, s0, sg0, t0, ga0, r0, c1, s1, sg1, t1, ga1, r1;
+        any |= jacobi_pair_params(g0, nr[a0], nr[b0], tol, c0, s0, sg0, t0, ga0, r0);
+        any |= jacobi_pair_params(g1, nr[a1], nr[b1], tol, c1, s1, sg1, t1, ga1, r1);
+        worst = fmaxf(worst, fmaxf(r0, r1));
+        const float2 C0 = make_float2(c0, c0), S0 = make_float2(s0, s0), N0 = make_float2(-s0 * sg0, -s0 * sg0),
+                     Q0 = make_float2(c0 * sg0, c0 * sg0);
+        const float2 C1 = make_float2(c1, c1), S1 = make_float2(s1, s1), N1 = make_float2(-s1 * sg1, -s1 * sg1),
+                     Q1 = make_float2(c1 * sg1, c1 * sg1);
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const float2 xa = X[a0][h], xb = X[b0][h], ya = X[a1][h], yb = X[b1][h];
+          X[a0][h] = __ffma2_rn(C0, xa, __fmul2_rn(N0, xb));
+          X[b0][h] = __ffma2_rn(S0, xa, __fmul2_rn(Q0, xb));
+          X[a1][h] = __ffma2_rn(C1, ya, __fmul2_rn(N1, yb));
+          X[b1][h] = __ffma2_rn(S1, ya, __fmul2_rn(Q1, yb));
+        }
+        nr[a0] = fmaxf(nr[a0] - t0 * ga0, 0.f);
+        nr[b0] = nr[b0] + t0 * ga0;
+        nr[a1] = fmaxf(nr[a1] - t1 * ga1, 0.f);
+        nr[b1] = nr[b1] + t1 * ga1;
+      }
+      if (any) {  // team-uniform: the four columns changed
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int h = 0; h < H; ++h) *reinterpret_cast<float2*>(Wc + (size_t)col[k] * pitch + 16 * h) = X[k][h];
+        if (tl == 0) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) nrm[col[k]] = nr[k];
+          *rot = 1;
+          atomicMax(&smax[sweep & 1], __float_as_int(worst));
+        }
+      }
+      P = team == 0 ? m1 : (P + 1 == m1 ? 0 : P + 1);
+      Q = Q + 1 == m1 ? 0 : Q + 1;
+      __syncthreads();
+    }
+    const int anyr = *rot;
+    const float worst = __int_as_float(smax[sweep & 1]);
+    __syncthreads();
+    if (tid == 0) flags[(sweep + 1) & 1] = smax[(sweep + 1) & 1] = 0;
+    __syncthreads();
+    sweeps_done = sweep + 1;
+    if (!anyr || worst < early_stop) break;
+  }
+  return sweeps_done;
+}
+
+// One step of the 4-column-block Jacobi (jacobi_block4_sweeps): four disjoint pairs
+// (A_j, B_j) of the team's eight register columns.  The four inner products are reduced over
+// the team's 16 lanes in five shuffles (after the first two levels each lane keeps one of the
+// four sums), lanes 4j..4j+3 compute pair j's rotation, and its (c sg, sn, tt |g|) reach the
+// other lanes by shuffles; the rotations then run two pairs per FFMA2.
+template <int R, int A0, int B0, int A1, int B1, int A2, int B2, int A3, int B3>
+__device__ __forceinline__ void blk4_step(float (&X)[8][R], float* nrm, int p4, int q4, int tl, int lane, float tol,
+                                          bool& any, float& worst) {
+  float2 d01 = make_float2(0.f, 0.f), d23 = d01, e01 = d01, e23 = d01;
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    if (h & 1) {
+      e01 = __ffma2_rn(make_float2(X[A0][h], X[A1][h]), make_float2(X[B0][h], X[B1][h]), e01);
+      e23 = __ffma2_rn(make_float2(X[A2][h], X[A3][h]), make_float2(X[B2][h], X[B3][h]), e23);
+    } else {
+      d01 = __ffma2_rn(make_float2(X[A0][h], X[A1][h]), make_float2(X[B0][h], X[B1][h]), d01);
+      d23 = __ffma2_rn(make_float2(X[A2][h], X[A3][h]), make_float2(X[B2][h], X[B3][h]), d23);
+    }
+  }
+  d01 = make_float2(d01.x + e01.x, d01.y + e01.y);
+  d23 = make_float2(d23.x + e23.x, d23.y + e23.y);
+  const bool b3 = tl & 8, b2 = tl & 4;
+  float k0 = b3 ? d23.x : d01.x, k1 = b3 ? d23.y : d01.y;
+  const float s0 = b3 ? d01.x : d23.x, s1 = b3 ? d01.y : d23.y;
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 8);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 8);
+  float f = b2 ? k1 : k0;
+  f += __shfl_xor_sync(0xffffffffu, b2 ? k0 : k1, 4);
+  f += __shfl_xor_sync(0xffffffffu, f, 2);
+  f += __shfl_xor_sync(0xffffffffu, f, 1);
+  // this lane's pair j = 2 b3 + b2: its columns' norms (shared memory, kept by lane 4 j)
+  constexpr int kA = A0 | (A1 << 3) | (A2 << 6) | (A3 << 9), kB = B0 | (B1 << 3) | (B2 << 6) | (B3 << 9);
+  const int sh = 3 * ((b3 ? 2 : 0) + (b2 ? 1 : 0));
+  const int ka = (kA >> sh) & 7, kb = (kB >> sh) & 7;
+  const int ca = (ka < 4 ? p4 : q4) + (ka & 3), cb = (kb < 4 ? p4 : q4) + (kb & 3);
+  const float al = nrm[ca], be = nrm[cb];
+  float c, sn, sg, tt, gabs, rel;
+  const bool doit = jacobi_pair_params(f, al, be, tol, c, sn, sg, tt, gabs, rel);
+  any |= doit;
+  worst = fmaxf(worst, rel);
+  __syncwarp();
+  if ((tl & 3) == 0 && doit) {
+    nrm[ca] = fmaxf(al - tt * gabs, 0.f);
+    nrm[cb] = be + tt * gabs;
+  }
+  __syncwarp();
+  const float qv = c * sg;
+  const int base = lane & 16;
+  float Qj[4], Sj[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    Qj[j] = __shfl_sync(0xffffffffu, qv, base + 4 * j);
+    Sj[j] = __shfl_sync(0xffffffffu, sn, base + 4 * j);
+  }
+  // w_a' = c w_a - sn sg w_b, w_b' = sn w_a + c sg w_b  (c = |c sg|, sg = sign(c sg))
+  const float2 C01 = make_float2(fabsf(Qj[0]), fabsf(Qj[1])), C23 = make_float2(fabsf(Qj[2]), fabsf(Qj[3]));
+  const float2 S01 = make_float2(Sj[0], Sj[1]), S23 = make_float2(Sj[2], Sj[3]);
+  const float2 Q01 = make_float2(Qj[0], Qj[1]), Q23 = make_float2(Qj[2], Qj[3]);
+  const float2 N01 = make_float2(Qj[0] < 0.f ? Sj[0] : -Sj[0], Qj[1] < 0.f ? Sj[1] : -Sj[1]);
+  const float2 N23 = make_float2(Qj[2] < 0.f ? Sj[2] : -Sj[2], Qj[3] < 0.f ? Sj[3] : -Sj[3]);
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const float2 xa = make_float2(X[A0][h], X[A1][h]), xb = make_float2(X[B0][h], X[B1][h]);
+    const float2 ya = make_float2(X[A2][h], X[A3][h]), yb = make_float2(X[B2][h], X[B3][h]);
+    const float2 na = __ffma2_rn(C01, xa, __fmul2_rn(N01, xb)), nb = __ffma2_rn(S01, xa, __fmul2_rn(Q01, xb));
+    const float2 ma = __ffma2_rn(C23, ya, __fmul2_rn(N23, yb)), mb = __ffma2_rn(S23, ya, __fmul2_rn(Q23, yb));
+    X[A0][h] = na.x, X[A1][h] = na.y, X[B0][h] = nb.x, X[B1][h] = nb.y;
+    X[A2][h] = ma.x, X[A3][h] = ma.y, X[B2][h] = mb.x, X[B3][h] = mb.y;
+  }
+}
+
+// Block Jacobi with blocks of four columns (n = 16 R, blockDim.x == 2 n): 16-lane teams
+// hold a block pair (eight columns, R rows per lane at stride 16) in registers, rotate its 16
+// cross pairs in four steps of four disjoint pairs (and the within-block pairs in three more
+// steps on the sweep's first round); n / 4 - 1 rounds per sweep.  Against the two-column
+// blocks this halves the rounds and the shared-memory traffic per rotation again (that
+// traffic bounds both), and the FFMA2s carry two pairs each.  pitch = 4 (mod 8): the two
+// teams of a warp read columns 4P + i, 4(P + 1) + i, whose 64-byte rows then fall in
+// complementary bank halves.  Same rotations, thresholds and stopping rules.
+template <int R>
+__device__ int jacobi_block4_sweeps(float* W, int pitch, int n, float* nrm, int* flags, int* smax, float tol,
+                                    int max_sweeps, float early_stop) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int team = tid >> 4, tl = tid & 15;
+  const int nbk = n >> 2, m1 = nbk - 1;
+  float* const Wc = W + tl;
+  int sweeps_done = 0;
+  for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
+    int* rot = &flags[sweep & 1];
+    for (int j = warp; j < n; j += nwarps) {
+      const float* wj = W + (size_t)j * pitch;
+      float s2 = 0.f;
+      for (int i = lane; i < n; i += 32) s2 += wj[i] * wj[i];
+      s2 = warp_sum(s2);
+      if (lane == 0) nrm[j] = s2;
+    }
+    __syncthreads();
+    int P = team == 0 ? m1 : team, Q = team == 0 ? 0 : m1 - team;
+    for (int r = 0; r < m1; ++r) {
+      float X[8][R];
+      const int p4 = 4 * P, q4 = 4 * Q;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int col = (k < 4 ? p4 : q4) + (k & 3);
+#pragma unroll
+        for (int h = 0; h < R; ++h) X[k][h] = Wc[(size_t)col * pitch + 16 * h];
+      }
+      bool any = false;
+      float worst = 0.f;
+      if (r == 0) {  // the within-block pairs, once per sweep
+        blk4_step<R, 0, 1, 2, 3, 4, 5, 6, 7>(X, nrm, p4, q4, tl, lane, tol, any, worst);
+        blk4_step<R, 0, 2, 1, 3, 4, 6, 5, 7>(X, nrm, p4, q4, tl, lane, tol, any, worst);
+        blk4_step<R, 0, 3, 1, 2, 4, 7, 5, 6>(X, nrm, p4, q4, tl, lane, tol, any, worst);
+      }
+      blk4_step<R, 0, 4, 1, 5, 2, 6, 3, 7>(X, nrm, p4, q4, tl, lane, tol, any, worst);
+      blk4_step<R, 0, 5, 1, 6, 2, 7, 3, 4>(X, nrm, p4, q4, tl, lane, tol, any, worst);
+      blk4_step<R, 0, 6, 1, 7, 2, 4, 3, 5>(X, nrm, p4, q4, tl, lane, tol, any, worst);
+      blk4_step<R, 0, 7, 1, 4, 2, 5, 3, 6>(X, nrm, p4, q4, tl, lane, tol, any, worst);
+      if (__any_sync(0xffffffffu, any)) {  // warp-uniform: store the (possibly) rotated columns
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int col = (k < 4 ? p4 : q4) + (k & 3);
+#pragma unroll
+          for (int h = 0; h < R; ++h) Wc[(size_t)col * pitch + 16 * h] = X[k][h];
+        }
+        const int wbits = __reduce_max_sync(0xffffffffu, __float_as_int(worst));
+        if (lane == 0) {
+          *rot = 1;
+          atomicMax(&smax[sweep & 1], wbits);
+        }
+      }
+      P = team == 0 ? m1 : (P + 1 == m1 ? 0 : P + 1);
+      Q = Q + 1 == m1 ? 0 : Q + 1;
+      __syncthreads();
+    }
+    const int anyr = *rot;
+    const float worst = __int_as_float(smax[sweep & 1]);
+    __syncthreads();
+    if (tid == 0) flags[(sweep + 1) & 1] = smax[(sweep + 1) & 1] = 0;
+    __syncthreads();
+    sweeps_done = sweep + 1;
+    if (!anyr || worst < early_stop) break;
+  }
+  return sweeps_done;
+}
+
+template <int TS, int MPL, int MINB, bool CHOL = false, int SLOTS = 4, int BLK = 0>
+__global__ void __launch_bounds__(BLK ? 288 : (MINB == 2 ? 576 : kJacobiMaxThreads), MINB)
     jacobi_qr_kernel(int64_t I1, int64_t I2, const float* __restrict__ A, JacobiOut o, int max_sweeps, int pitch,
                      unsigned long long* dbg) {
   if (o.skip && *o.skip) return;
@@ -1045,6 +1331,14 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     }
   };
   stamp(0);
+  // per-CTA span and sweeps (dbg[16 + 3 b ..]): start, end of the sweeps, sweep count
+  auto cta_stamp = [&](int slot, unsigned long long v) {
+    if (dbg && threadIdx.x == 0) {
+      if (slot < 2) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+      dbg[16 + 3 * (int64_t)blockIdx.x + slot] = v;
+    }
+  };
+  cta_stamp(0, 0);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const bool trans = I1 < I2;
   const int n = (int)(trans ? I1 : I2);
@@ -1059,7 +1353,20 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
   constexpr int TR = TS * MPL;  // register-tile rows of X (rows n..TR-1 are zero)
 
-  if (CHOL || !trans) {  // (G is symmetric: its rows are its columns)
+  if (CHOL) {  // G is symmetric: row i of G is column i of W (16-byte copies when rows allow)
+    if ((n & 3) == 0) {
+      const int n4 = n >> 2;
+      for (int l = tid; l < n * n4; l += nth) {
+        const int i = l / n4, j4 = l - i * n4;
+        *reinterpret_cast<float4*>(W + (size_t)i * pitch + 4 * j4) = reinterpret_cast<const float4*>(Ab)[l];
+      }
+    } else {
+      for (int l = tid; l < n * n; l += nth) {
+        const int i = l / n, j = l - i * n;
+        W[(size_t)i * pitch + j] = Ab[l];
+      }
+    }
+  } else if (!trans) {
     for (int l = tid; l < m * n; l += nth) {
       const int i = l / n, j = l - i * n;
       W[(size_t)j * pitch + i] = Ab[l];
@@ -1160,56 +1467,135 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   stamp(4);
   } else {
     // ---- Cholesky G = L L^T in place (column j of L in column j, rows >= j); a non-positive
-    // pivot (rank-deficient slice) zeroes its column.  Blocked right-looking: warp 0 factors
-    // a panel of CB columns (warp-synchronous), then every warp applies the panel's rank-CB
-    // update to the trailing columns with the panel entries of its column in registers
-    // (CB + 2 shared-memory accesses per CB FMAs instead of 3 per FMA, two block barriers
-    // per panel instead of one per column).
-    constexpr int CB = 8;
+    // pivot (rank-deficient slice) zeroes its column.  Blocked right-looking with panels of
+    // CB = 16 columns, three block barriers per panel:
+    //   (1) the CB x CB diagonal block is factored by warp 0 in registers (lane r holds row r,
+    //       pivots and multipliers by shuffles: no shared-memory round trips on the n-step
+    //       critical path);
+    //   (2) the panel rows below it are solved against it (L21 = A21 L11^-T), one thread per
+    //       row with the row in registers and L11 broadcast from shared memory;
+    //   (3) the trailing update A22 -= L21 L21^T in 4 x 4 register tiles (two 16-byte loads
+    //       per 16 FMAs), lower-triangle tiles only.
+    // (The previous warp-0 panel with per-column update passes took ~140 us of a ~640 us
+    // config-3 slice, latency- and shared-memory-bound.)  pitch is a multiple of 4.
+    constexpr int CB = 16;
+    float* dinv = vhead;  // 1 / L[k][k] (0 for a zeroed column)
     for (int k0 = 0; k0 < n; k0 += CB) {
-      const int kend = min(k0 + CB, n);
+      const int nb = min(CB, n - k0);
       if (warp == 0) {
-        for (int kk = k0; kk < kend; ++kk) {
-          float* wk = W + (size_t)kk * pitch;
-          const float pk = wk[kk];
+        float a[CB];
+        const int r = lane;
+#pragma unroll
+        for (int c = 0; c < CB; ++c) a[c] = (r < nb && c <= r) ? W[(size_t)(k0 + c) * pitch + k0 + r] : 0.f;
+        // (every loop fully unrolled with compile-time indices: a[] stays in registers)
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+          const float pk = __shfl_sync(0xffffffffu, a[c], c);
           const float d = pk >= FLT_MIN ? sqrtf(pk) : 0.f;
           const float inv = d > 0.f ? 1.f / d : 0.f;
-          __syncwarp();
-          if (lane == 0) wk[kk] = d;
-          for (int i = kk + 1 + lane; i < n; i += 32) wk[i] *= inv;
-          __syncwarp();
-          for (int jj = kk + 1; jj < kend; ++jj) {  // the rest of the panel
-            float* wj = W + (size_t)jj * pitch;
-            const float ljk = wk[jj];
-            for (int i = jj + lane; i < n; i += 32) wj[i] = fmaf(-wk[i], ljk, wj[i]);
+          a[c] = r == c ? d : (r > c ? a[c] * inv : a[c]);
+          if (r == c && c < nb) dinv[k0 + c] = inv;
+#pragma unroll
+          for (int jj = 0; jj < CB; ++jj) {
+            if (jj > c) {
+              const float ljc = __shfl_sync(0xffffffffu, a[c], jj);
+              a[jj] = r >= jj ? fmaf(-a[c], ljc, a[jj]) : a[jj];
+            }
           }
-          __syncwarp();
+        }
+        if (r < nb) {
+#pragma unroll
+          for (int c = 0; c < CB; ++c)
+            if (c <= r) W[(size_t)(k0 + c) * pitch + k0 + r] = a[c];
         }
       }
       __syncthreads();
-      const int nk = kend - k0;
-      for (int j = kend + warp; j < n; j += nwarps) {
-        float lj[CB];
+      if (k0 == 0) stamp(8);
+      const int s0 = k0 + nb;
+      if (s0 >= n) break;
+      for (int i = s0 + tid; i < n; i += nth) {  // (2) rows below the diagonal block
+        float a[CB];
 #pragma unroll
-        for (int kk = 0; kk < CB; ++kk) lj[kk] = kk < nk ? W[(size_t)(k0 + kk) * pitch + j] : 0.f;
-        float* wj = W + (size_t)j * pitch;
-        const float* lp = W + (size_t)k0 * pitch;
-        for (int i = j + lane; i < n; i += 32) {
-          float acc = wj[i];
+        for (int c = 0; c < CB; ++c) a[c] = c < nb ? W[(size_t)(k0 + c) * pitch + i] : 0.f;
+        const float* l11 = W + (size_t)k0 * pitch + k0;
 #pragma unroll
-          for (int kk = 0; kk < CB; ++kk)
-            if (kk < nk) acc = fmaf(-lp[(size_t)kk * pitch + i], lj[kk], acc);
-          wj[i] = acc;
+        for (int c = 0; c < CB; ++c) {
+          a[c] *= c < nb ? dinv[k0 + c] : 0.f;
+#pragma unroll
+          for (int jj = 0; jj < CB; ++jj)
+            if (jj > c) a[jj] = fmaf(-a[c], jj < nb ? l11[(size_t)c * pitch + jj] : 0.f, a[jj]);
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+          if (c < nb) W[(size_t)(k0 + c) * pitch + i] = a[c];
+      }
+      __syncthreads();
+      if (k0 == 0) stamp(9);
+      // (3) A22[j][i] -= sum_c L[i][c] L[j][c], s0 <= j <= i < n, 4 x 4 tiles (bi >= bj)
+      const int T = (n - s0 + 3) >> 2;
+      const float* lp = W + (size_t)k0 * pitch;
+      for (int l = tid; l < T * (T + 1) / 2; l += nth) {
+        int bi = (int)((sqrtf(8.f * (float)l + 1.f) - 1.f) * 0.5f);
+        while (bi * (bi + 1) / 2 > l) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= l) ++bi;
+        const int bj = l - bi * (bi + 1) / 2;
+        const int i0 = s0 + 4 * bi, j0 = s0 + 4 * bj;
+        float acc[4][4];
+        const bool full = i0 + 3 < n;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const float* wj = W + (size_t)min(j0 + jj, n - 1) * pitch + i0;
+          if (full) {
+            const float4 v = *reinterpret_cast<const float4*>(wj);
+            acc[jj][0] = v.x, acc[jj][1] = v.y, acc[jj][2] = v.z, acc[jj][3] = v.w;
+          } else {
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) acc[jj][ii] = i0 + ii < n ? wj[ii] : 0.f;
+          }
+        }
+#pragma unroll 4
+        for (int c = 0; c < nb; ++c) {
+          const float* lc = lp + (size_t)c * pitch;
+          float li[4], lj[4];
+          if (full) {
+            const float4 v = *reinterpret_cast<const float4*>(lc + i0);
+            li[0] = v.x, li[1] = v.y, li[2] = v.z, li[3] = v.w;
+          } else {
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) li[ii] = i0 + ii < n ? lc[i0 + ii] : 0.f;
+          }
+          const float4 u = *reinterpret_cast<const float4*>(lc + j0);  // j0 + 3 <= i0 + 3 < pitch
+          lj[0] = u.x, lj[1] = u.y, lj[2] = u.z, lj[3] = u.w;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) acc[jj][ii] = fmaf(-li[ii], lj[jj], acc[jj][ii]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          if (j0 + jj >= n) break;
+          float* wj = W + (size_t)(j0 + jj) * pitch + i0;
+          if (full) {
+            *reinterpret_cast<float4*>(wj) = make_float4(acc[jj][0], acc[jj][1], acc[jj][2], acc[jj][3]);
+          } else {
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii)
+              if (i0 + ii < n) wj[ii] = acc[jj][ii];
+          }
         }
       }
       __syncthreads();
+      if (k0 == 0) stamp(10);
+      if (k0 == 64) stamp(11);
     }
     // X = L: clear the upper triangle and the rows n .. TR-1
+    stamp(3);
     for (int l = tid; l < n * TR; l += nth) {
       const int c = l / TR, r = l - c * TR;
       if (r < c || r >= n) W[(size_t)c * pitch + r] = 0.f;
     }
     __syncthreads();
+    stamp(4);
   }
 
   // ---- one-sided Jacobi on the n columns of X (n rows), as jacobi_kernel's fp32 path
@@ -1229,6 +1615,11 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
   const float* const Wc = W + 2 * tl;
   int* smax = flags + 4;  // per-sweep-parity largest relative rotated |gamma| (float bits; rank_sh later)
   if (tid == 0) smax[0] = smax[1] = 0;
+  if constexpr (BLK == 4) {
+    sweeps_done = jacobi_block4_sweeps<MPL>(W, pitch, n, nrm, flags, smax, tol, max_sweeps, o.early_stop);
+  } else if constexpr (BLK == 2) {
+    sweeps_done = jacobi_block_sweeps<MPL>(W, pitch, n, nrm, flags, smax, tol, max_sweeps, o.early_stop);
+  } else {
   for (int sweep = 0; sweep < max_sweeps && n > 1; ++sweep) {
     int* rot = &flags[sweep & 1];
     for (int j = warp; j < n; j += nwarps) {
@@ -1311,7 +1702,10 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     // there the singular values, and so the SVT's shrink factors, nearly coincide
     if (!any || worst < o.early_stop) break;
   }
+  }
   stamp(5);
+  cta_stamp(1, 0);
+  cta_stamp(2, (unsigned long long)sweeps_done);
   if (o.stats && tid == 0) {
     atomicAdd(&o.stats[0], 1ull);
     atomicAdd(&o.stats[1], (unsigned long long)sweeps_done);
@@ -1385,6 +1779,18 @@ int launch_qr_variant(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const
   return LTB_OK;
 }
 
+// the block-pair Jacobi variant (warm Cholesky path): 2 n threads, two CTAs per SM
+template <int MPL, int BLK>
+int launch_qr_blk(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* A, const JacobiOut& o,
+                  int max_sweeps, int n, int pitch) {
+  const size_t smem = jacobi_qr_smem(n, pitch);
+  auto kern = jacobi_qr_kernel<BLK == 4 ? 16 : 8, MPL, 2, true, 1, BLK>;
+  LTB_TRY(ensure_smem(ctx, kern, smem, true));
+  kern<<<(unsigned)batch, 2 * n, smem, ctx->stream>>>(I1, I2, A, o, max_sweeps, pitch, ctx->opt_qr_timeline);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
+
 // 1 when the QR-preconditioned resident kernel takes this fp32 SVT; 0 to use the others
 constexpr int g_svt_qr = 1;
 constexpr int g_qr_max_sweeps = 40;  // timing hook: 0 measures the QR and emission stages alone
@@ -1415,6 +1821,7 @@ int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const 
   else return LTB_EUNSUPPORTED;
   int pitch = std::max(m, TSv * MPLv);
   pitch += pitch & 1;
+  if (chol) pitch = (pitch + 3) & ~3;  // the Cholesky's 16-byte tile accesses
   // an 8-lane team reads 64 bytes of its column: with pitch = 16 (mod 32) floats the four
   // teams of a warp (consecutive columns) alternate bank halves instead of colliding
   if (TSv == 8) pitch += (16 - pitch % 32 + 32) % 32;
@@ -1422,6 +1829,27 @@ int launch_jacobi_qr(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const 
   if (smem > kSmemLimit) return LTB_EUNSUPPORTED;
   const bool two = 2 * (smem + 1024) <= 228 * 1024;
   const int ms = g_qr_max_sweeps;
+  // warm Cholesky path: the block-pair Jacobi (n / 4 teams of 8 lanes, 2 n <= 288 threads)
+  if (chol && TSv == 8 && n % 4 == 0 && 2 * n <= 288 && ctx->opt_jacobi_pairs != 1) {
+    // pitch = 8 (mod 16) floats: the four teams of a warp read columns 2P (or 2P + 1) of
+    // consecutive blocks P, whose 64-byte chunks then alternate bank halves (with pitch = 16
+    // (mod 32) every even column starts in the same half: 4-way instead of 2-way wavefronts)
+    const int base = std::max(m, TSv * MPLv);
+    if (n % 16 == 0 && ctx->opt_jacobi_pairs == 3) {  // four-column blocks (measured slower: spills at 96 registers)
+      const int bpitch4 = base + ((4 - base) % 8 + 8) % 8;  // 4 (mod 8)
+      const size_t bsm4 = jacobi_qr_smem(n, bpitch4);
+      if (2 * (bsm4 + 1024) <= 228 * 1024) {
+        if (n == 128) return launch_qr_blk<8, 4>(ctx, batch, I1, I2, A, o, ms, n, bpitch4);
+        if (n == 144) return launch_qr_blk<9, 4>(ctx, batch, I1, I2, A, o, ms, n, bpitch4);
+      }
+    }
+    const int bpitch = base + ((8 - base) % 16 + 16) % 16;
+    const size_t bsm = jacobi_qr_smem(n, bpitch);
+    if (2 * (bsm + 1024) <= 228 * 1024) {
+      if (MPLv == 16) return launch_qr_blk<16, 2>(ctx, batch, I1, I2, A, o, ms, n, bpitch);
+      if (MPLv == 18) return launch_qr_blk<18, 2>(ctx, batch, I1, I2, A, o, ms, n, bpitch);
+    }
+  }
 #define LTB_QR(TS_, MPL_)                                                                              \
   if (chol)                                                                                              \
     return two ? launch_qr_variant<TS_, MPL_, 2, true>(ctx, batch, I1, I2, A, o, ms, n, pitch)          \

@@ -261,3 +261,24 @@ def test_config4_reduced_pga_50_iterations():
     np.testing.assert_allclose([r.mu for r in trace.records], [r[1] for r in recs], rtol=1e-14)
     assert [r.t for r in trace.records] == [r[2] for r in recs]
     assert rel_err(x, ref) < 1e-4
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("shape", [(144, 176, 2, 3), (160, 128, 3, 2)])
+def test_warm_jacobi_variants_config3_recipe(variant, shape):
+    """The warm (carried-basis, Cholesky-preconditioned) SVT inside fp32 PGA with each Jacobi
+    variant (LTB_OPT_JACOBI_PAIRS: 0 two-column blocks (default), 1 one pair per team, 2 two-column
+    blocks, 3 four-column blocks) on the config-3 recipe with n = 144 / 128 columns, 80 iterations,
+    against the fp64 oracle trajectory."""
+    from paper_2202_02870_b200 import _native as nat
+
+    m, mask = config3_inputs(O.l_product, O.ospec, shape=shape, rank=4, seed=5)
+    spec = L.make_spec("dct", m.shape)
+    nat.check(nat.lib().ltb_ctx_set_option(nat.context(), nat.OPT_JACOBI_PAIRS, variant))
+    try:
+        x, trace = L.pga_complete(m, mask, L.CompletionConfig(spec=spec, tol=1e-300, max_iters=80), precision="fp32")
+    finally:
+        nat.check(nat.lib().ltb_ctx_set_option(nat.context(), nat.OPT_JACOBI_PAIRS, 0))
+    ref, recs, _ = O.pga_complete(m.astype(np.float64), mask, O.ospec("dct", m.shape), tol=1e-300, max_iters=80)
+    assert trace.iterations == 80
+    assert rel_err(x, ref) < 1e-4

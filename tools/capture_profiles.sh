@@ -2,15 +2,15 @@
 # Round profile capture on the GPU box: bench JSON, launch list of a short bench run, and
 # ncu --set full captures of the top kernels (each command runs once without ncu first).
 set -x
-R=${1:-r01}
+R=${1:-r02}
 mkdir -p gpurun_out/prof
 python bench.py > gpurun_out/prof/${R}_bench.json 2> gpurun_out/prof/${R}_bench.err
 python bench.py --steps 3 --warmup 3 --skip-extras --no-cpu-baseline --pga-iters 60 > /dev/null 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/${R}_launches.csv \
     python bench.py --steps 3 --warmup 3 --skip-extras --no-cpu-baseline --pga-iters 60 > /dev/null 2>&1
-python tools/experiments/pdl_ab.py > /dev/null 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:tc3_kernel -c 3 -o gpurun_out/prof/${R}_tc3 \
-    python tools/experiments/pdl_ab.py > /dev/null 2>&1
+python tools/experiments/lprod_fused_time.py > gpurun_out/prof/${R}_lprod_fused_timeline.txt 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:lprod_fused_kernel -s 3 -c 1 -o gpurun_out/prof/${R}_lprod_fused \
+    python tools/experiments/lprod_fused_time.py > /dev/null 2>&1
 python tools/experiments/prof_pga_late.py 120 2 > /dev/null 2>&1 && \
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:jacobi_qr_kernel -c 1 \
     -o gpurun_out/prof/${R}_jacobi_qr python tools/experiments/prof_pga_late.py 120 2 > /dev/null 2>&1
@@ -25,11 +25,11 @@ ls -la gpurun_out/prof
 # raw CSV per report, then drop the reports themselves
 P=gpurun_out/prof
 python tools/experiments/ncu_summary.py $P/${R}_ncu_summary.md \
-    $P/${R}_tc3.ncu-rep:"config-2 l_product tcgen05 kernels (paired forward K1, slice GEMM K2, inverse K1')" \
+    $P/${R}_lprod_fused.ncu-rep:"config-2 l_product, the one-launch persistent tcgen05 kernel (F, G, I tiles)" \
     $P/${R}_jacobi_qr.ncu-rep:"config-3 PGA K3 (Cholesky-preconditioned Jacobi, warm iteration 121)" \
     $P/${R}_xform_pga.ncu-rep:"config-3 PGA fused transforms (K1 + K4 prologue, K1' + norms epilogue)" \
     $P/${R}_jacobi_block.ncu-rep:"config-4-size blocked Jacobi round (complex64 1024x1024)" \
     --launches $P/${R}_launches.csv:"bench.py --steps 3 --warmup 3 --skip-extras --pga-iters 60"
 for f in $P/*.ncu-rep; do ncu -i $f --page raw --csv > ${f%.ncu-rep}_raw.csv 2>/dev/null; done
-rm -f $P/*.ncu-rep
+mv $P/${R}_lprod_fused.ncu-rep gpurun_out/ 2>/dev/null; rm -f gpurun_out/prof/*.ncu-rep
 du -sh gpurun_out

@@ -7,7 +7,7 @@ from pathlib import Path
 import numpy as np
 import torch
 import torch.distributed as dist
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 import paper_2202_02870_b200 as L  # noqa: E402

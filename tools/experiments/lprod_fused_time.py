@@ -87,3 +87,20 @@ for j in range(NT):
 print("CTA 0 k-blocks: TMA issued, landed (converter), TMEM written, MMA issued")
 for i in range(48):
     print(i, np.round(kb[i], 2))
+# per dependency group: completion (last epilogue done) and first / last claim
+print("groups (F: A0, B0, B1, A1 by 128 tiles; G: (mb,nb) by 96; I: (mb,nb) by 128): done-min / done-max / claim-min / claim-max us")
+allt = []
+for cta in range(148):
+    for j in range(NT):
+        tid = int(tl[cta, j, 0]) - 1
+        if tid >= 0:
+            allt.append((tid, (tl[cta, j, 1] - t0) / 1e3, (tl[cta, j, 6] - t0) / 1e3, (tl[cta, j, 2] - t0) / 1e3, cta))
+allt = np.array(allt)
+bounds = [(0, 128), (128, 256), (256, 384), (384, 512)] + [(512 + 96 * g, 512 + 96 * (g + 1)) for g in range(4)] + \
+    [(896 + 128 * g, 896 + 128 * (g + 1)) for g in range(4)]
+for lo, hi in bounds:
+    sel = allt[(allt[:, 0] >= lo) & (allt[:, 0] < hi)]
+    if len(sel):
+        print(f"  tiles {lo}-{hi}: n={len(sel)} done {sel[:, 2].min():.2f} / {sel[:, 2].max():.2f}  claim {sel[:, 1].min():.2f} / {sel[:, 1].max():.2f}  deps met {sel[:, 3].min():.2f} / {np.median(sel[:, 3]):.2f} / {sel[:, 3].max():.2f}")
+        k = int(np.argmax(sel[:, 2]))
+        print(f"    last done: tile {int(sel[k, 0])} on CTA {int(sel[k, 4])}")

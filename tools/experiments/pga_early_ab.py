@@ -5,7 +5,7 @@ import sys
 import time
 from pathlib import Path
 import numpy as np
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 import paper_2202_02870_b200 as L  # noqa: E402

@@ -3,7 +3,7 @@ import sys
 from pathlib import Path
 import numpy as np
 import torch
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 from paper_2202_02870_b200 import _native as nat  # noqa: E402
 

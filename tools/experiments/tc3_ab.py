@@ -1,7 +1,7 @@
 """A/B of the 3xTF32 engines (A split in shared memory vs A staged in TMEM) on the l_product step."""
 import sys
 from pathlib import Path
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tools"))
 sys.argv = [sys.argv[0]]
 from paper_2202_02870_b200 import _native as nat  # noqa: E402

@@ -1,7 +1,7 @@
 """tcgen05 engine at the l_product shapes with each epilogue mode (CUDA-graph timed)."""
 import sys
 from pathlib import Path
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tools"))
 sys.argv = [sys.argv[0]]

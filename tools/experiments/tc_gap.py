@@ -2,7 +2,7 @@
 import ctypes as C, sys
 from pathlib import Path
 import torch
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 from paper_2202_02870_b200 import _native as nat  # noqa: E402
 lib = nat.lib(); lib.ltb_tc_debug_set_timeline.argtypes = [C.c_void_p]; lib.ltb_tc_debug_set_epi_mode.argtypes = [C.c_int]

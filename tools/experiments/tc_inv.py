@@ -2,7 +2,7 @@
 K-major A, 3xTF32 vs 1xTF32, with and without epilogue stores (CUDA-graph timed)."""
 import sys
 from pathlib import Path
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tools"))
 import torch  # noqa: E402
