@@ -494,7 +494,9 @@ __global__ void __launch_bounds__(kLpThreads, 1)
         __syncwarp();
         if (lane == 0) {
           if constexpr (kLpLsuEpi) {
-            __threadfence();
+            // no separate fence: red.release orders the warp's stores (made visible to this
+            // lane by the __syncwarp above; release is cumulative), and the consumer's
+            // ld.acquire + fence.proxy.async orders them before its TMA loads
           } else {
             bulk_wait_all();
             fence_proxy_async_global();

@@ -62,6 +62,18 @@ __device__ __forceinline__ float rsqrt_apx(float x) {
   return y;
 }
 
+// fp64 MUFU approximations (MUFU.RCP64H / RSQ64H, ~20-bit): Jacobi rotation parameters only
+__device__ __forceinline__ double rcp_apx64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+__device__ __forceinline__ double rsqrt_apx64(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
 // two consecutive elements, one vector shared-memory access (LDS.64 / LDS.128)
 template <typename T> struct alignas(2 * sizeof(T)) vec2 {
   T a, b;
@@ -286,13 +298,36 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
         // one square root for the test, and sqrt(1 + zeta^2) / rsqrt instead of hypot and a
         // division below |zeta| = 1e100 (the rotation chain is the latency of a round)
         constexpr bool DBL = sizeof(R) == 8;  // (fp32 keeps two roots: al * be may overflow)
-        const R sab = DBL ? sqrt(al * be) : sqrt(al) * sqrt(be);
-        if (!active || !(gabs > tol * sab) || al == (R)0 || be == (R)0) continue;
-        const R zeta = (be - al) * ((R)0.5 / gabs);
-        const R az = fabs(zeta);
-        const R den = az < (R)1e18 ? az + sqrt(fma(az, az, (R)1)) : (R)2 * az;
-        const R t = (zeta >= 0 ? (R)1 : (R)-1) / den;
-        const R c = DBL ? rsqrt(fma(t, t, (R)1)) : (R)1 / sqrt(fma(t, t, (R)1));
+        R sab, t, c;
+        if constexpr (DBL) {
+          // fp64: every lane of a team computes the parameters, so the IEEE sqrt / division
+          // sequences (software, tens of DFMAs each) made the rotation chain FP64-throughput
+          // bound.  The threshold test, zeta and t only need ~20 correct bits (an inexact t
+          // leaves a ~1e-6 relative inner product for the next sweep; the rotation stays
+          // orthogonal): MUFU approximations.  c = (1 + t^2)^-1/2 must be exact to fp64 for
+          // orthogonality: MUFU rsqrt + three Newton steps.
+          const double prod = al * be;
+          sab = prod * rsqrt_apx64(prod);
+          if (!active || !(gabs > tol * sab) || al == (R)0 || be == (R)0) continue;
+          const double zeta = (be - al) * (0.5 * rcp_apx64(gabs));
+          const double az = fabs(zeta);
+          const double z1 = fma(az, az, 1.0);
+          const double den = az < 1e18 ? az + z1 * rsqrt_apx64(z1) : 2.0 * az;
+          t = copysign(rcp_apx64(den), zeta);
+          const double x1 = fma(t, t, 1.0);
+          double cc = rsqrt_apx64(x1);
+#pragma unroll
+          for (int it = 0; it < 3; ++it) cc = cc * fma(-0.5 * x1 * cc, cc, 1.5);
+          c = cc;
+        } else {
+          sab = sqrt(al) * sqrt(be);
+          if (!active || !(gabs > tol * sab) || al == (R)0 || be == (R)0) continue;
+          const R zeta = (be - al) * ((R)0.5 / gabs);
+          const R az = fabs(zeta);
+          const R den = az < (R)1e18 ? az + sqrt(fma(az, az, (R)1)) : (R)2 * az;
+          t = (zeta >= 0 ? (R)1 : (R)-1) / den;
+          c = (R)1 / sqrt(fma(t, t, (R)1));
+        }
         const R s = c * t;
         // phase e^{-i phi} applied to column q so the Gram entry becomes real
         T ph;
@@ -349,7 +384,8 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
           // alpha' = alpha - t|gamma|, beta' = beta + t|gamma| for the rotation that zeroes gamma
           nrm[p] = fmax(al - t * gabs, (R)0);
           nrm[q] = be + t * gabs;
-          *rot = 1;
+          // bit 0: the sweep rotated; bit 1: a rotation with |gamma| / sqrt(alpha beta) >= early_stop
+          atomicOr(rot, (o.early_stop > 0.f && gabs >= (R)o.early_stop * sab) ? 3 : 1);
         }
       }
       __syncthreads();
@@ -359,7 +395,10 @@ __global__ void __launch_bounds__(MINB == 2 ? 576 : kJacobiMaxThreads, MINB)
     if (tid == 0) flags[(sweep + 1) & 1] = 0;
     __syncthreads();
     sweeps_done = sweep + 1;
-    if (!any) break;
+    // without rotations the sweep changed nothing; with early_stop (the warm fp64 PGA SVT:
+    // sqrt(tol)), a sweep whose rotations all had relative inner products below it leaves
+    // inner products of order tol behind (quadratic convergence), as in jacobi_qr_kernel
+    if (!(any & 1) || (o.early_stop > 0.f && !(any & 2))) break;
   }
   if (o.stats && tid == 0) {
     atomicAdd(&o.stats[0], 1ull);
@@ -2017,6 +2056,8 @@ namespace {
 // columns w_j = sigma_j u_j are those of G itself (V J is orthogonal), so the usual V-free
 // recomposition with G applies unchanged, and V <- V J for the next call (rounding drift
 // ~1e-16 per call in fp64: no re-orthonormalisation).  warm == 0: A0 = G, V <- J.
+constexpr int g_carry64_early = 1;  // the sqrt(tol) early stop for warm fp64 carried SVTs
+
 int ltb_svt_carry64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const double* G, double tau,
                          double* out, double* V, int warm, const int* skip) {
   const bool trans = I1 < I2;
@@ -2043,6 +2084,9 @@ int ltb_svt_carry64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, co
     src = A0;
   }
   JacobiOut o{w, nullptr, vc, kept, d, tau, skip};
+  // warm calls: stop after a sweep whose rotations all had relative inner products below
+  // sqrt(tol), tol = eps sqrt(m) the rotation threshold (the inner products left are ~tol)
+  if (warm && g_carry64_early) o.early_stop = (float)std::sqrt(DBL_EPSILON * std::sqrt((double)m));
   int st = launch_jacobi<double, true>(ctx, batch, I1, I2, src, o);
   if (st != LTB_OK) return st;
   if (!trans) {
