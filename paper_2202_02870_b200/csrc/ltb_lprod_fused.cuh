@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kLpThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kLpRbStages; ++s) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rfree[s], kConvA);
+      mbar_init(&rfree[s], kConvA + 1);  // converters read it; the MMAs (F tiles: A hi from here) done
     }
     for (int s = 0; s < kLpGStages; ++s) {
       mbar_init(&gfull[s], 1);
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kLpThreads, 1)
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idX = idesc_tf32(kLpBnX, false, false);
     constexpr uint32_t idG = idesc_tf32(kLpBnG, false, true);
-    int it_g = 0, it_t = 0, j = 0, nres = 0, res = -1;
+    int it_g = 0, it_r = 0, it_t = 0, j = 0, nres = 0, res = -1;
     for (;;) {
       const int t = next_tile();
       if (t < 0) break;
@@ -351,31 +351,49 @@ __global__ void __launch_bounds__(kLpThreads, 1)
         tc_fence_after();
         if (lane == 0) lp_kstamp(dbg, it_t, 3);
         const uint32_t ahi = tmem + (uint32_t)(kLpACol + 64 * ts), alo = ahi + 32;
+        // K-major A (F and G tiles): the raw fp32 tile in shared memory is the hi operand
+        // (kind::tf32 reads the top 19 bits, i.e. trunc(x), as for B-hat below), so the
+        // converters write only lo = round(x - trunc(x)) to TMEM
         if (gk) {
           const int s = it_g % kLpGStages;
+          const uint64_t dah0 = umma_desc(smem_u32(g_stage(s)), 16u, 1024u, false);
           const uint64_t dbh0 = umma_desc(smem_u32(g_stage(s) + kLpABytes), g_mn_lbo, g_mn_sbo, true);
           const uint64_t dbl0 = umma_desc(smem_u32(g_stage(s) + kLpABytes + kLpGBBytes), g_mn_lbo, g_mn_sbo, true);
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
-            const uint64_t kof = (uint64_t)((1024u * kk) >> 4);
-            umma_tf32_ta_w(dacc, ahi + 8 * kk, dbh0 + kof, idG, (kt > 0 || kk > 0) ? 1u : 0u);
-            umma_tf32_ta_w(dacc, ahi + 8 * kk, dbl0 + kof, idG, 1u);
+            const uint64_t kof = (uint64_t)((1024u * kk) >> 4), aof = (uint64_t)((32u * kk) >> 4);
+            umma_tf32_w(dacc, dah0 + aof, dbh0 + kof, idG, (kt > 0 || kk > 0) ? 1u : 0u);
+            umma_tf32_w(dacc, dah0 + aof, dbl0 + kof, idG, 1u);
             umma_tf32_ta_w(dacc, alo + 8 * kk, dbh0 + kof, idG, 1u);
           }
           umma_commit_w(&tfree[ts]);
           umma_commit_w(&gfree[s]);
           ++it_g;
         } else {
+          const int s = it_r % kLpRbStages;
           const uint64_t dbh0 = umma_desc(smem_u32(res_hi(kt)), 16u, 1024u, false);
           const uint64_t dbl0 = umma_desc(smem_u32(res_lo(kt)), 16u, 1024u, false);
+          if (d.kind == LP_F) {
+            const uint64_t dah0 = umma_desc(smem_u32(r_stage(s)), 16u, 1024u, false);
 #pragma unroll
-          for (int kk = 0; kk < kBK / 8; ++kk) {
-            const uint64_t kof = (uint64_t)((32u * kk) >> 4);
-            umma_tf32_ta_w(dacc, ahi + 8 * kk, dbh0 + kof, idX, (kt > 0 || kk > 0) ? 1u : 0u);
-            umma_tf32_ta_w(dacc, ahi + 8 * kk, dbl0 + kof, idX, 1u);
-            umma_tf32_ta_w(dacc, alo + 8 * kk, dbh0 + kof, idX, 1u);
+            for (int kk = 0; kk < kBK / 8; ++kk) {
+              const uint64_t kof = (uint64_t)((32u * kk) >> 4);
+              umma_tf32_w(dacc, dah0 + kof, dbh0 + kof, idX, (kt > 0 || kk > 0) ? 1u : 0u);
+              umma_tf32_w(dacc, dah0 + kof, dbl0 + kof, idX, 1u);
+              umma_tf32_ta_w(dacc, alo + 8 * kk, dbh0 + kof, idX, 1u);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < kBK / 8; ++kk) {
+              const uint64_t kof = (uint64_t)((32u * kk) >> 4);
+              umma_tf32_ta_w(dacc, ahi + 8 * kk, dbh0 + kof, idX, (kt > 0 || kk > 0) ? 1u : 0u);
+              umma_tf32_ta_w(dacc, ahi + 8 * kk, dbl0 + kof, idX, 1u);
+              umma_tf32_ta_w(dacc, alo + 8 * kk, dbh0 + kof, idX, 1u);
+            }
           }
           umma_commit_w(&tfree[ts]);
+          umma_commit_w(&rfree[s]);  // the raw stage may be refilled once these MMAs completed
+          ++it_r;
         }
         if (kt == nk - 1) {
           umma_commit_w(&accf[a]);
@@ -411,17 +429,14 @@ __global__ void __launch_bounds__(kLpThreads, 1)
           ++it_r;
         }
         if (threadIdx.x == 64) lp_kstamp(dbg, it_t, 1);
-        if (d.kind != LP_I) {  // 128B-swizzled K-major rows: 16-byte chunk c of row r at c ^ (r & 7)
+        const bool kmaj = d.kind != LP_I;
+        if (kmaj) {  // 128B-swizzled K-major rows: 16-byte chunk c of row r at c ^ (r & 7); lo only
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const float4 v = *reinterpret_cast<const float4*>(ab + row * 128 + ((c ^ (row & 7)) << 4));
             const float x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float h = tf32_trunc(x[e]);
-              hi[4 * c + e] = __float_as_uint(h);
-              lo[4 * c + e] = __float_as_uint(tf32_round(x[e] - h));
-            }
+            for (int e = 0; e < 4; ++e) lo[4 * c + e] = __float_as_uint(tf32_round(x[e] - tf32_trunc(x[e])));
           }
         } else {  // unswizzled [k][32 rows] boxes
           const float* cb = reinterpret_cast<const float*>(ab + (row >> 5) * 4096) + (row & 31);
@@ -438,7 +453,7 @@ __global__ void __launch_bounds__(kLpThreads, 1)
         mbar_wait(&tfree[ts], ((it_t / kTm3) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tq4 = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kLpACol + 64 * ts);
-        tmem_st32(tq4, hi);
+        if (!kmaj) tmem_st32(tq4, hi);
         tmem_st32(tq4 + 32, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();

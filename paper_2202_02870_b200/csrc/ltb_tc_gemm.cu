@@ -517,6 +517,19 @@ __device__ __forceinline__ void umma_tf32_ta_w(uint32_t tmem_d, uint32_t tmem_a,
       "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
 
+// warp-uniform issue with A from shared memory (descriptor), as umma_tf32_ta_w
+__device__ __forceinline__ void umma_tf32_w(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
 __device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n\t"
