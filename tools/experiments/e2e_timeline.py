@@ -16,8 +16,12 @@ c = torch.empty((256, 256, 3, 32), dtype=torch.float32, pin_memory=True).numpy()
 a[...] = rng.standard_normal(a.shape)
 b[...] = rng.standard_normal(b.shape)
 spec = L.make_spec("dct", (256, 256, 3, 32))
-for ch in [int(x) for x in (sys.argv[1:] or ["8"])]:
-    nat.lib().ltb_debug_set_lprod_chunks(ch)
+import time
+for ch in [8]:
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter(); L.l_product(a, b, spec, out=c); ts.append(time.perf_counter() - t0)
+    print(f"host wall per call: median {np.median(ts) * 1e6:.1f} us, min {min(ts) * 1e6:.1f} us")
     for _ in range(3):
         L.l_product(a, b, spec, out=c)
     with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
