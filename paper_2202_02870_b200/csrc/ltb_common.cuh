@@ -134,6 +134,8 @@ struct ltb_ctx {
   unsigned long long* d_stats = nullptr;  // [0] Jacobi slices, [1] Jacobi sweeps
   // copy streams of the pipelined host-to-host l_product (created on first use)
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  // split batched SVT (ltb_svt_carry_impl): a high- and a low-priority stream (first use)
+  cudaStream_t split_hi = nullptr, split_hi2 = nullptr, split_lo = nullptr;
   // pageable host copies: two pinned staging buffers and their DMA events (first use)
   void* h_stage[2] = {nullptr, nullptr};
   cudaEvent_t ev_stage[2] = {nullptr, nullptr};
@@ -144,7 +146,7 @@ struct ltb_ctx {
   int opt_force_blocked = 0;                       // route every SVD through the blocked Jacobi tier
   unsigned long long* opt_tc_timeline = nullptr;   // tcgen05 kernels: per-tile clock stamps (CTA 0)
   unsigned long long* opt_qr_timeline = nullptr;   // QR-preconditioned Jacobi: stage stamps (CTA 0)
-  int opt_jacobi_pairs = 0;  // warm Cholesky Jacobi: 0 four-column blocks, 1 one pair per team, 2 two-column blocks
+  int opt_jacobi_pairs = 0;  // warm Cholesky Jacobi: 0 / 2 two-column blocks, 1 one pair per team, 3 four-column blocks
 };
 
 struct ltb_spec {
@@ -161,6 +163,11 @@ struct ltb_spec {
   void* d_mats[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   int64_t mat_off[16] = {0};
   int64_t mat_total = 0;
+  // real specs, per direction [0=fwd,1=inv] and mode: the mode matrix A (n even) has the
+  // even/odd symmetry of the DCT-II (1: A[i][n-1-j] = (-1)^i A[i][j]) or of its transpose
+  // (2: A[n-1-i][j] = (-1)^j A[i][j]), 0 none; the fp32 tile engine then halves the mode
+  // product's multiply-adds (xform_tile: mode_step_f2_sym*)
+  int sym[2][16] = {{0}, {0}};
   // real specs with P <= kKronMax: the dense Kronecker matrix of L and of L^{-1}
   // (C-order trailing index), fp32, for the tensor-core transform path
   float* d_kron[2] = {nullptr, nullptr};  // [P*P raw fp32 | P*P 3xTF32 lo part]

@@ -1,4 +1,6 @@
 // Context, memory, spec upload and small C-ABI glue for libltb.
+#include <algorithm>
+#include <cmath>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstring>
@@ -130,6 +132,9 @@ void ltb_ctx_destroy(ltb_ctx* ctx) {
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
   if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
+  if (ctx->split_hi) cudaStreamDestroy(ctx->split_hi);
+  if (ctx->split_hi2) cudaStreamDestroy(ctx->split_hi2);
+  if (ctx->split_lo) cudaStreamDestroy(ctx->split_lo);
   if (ctx->h_big) cudaFreeHost(ctx->h_big);
   for (int b = 0; b < 2; ++b) {
     if (ctx->h_stage[b]) cudaFreeHost(ctx->h_stage[b]);
@@ -434,6 +439,27 @@ int ltb_spec_create(ltb_ctx* ctx, int ntrail, const int64_t* trail_dims, int nmo
     if (total > 0) cudaMemcpy(d64, src, n_el * sizeof(double), cudaMemcpyHostToDevice);
     s->d_mats[0][dir] = d32;
     s->d_mats[1][dir] = d64;
+  }
+  // even/odd symmetric real mode matrices (the DCT and its inverse); a match within 1e-12
+  // of the largest entry (the fp32 engine then uses half of the matrix)
+  if (!is_complex && total > 0) {
+    for (int dir = 0; dir < 2; ++dir)
+      for (int k = 0; k < nmodes; ++k) {
+        const int n = s->sizes[k];
+        if (n % 2 || n < 8) continue;
+        const double* M = (dir == 0 ? h_fwd : h_inv) + s->mat_off[k];
+        double mx = 0.0;
+        for (int64_t l = 0; l < (int64_t)n * n; ++l) mx = std::max(mx, std::fabs(M[l]));
+        const double tol = 1e-12 * mx;
+        bool c1 = mx > 0.0, c2 = mx > 0.0;
+        for (int i = 0; i < n && (c1 || c2); ++i)
+          for (int j = 0; j < n; ++j) {
+            const double a = M[(int64_t)i * n + j];
+            if (c1 && std::fabs(M[(int64_t)i * n + (n - 1 - j)] - ((i & 1) ? -a : a)) > tol) c1 = false;
+            if (c2 && std::fabs(M[(int64_t)(n - 1 - i) * n + j] - ((j & 1) ? -a : a)) > tol) c2 = false;
+          }
+        s->sym[dir][k] = c1 ? 1 : (c2 ? 2 : 0);
+      }
   }
   // conjugate-slice pairing for real input data (complex specs): every transformed
   // mode is real (partner index j) or has exactly Hermitian rows (partner (n - j) mod n)

@@ -1963,91 +1963,225 @@ constexpr float g_carry_tol_scale = 1.f;
 // iterate's error against the fp64 run unchanged (3.2e-5)
 constexpr float g_carry_early = 1.f;
 
-int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
-                       float* V, int warm, const int* skip) {
-  const bool trans = I1 < I2;
-  const int64_t m = trans ? I2 : I1, n = trans ? I1 : I2;
-  if (batch <= 0 || batch > 65535 || n < 32) return LTB_EUNSUPPORTED;  // grid.y carries the slice
-  const int64_t nn = n * n;
-  WsScope ws(ctx);
+namespace {
+// One batch of the carried fp32 SVT in three phases, so that two batches can be interleaved
+// on different streams (see ltb_svt_carry_impl): pre (A0 = G V, Gram matrix), the Jacobi, post
+// (basis update, Newton-Schulz, recomposition).  Each phase launches on ctx->stream.
+struct CarryPart {
+  int64_t batch, I1, I2, m, n, nn;
+  bool trans;
+  const float* G;
+  float *out, *V;
+  int warm;
+  const int* skip;
+  double tau;
+  void* ws[8] = {};
+  int nws = 0;
   float *A0 = nullptr, *Y = nullptr, *sv = nullptr, *dd = nullptr, *VR = nullptr, *Vn = nullptr, *S = nullptr;
   int* kept = nullptr;
-  LTB_TRY(ws.alloc(sizeof(float) * batch * n * m, &A0));
-  LTB_TRY(ws.alloc(sizeof(float) * batch * nn, &Y));
-  LTB_TRY(ws.alloc(sizeof(float) * batch * n, &sv));
-  LTB_TRY(ws.alloc(sizeof(float) * batch * n, &dd));
-  LTB_TRY(ws.alloc(sizeof(float) * batch * nn, &VR));
-  LTB_TRY(ws.alloc(sizeof(float) * batch * nn, &Vn));
-  LTB_TRY(ws.alloc(sizeof(float) * batch * nn, &S));
-  LTB_TRY(ws.alloc(sizeof(int) * batch, &kept));
-  const int F = LTB_F32;
-  const float* src = G;
-  if (warm) {  // A0 = V^T G (I1 < I2) or G V: the preconditioned slices, same shape as G
+  CarryPart(int64_t b, int64_t i1, int64_t i2, const float* g, double t, float* o, float* v, int w, const int* sk)
+      : batch(b), I1(i1), I2(i2), G(g), out(o), V(v), warm(w), skip(sk), tau(t) {
+    trans = I1 < I2;
+    m = trans ? I2 : I1;
+    n = trans ? I1 : I2;
+    nn = n * n;
+  }
+  template <typename T> int alloc(ltb_ctx* ctx, size_t bytes, T** p) {
+    void* q = nullptr;
+    LTB_TRY(ltb_ws_alloc(ctx, bytes, &q));
+    ws[nws++] = q;
+    *p = (T*)q;
+    return LTB_OK;
+  }
+  void release(ltb_ctx* ctx) {  // stream-ordered on ctx->stream (the phase that used them last)
+    while (nws > 0) ltb_ws_free(ctx, ws[--nws]);
+  }
+  int allocate(ltb_ctx* ctx) {
+    LTB_TRY(alloc(ctx, sizeof(float) * batch * n * m, &A0));
+    LTB_TRY(alloc(ctx, sizeof(float) * batch * nn, &Y));
+    LTB_TRY(alloc(ctx, sizeof(float) * batch * n, &sv));
+    LTB_TRY(alloc(ctx, sizeof(float) * batch * n, &dd));
+    LTB_TRY(alloc(ctx, sizeof(float) * batch * nn, &VR));
+    LTB_TRY(alloc(ctx, sizeof(float) * batch * nn, &Vn));
+    LTB_TRY(alloc(ctx, sizeof(float) * batch * nn, &S));
+    LTB_TRY(alloc(ctx, sizeof(int) * batch, &kept));
+    return LTB_OK;
+  }
+  int pre(ltb_ctx* ctx) {
+    const int F = LTB_F32;
+    if (!warm) return LTB_OK;
+    // A0 = V^T G (I1 < I2) or G V: the preconditioned slices, same shape as G
     if (trans)
       LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, m, n, LTB_OP_T, V, n, nn, LTB_OP_N, G, m, n * m, A0, m, n * m, nullptr,
                             nullptr, nullptr, nullptr, nullptr, skip));
     else
       LTB_TRY(ltb_gemm_impl(ctx, F, batch, m, n, n, LTB_OP_N, G, n, m * n, LTB_OP_N, V, n, nn, A0, n, m * n, nullptr,
                             nullptr, nullptr, nullptr, nullptr, skip));
-    src = A0;
+    if (g_carry_chol) {
+      // A0's columns are nearly orthogonal: factor its Gram matrix (tensor-core GEMM) by
+      // Cholesky instead of a Householder QR of A0
+      if (trans)  // oriented W = A0^T: G = A0 A0^T
+        LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, m, LTB_OP_N, A0, m, n * m, LTB_OP_T, A0, m, n * m, S, n, nn,
+                              nullptr, nullptr, nullptr, nullptr, nullptr, skip));
+      else  // W = A0: G = A0^T A0
+        LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, m, LTB_OP_T, A0, n, m * n, LTB_OP_N, A0, n, m * n, S, n, nn,
+                              nullptr, nullptr, nullptr, nullptr, nullptr, skip));
+    }
+    return LTB_OK;
   }
-  JacobiOut o{nullptr, sv, Y, kept, dd, tau, skip};
-  o.stats = ctx->d_stats;
-  o.tol_scale = g_carry_tol_scale;
-  if (warm) o.early_stop = g_carry_early * sqrtf(FLT_EPSILON * sqrtf((float)n) * g_carry_tol_scale);
-  int st;
-  if (warm && g_carry_chol) {
-    // A0's columns are nearly orthogonal: factor its Gram matrix (tensor-core GEMM) by
-    // Cholesky instead of a Householder QR of A0 (Y reused as the Gram stack)
-    if (trans)  // oriented W = A0^T: G = A0 A0^T
-      LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, m, LTB_OP_N, A0, m, n * m, LTB_OP_T, A0, m, n * m, S, n, nn, nullptr,
-                            nullptr, nullptr, nullptr, nullptr, skip));
-    else  // W = A0: G = A0^T A0
-      LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, m, LTB_OP_T, A0, n, m * n, LTB_OP_N, A0, n, m * n, S, n, nn, nullptr,
-                            nullptr, nullptr, nullptr, nullptr, skip));
-    st = launch_jacobi_qr(ctx, batch, n, n, S, o, true);
-  } else {
-    st = launch_jacobi_qr(ctx, batch, I1, I2, src, o);
+  int jacobi(ltb_ctx* ctx) {
+    JacobiOut o{nullptr, sv, Y, kept, dd, tau, skip};
+    o.stats = ctx->d_stats;
+    o.tol_scale = g_carry_tol_scale;
+    if (warm) o.early_stop = g_carry_early * sqrtf(FLT_EPSILON * sqrtf((float)n) * g_carry_tol_scale);
+    if (warm && g_carry_chol) return launch_jacobi_qr(ctx, batch, n, n, S, o, true);
+    return launch_jacobi_qr(ctx, batch, I1, I2, warm ? A0 : G, o);
   }
-  if (st != LTB_OK) return st;
-  // V_A0: normalised Jacobi columns completed to an orthonormal basis (row-major, column j = v_j)
-  LTB_TRY(ensure_smem(ctx, complete_u_kernel<float>, (size_t)n * sizeof(float)));
-  complete_u_kernel<float><<<(unsigned)batch, 256, (size_t)n * sizeof(float), ctx->stream>>>((int)n, (int)n, Y, sv, VR,
-                                                                                              1);
-  LTB_LAUNCH_CHECK(ctx);
-  const float* Vc = VR;  // V_prev V_A0
-  if (warm) {
-    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, V, n, nn, LTB_OP_N, VR, n, nn, Vn, n, nn, nullptr, nullptr,
+  int post(ltb_ctx* ctx) {
+    const int F = LTB_F32;
+    // V_A0: normalised Jacobi columns completed to an orthonormal basis (row-major, column j = v_j)
+    LTB_TRY(ensure_smem(ctx, complete_u_kernel<float>, (size_t)n * sizeof(float)));
+    complete_u_kernel<float><<<(unsigned)batch, 256, (size_t)n * sizeof(float), ctx->stream>>>((int)n, (int)n, Y, sv,
+                                                                                                VR, 1);
+    LTB_LAUNCH_CHECK(ctx);
+    const float* Vc = VR;  // V_prev V_A0
+    if (warm) {
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, V, n, nn, LTB_OP_N, VR, n, nn, Vn, n, nn, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, skip));
+      Vc = Vn;
+    }
+    // Newton-Schulz: V = Vc (3I - Vc^T Vc) / 2, every call: without it the basis drifts from
+    // orthonormality by about one fp32 rounding per call, and the 200-iteration config-3
+    // iterate leaves the fp32 tolerance (measured error vs fp64: 3.2e-5 every call, 5.0e-5
+    // every 2nd, 2.1e-4 every 4th)
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_T, Vc, n, nn, LTB_OP_N, Vc, n, nn, S, n, nn, nullptr, nullptr,
                           nullptr, nullptr, nullptr, skip));
-    Vc = Vn;
+    const dim3 grid((unsigned)std::min<int64_t>((nn + 1023) / 1024, 64), (unsigned)batch);
+    ns_combine_kernel<<<grid, 256, 0, ctx->stream>>>((int)n, S, Y, skip);  // Y reused as M
+    LTB_LAUNCH_CHECK(ctx);
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, Vc, n, nn, LTB_OP_N, Y, n, nn, V, n, nn, nullptr, nullptr,
+                          nullptr, nullptr, nullptr, skip));
+    // T = V diag(sqrt((s - tau)_+ / s)),  Z = T T^T (K limited to the kept count),  out
+    col_scale_kernel<<<grid, 256, 0, ctx->stream>>>((int)n, V, dd, VR, skip);  // VR reused as T
+    LTB_LAUNCH_CHECK(ctx);
+    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, VR, n, nn, LTB_OP_T, VR, n, nn, S, n, nn, nullptr, nullptr,
+                          kept, nullptr, nullptr, skip));
+    if (trans)
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, m, n, LTB_OP_N, S, n, nn, LTB_OP_N, G, m, n * m, out, m, n * m, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, skip));
+    else
+      LTB_TRY(ltb_gemm_impl(ctx, F, batch, m, n, n, LTB_OP_N, G, n, m * n, LTB_OP_N, S, n, nn, out, n, m * n, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, skip));
+    return LTB_OK;
   }
-  // Newton-Schulz: V = Vc (3I - Vc^T Vc) / 2, every call: without it the basis drifts from
-  // orthonormality by about one fp32 rounding per call, and the 200-iteration config-3
-  // iterate leaves the fp32 tolerance (measured error vs fp64: 3.2e-5 every call, 5.0e-5
-  // every 2nd, 2.1e-4 every 4th)
-  LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_T, Vc, n, nn, LTB_OP_N, Vc, n, nn, S, n, nn, nullptr, nullptr,
-                        nullptr, nullptr, nullptr, skip));
-  const dim3 grid((unsigned)std::min<int64_t>((nn + 1023) / 1024, 64), (unsigned)batch);
-  ns_combine_kernel<<<grid, 256, 0, ctx->stream>>>((int)n, S, Y, skip);  // Y reused as M
-  LTB_LAUNCH_CHECK(ctx);
-  LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, Vc, n, nn, LTB_OP_N, Y, n, nn, V, n, nn, nullptr, nullptr,
-                        nullptr, nullptr, nullptr, skip));
-  // T = V diag(sqrt((s - tau)_+ / s)),  Z = T T^T (K limited to the kept count),  out
-  col_scale_kernel<<<grid, 256, 0, ctx->stream>>>((int)n, V, dd, VR, skip);  // VR reused as T
-  LTB_LAUNCH_CHECK(ctx);
-  LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, n, n, LTB_OP_N, VR, n, nn, LTB_OP_T, VR, n, nn, S, n, nn, nullptr, nullptr,
-                        kept, nullptr, nullptr, skip));
-  if (trans)
-    LTB_TRY(ltb_gemm_impl(ctx, F, batch, n, m, n, LTB_OP_N, S, n, nn, LTB_OP_N, G, m, n * m, out, m, n * m, nullptr,
-                          nullptr, nullptr, nullptr, nullptr, skip));
-  else
-    LTB_TRY(ltb_gemm_impl(ctx, F, batch, m, n, n, LTB_OP_N, G, n, m * n, LTB_OP_N, S, n, nn, out, n, m * n, nullptr,
-                          nullptr, nullptr, nullptr, nullptr, skip));
-  return LTB_OK;
+};
+
+int carry_checks(int64_t batch, int64_t I1, int64_t I2) {
+  const int64_t n = std::min(I1, I2);
+  return (batch <= 0 || batch > 65535 || n < 32) ? LTB_EUNSUPPORTED : LTB_OK;  // grid.y carries the slice
 }
 
-namespace {
+// RAII: restores ctx->stream and releases the events on every return path
+struct StreamSwap {
+  ltb_ctx* ctx;
+  cudaStream_t main;
+  cudaEvent_t ev[6] = {};
+  explicit StreamSwap(ltb_ctx* c) : ctx(c), main(c->stream) {}
+  ~StreamSwap() {
+    ctx->stream = main;
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
 }  // namespace
+
+// The warm Jacobi runs one slice per CTA, two CTAs per SM: a batch just above a multiple of the
+// 2 x SMs slots (config 3: 300 slices on 296) leaves a few slices for a second wave, during
+// which the rest of the GPU idles (the launch took about twice a slice's latency).  Every
+// slice's chain (A0 / Gram GEMMs, Jacobi, basis update, recomposition) is independent, so the
+// batch is split into the whole waves (big) and the remainder (small):
+//   small pre   (low-priority stream)  -- runs beside big pre
+//   big pre     (high priority)        -> event E
+//   small Jacobi (low priority, waits E): pending beside the big Jacobi, so the block
+//                scheduler dispatches the big one's CTAs first and the small one's into the
+//                slots the first finished CTAs free
+//   big Jacobi, big post (high priority): the post GEMMs run on the SMs the big Jacobi frees
+//   small post  (a second high-priority stream, after the small Jacobi)
+constexpr int g_carry_split = 1;
+
+int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* G, double tau, float* out,
+                       float* V, int warm, const int* skip) {
+  LTB_TRY(carry_checks(batch, I1, I2));
+  const int64_t slots = 2 * (int64_t)ctx->num_sms;
+  const int64_t whole = batch / slots * slots, rest = batch - whole;
+  if (!(g_carry_split && warm && whole > 0 && rest > 0 && rest * 8 <= slots)) {
+    CarryPart p(batch, I1, I2, G, tau, out, V, warm, skip);
+    int st = p.allocate(ctx);
+    if (st == LTB_OK) st = p.pre(ctx);
+    if (st == LTB_OK) st = p.jacobi(ctx);
+    if (st == LTB_OK) st = p.post(ctx);
+    p.release(ctx);
+    return st;
+  }
+  if (!ctx->split_hi) {
+    int lo = 0, hi = 0;
+    LTB_CUDA_TRY(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    LTB_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->split_hi, cudaStreamNonBlocking, hi));
+    LTB_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->split_hi2, cudaStreamNonBlocking, hi));
+    LTB_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&ctx->split_lo, cudaStreamNonBlocking, lo));
+  }
+  const int64_t n = std::min(I1, I2), S = I1 * I2;
+  StreamSwap sw(ctx);
+  for (cudaEvent_t& e : sw.ev) LTB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t fork = sw.ev[0], e_pre = sw.ev[1], e_small_jac = sw.ev[2], j_big = sw.ev[3], j_small = sw.ev[4];
+  // the workspace is allocated and (after the join) released on the caller's stream, so the
+  // stream-ordered pool reuses it from call to call as in the unsplit case
+  CarryPart big(whole, I1, I2, G, tau, out, V, warm, skip);
+  CarryPart small(rest, I1, I2, G + whole * S, tau, out + whole * S, V + whole * n * n, warm, skip);
+  struct Release {
+    ltb_ctx* ctx;
+    CarryPart *a, *b;
+    cudaStream_t main;
+    ~Release() {
+      const cudaStream_t cur = ctx->stream;
+      ctx->stream = main;
+      a->release(ctx);
+      b->release(ctx);
+      ctx->stream = cur;
+    }
+  } rel{ctx, &big, &small, sw.main};
+  LTB_TRY(big.allocate(ctx));
+  LTB_TRY(small.allocate(ctx));
+  LTB_CUDA_TRY(ctx, cudaEventRecord(fork, sw.main));
+  LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->split_hi, fork, 0));
+  LTB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->split_lo, fork, 0));
+  int st = LTB_OK;
+  ctx->stream = ctx->split_lo;
+  if (st == LTB_OK) st = small.pre(ctx);
+  ctx->stream = ctx->split_hi;
+  if (st == LTB_OK) st = big.pre(ctx);
+  if (st == LTB_OK) st = cudaEventRecord(e_pre, ctx->split_hi) == cudaSuccess ? LTB_OK : LTB_ECUDA;
+  ctx->stream = ctx->split_lo;
+  if (st == LTB_OK) st = cudaStreamWaitEvent(ctx->split_lo, e_pre, 0) == cudaSuccess ? LTB_OK : LTB_ECUDA;
+  if (st == LTB_OK) st = small.jacobi(ctx);
+  if (st == LTB_OK) st = cudaEventRecord(e_small_jac, ctx->split_lo) == cudaSuccess ? LTB_OK : LTB_ECUDA;
+  ctx->stream = ctx->split_hi;
+  if (st == LTB_OK) st = big.jacobi(ctx);
+  if (st == LTB_OK) st = big.post(ctx);
+  ctx->stream = ctx->split_hi2;
+  if (st == LTB_OK) st = cudaStreamWaitEvent(ctx->split_hi2, e_small_jac, 0) == cudaSuccess ? LTB_OK : LTB_ECUDA;
+  if (st == LTB_OK) st = small.post(ctx);
+  // join every stream into the caller's (also on failure: nothing may outlive the call, and
+  // the workspace is released behind all of it)
+  cudaEventRecord(j_big, ctx->split_hi);
+  cudaEventRecord(j_small, ctx->split_hi2);
+  cudaEventRecord(sw.ev[5], ctx->split_lo);
+  cudaStreamWaitEvent(sw.main, j_big, 0);
+  cudaStreamWaitEvent(sw.main, j_small, 0);
+  cudaStreamWaitEvent(sw.main, sw.ev[5], 0);
+  if (st == LTB_ECUDA) return ltb_set_error(ctx, LTB_ECUDA, "carried SVT: stream ordering failed");
+  return st;
+}
 
 // fp64 SVT carrying the slices' right bases V (n x n row-major, n = min(I1, I2)) between
 // PGA iterations, as ltb_svt_carry_impl does in fp32 but without the QR / Cholesky stage:

@@ -21,6 +21,8 @@ struct ModeStep {
   int64_t hi, lo;
   int64_t mat_off;   // element offset of the row-major matrix in global memory
   int smem_off;      // element offset of the transposed padded matrix in shared memory
+  int sym;           // ltb_spec::sym of the step's matrix (even/odd symmetry), 0 none
+  int sym_on;        // the fp32 FFMA2 plan stages the half matrix and runs mode_step_f2_sym*
 };
 
 struct XformParams {
@@ -52,6 +54,8 @@ inline void build_steps(const ltb_spec* spec, int inverse, XformParams& p) {
     p.step[k].hi = hi;
     p.step[k].lo = lo;
     p.step[k].mat_off = spec->mat_off[m];
+    p.step[k].sym = spec->is_complex ? 0 : spec->sym[inverse ? 1 : 0][m];
+    p.step[k].sym_on = 0;
   }
   p.P = (int)spec->P;
   p.invP = 1.0f / (float)p.P;
@@ -70,6 +74,7 @@ inline void plan_matrices(XformParams& p) {
     ms.npad = (ms.n + rb - 1) / rb * rb;
     ms.inv_nblk = 1.0f / (float)(ms.npad / rb);
     ms.inv_lo = 1.0f / (float)ms.lo;
+    ms.sym_on = 0;
     off = (off + RB - 1) / RB * RB;  // every matrix starts vector-aligned
     ms.smem_off = off;
     off += ms.n * ms.npad;
@@ -324,6 +329,108 @@ __device__ __forceinline__ void mode_step_f2(const XformParams& p, const ModeSte
   }
 }
 
+// Even/odd symmetric modes (DCT-II and its inverse, ltb_spec::sym), fp32 FFMA2 as
+// mode_step_f2, half the multiply-adds of the full product.  n even, h = n / 2.
+// sym 1, A[i][n-1-j] = (-1)^i A[i][j] (forward DCT-II): out_i = sum_{j<h} A[i][j] (v_j +- v_{n-1-j}),
+//   + for even i, - for odd i; a work item takes RBM rows of one parity.  Shared memory: two
+//   parity planes, Msm[(par h + j) npad + e] = A[2 e + par][j] (j < h, e < h)
+template <int RBM>
+__device__ __forceinline__ void mode_step_f2_sym1(const XformParams& p, const ModeStep& ms,
+                                                  const float* __restrict__ src, float* __restrict__ dst,
+                                                  const float* __restrict__ Msm, int tid) {
+  const int n = ms.n, h = n >> 1, npad = ms.npad, lo = (int)ms.lo, hi = (int)ms.hi;
+  const int half = p.TT >> 1, pitch = p.pitch;
+  const int hshift = p.ttshift - 1;
+  const int nblk = npad / RBM;  // blocks per parity
+  const int work = hi * lo * 2 * nblk * half;
+  for (int w = tid; w < work; w += kXformThreads) {
+    const int t = w & (half - 1);
+    const int r0 = w >> hshift;
+    const int r1 = fdiv(r0, 2 * nblk, ms.inv_nblk);  // inv_nblk = 1 / (2 nblk)
+    const int rem = r0 - r1 * 2 * nblk;
+    const int par = rem >= nblk ? 1 : 0;
+    const int e0 = (rem - par * nblk) * RBM;
+    const int hi_i = fdiv(r1, lo, ms.inv_lo);
+    const int lo_i = r1 - hi_i * lo;
+    const int base = hi_i * n * lo + lo_i;
+    const int jstride = lo * pitch;
+    const float sg = par ? -1.f : 1.f;
+    const float2 SG = make_float2(sg, sg);
+    float2 acc[RBM];
+#pragma unroll
+    for (int rr = 0; rr < RBM; ++rr) acc[rr] = make_float2(0.f, 0.f);
+    const float* c1 = src + base * pitch + t;
+    const float* c2 = c1 + (n - 1) * jstride;
+    const float* mrowp = Msm + par * h * npad + e0;
+#pragma unroll 2
+    for (int j = 0; j < h; ++j, c1 += jstride, c2 -= jstride, mrowp += npad) {
+      const float2 x = __ffma2_rn(SG, make_float2(c2[0], c2[half]), make_float2(c1[0], c1[half]));
+      const mrow<float, RBM> mv = *reinterpret_cast<const mrow<float, RBM>*>(mrowp);
+#pragma unroll
+      for (int rr = 0; rr < RBM; ++rr) acc[rr] = __ffma2_rn(make_float2(mv.v[rr], mv.v[rr]), x, acc[rr]);
+    }
+    float* out = dst + base * pitch + t;
+#pragma unroll
+    for (int rr = 0; rr < RBM; ++rr)
+      if (e0 + rr < h) {
+        const int i = 2 * (e0 + rr) + par;
+        out[i * jstride] = acc[rr].x;
+        out[i * jstride + half] = acc[rr].y;
+      }
+  }
+}
+
+// sym 2, A[n-1-i][j] = (-1)^j A[i][j] (inverse DCT, the transpose): with E_i / O_i the sums over
+//   even / odd j of A[i][j] v_j (i < h), out_i = E_i + O_i and out_{n-1-i} = E_i - O_i; a work
+//   item takes RBM rows i < h and writes 2 RBM outputs.  Shared memory Msm[j npad + i] = A[i][j]
+template <int RBM>
+__device__ __forceinline__ void mode_step_f2_sym2(const XformParams& p, const ModeStep& ms,
+                                                  const float* __restrict__ src, float* __restrict__ dst,
+                                                  const float* __restrict__ Msm, int tid) {
+  const int n = ms.n, h = n >> 1, npad = ms.npad, lo = (int)ms.lo, hi = (int)ms.hi;
+  const int half = p.TT >> 1, pitch = p.pitch;
+  const int hshift = p.ttshift - 1;
+  const int nblk = npad / RBM;
+  const int work = hi * lo * nblk * half;
+  for (int w = tid; w < work; w += kXformThreads) {
+    const int t = w & (half - 1);
+    const int r0 = w >> hshift;
+    const int r1 = fdiv(r0, nblk, ms.inv_nblk);
+    const int i0 = (r0 - r1 * nblk) * RBM;
+    const int hi_i = fdiv(r1, lo, ms.inv_lo);
+    const int lo_i = r1 - hi_i * lo;
+    const int base = hi_i * n * lo + lo_i;
+    const int jstride = lo * pitch;
+    float2 ae[RBM], ao[RBM];
+#pragma unroll
+    for (int rr = 0; rr < RBM; ++rr) ae[rr] = ao[rr] = make_float2(0.f, 0.f);
+    const float* col = src + base * pitch + t;
+    const float* mrowp = Msm + i0;
+#pragma unroll 2
+    for (int j = 0; j < n; j += 2, col += 2 * jstride, mrowp += 2 * npad) {
+      const float2 ve = make_float2(col[0], col[half]);
+      const float2 vo = make_float2(col[jstride], col[jstride + half]);
+      const mrow<float, RBM> me = *reinterpret_cast<const mrow<float, RBM>*>(mrowp);
+      const mrow<float, RBM> mo = *reinterpret_cast<const mrow<float, RBM>*>(mrowp + npad);
+#pragma unroll
+      for (int rr = 0; rr < RBM; ++rr) {
+        ae[rr] = __ffma2_rn(make_float2(me.v[rr], me.v[rr]), ve, ae[rr]);
+        ao[rr] = __ffma2_rn(make_float2(mo.v[rr], mo.v[rr]), vo, ao[rr]);
+      }
+    }
+    float* out = dst + base * pitch + t;
+#pragma unroll
+    for (int rr = 0; rr < RBM; ++rr)
+      if (i0 + rr < h) {
+        const int i = i0 + rr;
+        out[i * jstride] = ae[rr].x + ao[rr].x;
+        out[i * jstride + half] = ae[rr].y + ao[rr].y;
+        out[(n - 1 - i) * jstride] = ae[rr].x - ao[rr].x;
+        out[(n - 1 - i) * jstride + half] = ae[rr].y - ao[rr].y;
+      }
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 template <typename Tc, typename Tm, class Loader, class Storer>
 __global__ void __launch_bounds__(kXformThreads)
@@ -347,6 +454,23 @@ __global__ void __launch_bounds__(kXformThreads)
       const int n = p.step[s].n, npad = p.step[s].npad;
       const Tm* M = mats + p.step[s].mat_off;
       Tm* dst = Ms + p.step[s].smem_off;
+      if (p.step[s].sym_on == 1) {  // parity planes of the first h columns
+        const int h = n >> 1;
+        for (int l = tid; l < 2 * h * npad; l += kXformThreads) {
+          const int r = l / npad, e = l - r * npad;  // r = par h + j
+          const int par = r >= h ? 1 : 0, j = r - par * h;
+          dst[l] = (e < h) ? M[(size_t)(2 * e + par) * n + j] : zero_v<Tm>();
+        }
+        continue;
+      }
+      if (p.step[s].sym_on == 2) {  // the first h rows, transposed
+        const int h = n >> 1;
+        for (int l = tid; l < n * npad; l += kXformThreads) {
+          const int j = l / npad, i = l - j * npad;
+          dst[l] = (i < h) ? M[(size_t)i * n + j] : zero_v<Tm>();
+        }
+        continue;
+      }
       for (int l = tid; l < n * npad; l += kXformThreads) {
         const int j = l / npad, i = l - j * npad;
         dst[l] = (i < n) ? M[(size_t)i * n + j] : zero_v<Tm>();
@@ -377,7 +501,23 @@ __global__ void __launch_bounds__(kXformThreads)
     const Tm* Msm = Ms + ms.smem_off;
     bool done = false;
     if constexpr (std::is_same<Tc, float>::value && std::is_same<Tm, float>::value) {
-      if (p.mats_in_smem && TT >= 2) {
+      if (p.mats_in_smem && TT >= 2 && ms.sym_on) {
+        if (ms.sym_on == 1) {
+          switch (ms.rb) {
+            case 4: mode_step_f2_sym1<4>(p, ms, src, dst, Msm, tid); break;
+            case 6: mode_step_f2_sym1<6>(p, ms, src, dst, Msm, tid); break;
+            case 10: mode_step_f2_sym1<10>(p, ms, src, dst, Msm, tid); break;
+            default: mode_step_f2_sym1<8>(p, ms, src, dst, Msm, tid); break;
+          }
+        } else {
+          switch (ms.rb) {
+            case 4: mode_step_f2_sym2<4>(p, ms, src, dst, Msm, tid); break;
+            case 6: mode_step_f2_sym2<6>(p, ms, src, dst, Msm, tid); break;
+            default: mode_step_f2_sym2<8>(p, ms, src, dst, Msm, tid); break;
+          }
+        }
+        done = true;
+      } else if (p.mats_in_smem && TT >= 2) {
         switch (ms.rb) {  // kF2Blocks
           case 1: mode_step_f2<1>(p, ms, src, dst, Msm, tid); break;
           case 2: mode_step_f2<2>(p, ms, src, dst, Msm, tid); break;
@@ -439,12 +579,38 @@ __global__ void __launch_bounds__(kXformThreads)
 // fill whole rounds of the CTA's threads; e.g. n = 100 under a 3 x 100 spec with 16-tube
 // tiles: rb = 8 gives 312 items (two rounds, the second 22% busy), rb = 10 gives 240 (one)
 constexpr int kF2Blocks[] = {1, 2, 4, 6, 8, 10, 12, 16};
+constexpr int g_xform_sym = 1;  // even/odd symmetric modes at half the multiply-adds
 
 inline void plan_matrices_f2(XformParams& p) {
   const int half = p.TT >> 1;
   int off = 0;
   for (int s = 0; s < p.nsteps; ++s) {
     ModeStep& ms = p.step[s];
+    if (ms.sym && g_xform_sym) {  // even/odd modes: rows of one parity (1) or the first half (2)
+      const int h = ms.n >> 1;
+      int64_t best = -1;
+      for (int rb : {4, 6, 8, 10}) {
+        if (ms.sym == 2 && rb > 8) continue;  // 2 rb accumulators
+        const int64_t nblk = (h + rb - 1) / rb;
+        const int64_t items = ms.hi * ms.lo * nblk * (ms.sym == 1 ? 2 : 1) * half;
+        const int64_t per = ms.sym == 1 ? (int64_t)h * (rb + 4) : (int64_t)ms.n * (rb + 2);
+        const int64_t cost = (items + kXformThreads - 1) / kXformThreads * per;
+        if (best < 0 || cost < best) {
+          best = cost;
+          ms.rb = rb;
+        }
+      }
+      ms.npad = (h + ms.rb - 1) / ms.rb * ms.rb;
+      const int nblk = ms.npad / ms.rb;
+      ms.inv_nblk = 1.0f / (float)(ms.sym == 1 ? 2 * nblk : nblk);
+      ms.inv_lo = 1.0f / (float)ms.lo;
+      ms.sym_on = ms.sym;
+      off = (off + 3) / 4 * 4;
+      ms.smem_off = off;
+      off += (ms.sym == 1 ? 2 * h : ms.n) * ms.npad;
+      continue;
+    }
+    ms.sym_on = 0;
     int64_t best = -1;
     for (int rb : kF2Blocks) {
       const int64_t nblk = (ms.n + rb - 1) / rb;
