@@ -996,6 +996,9 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   if ((f32 || c32) && !WANT_V && g_qr_early > 0.f) {  // svt / values in single precision
     relmax = reinterpret_cast<unsigned*>(flags + 2 * batch);
     early = g_qr_early * sqrtf(FLT_EPSILON * sqrtf((float)std::max(g.m, 1)));
+  } else if (o.early_stop > 0.f) {  // the caller's early stop (warm carried fp64 SVT: sqrt(tol))
+    relmax = reinterpret_cast<unsigned*>(flags + 2 * batch);
+    early = o.early_stop;
   }
   int* count = flags + 3 * batch;
   LTB_CUDA_TRY(ctx, cudaMemsetAsync(rot, 0, sizeof(int) * batch, ctx->stream));
