@@ -366,3 +366,28 @@ def test_l_product_pinned_host_pipeline(dt, a_shape, n):
     ref = O.l_product(a.astype(np.float64), b.astype(np.float64), O.ospec("dct", pc.shape))
     assert rel_err(pc, ref) < (1e-4 if dt == np.float32 else 1e-10)
     np.testing.assert_array_equal(pc, plain)
+
+
+@pytest.mark.parametrize("trail,kind", [((5, 120), "dct"), ((3, 100, 2), "dct"), ((7, 90), "explicit_dct"),
+                                        ((6, 98), "explicit_rand")])
+def test_tile_engine_even_odd_modes(trail, kind):
+    """fp32 transforms through the shared-memory tile engine (P > 512, so not the tensor-core
+    Kronecker path): DCT modes (and an explicit DCT matrix) take the even/odd half-matrix mode
+    steps, a random explicit matrix the full ones; forward and inverse against the oracle."""
+    rng = np.random.default_rng(11)
+    shape = (9, 7) + trail
+    x = rng.standard_normal(shape).astype(np.float32)
+    if kind == "dct":
+        spec, ospec = L.make_spec("dct", shape), O.ospec("dct", shape)
+    else:
+        n = trail[-1]
+        m = L.build_dct_matrix(n) if kind == "explicit_dct" else np.linalg.qr(rng.standard_normal((n, n)))[0]
+        mats = {len(shape): m}
+        md = [len(shape)]
+        spec = L.make_spec("explicit", shape, modes=md, matrices=mats)
+        ospec = O.ospec("explicit", shape, modes=md, matrices=mats)
+    y = L.apply_l(x, spec)
+    ref = O.forward(x.astype(np.float64), ospec)
+    assert rel_err(y, ref) < 1e-5
+    back = L.apply_l_inv(y, spec)
+    assert rel_err(back, x) < 1e-5
