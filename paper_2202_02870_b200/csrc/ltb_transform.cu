@@ -302,6 +302,27 @@ extern "C" int ltb_mode_product(ltb_ctx* ctx, int64_t outer, int64_t nin, int64_
   const bool dbl = dtype_is_double(dtype_out);
   if (dtype_is_double(dtype_in) != dbl || dtype_is_double(dtype_mat) != dbl)
     return ltb_set_error(ctx, LTB_EPARAM, "mode_product: mixed precision");
+  if (dtype_in == dtype_mat && dtype_in == dtype_out && nin > 0) {
+    // y[o, :, l] = M x[o, :, l] is a GEMM (core.py:110-122 unfolds to the same product):
+    //   inner == 1  one GEMM  Y (outer x nout) = X (outer x nin) M^T
+    //   otherwise   outer GEMMs Y_o (nout x inner) = M (nout x nin) X_o (nin x inner), M shared
+    // through the shared-memory tiled / tcgen05 engine of ltb_gemm.cu (batches of <= 65535)
+    const size_t es = dtype_size(dtype_in);
+    if (inner == 1)
+      return ltb_gemm_impl(ctx, dtype_in, 1, outer, nout, nin, LTB_OP_N, d_in, nin, 0, LTB_OP_T, d_mat, nin, 0, d_out,
+                           nout, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (inner >= 16) {
+      for (int64_t o0 = 0; o0 < outer; o0 += 65535) {
+        const int64_t nb = std::min<int64_t>(65535, outer - o0);
+        LTB_TRY(ltb_gemm_impl(ctx, dtype_in, nb, nout, inner, nin, LTB_OP_N, d_mat, nin, 0, LTB_OP_N,
+                              (const char*)d_in + es * o0 * nin * inner, inner, nin * inner,
+                              (char*)d_out + es * o0 * nout * inner, inner, nout * inner, nullptr, nullptr, nullptr,
+                              nullptr, nullptr, nullptr));
+      }
+      return LTB_OK;
+    }
+  }
+  // short inner runs (2..15) or mixed real / complex operands: one output per thread
   const int blocks = grid_for(total, 256, ctx->num_sms * 16);
   return dispatch_dtype(dtype_in, [&](auto ti) {
     using Tin = typename decltype(ti)::type;

@@ -136,6 +136,34 @@ def test_mode_n_product_large_real():
         assert rel_err(L.mode_n_product(x, uu, n), O.mode_product(x, uu, n)) < 1e-12
 
 
+@pytest.mark.parametrize(
+    "shape,n,dtype",
+    [
+        ((40, 30, 20), 3, np.float64),       # inner == 1: one GEMM X M^T
+        ((40, 30, 20), 3, np.float32),       # (tcgen05 3xTF32 engine)
+        ((7, 33, 48), 2, np.float32),        # batched GEMMs with the matrix shared (inner >= 16)
+        ((7, 33, 48), 2, np.complex64),
+        ((5, 6, 40, 17), 3, np.complex128),
+        ((9, 20, 5), 2, np.float64),         # inner 2..15: the per-output kernel
+        ((70000, 2, 16), 2, np.float64),     # more than 65535 GEMM batches
+        ((0, 4, 3), 2, np.float64),
+    ],
+)
+def test_mode_n_product_gemm_paths(shape, n, dtype):
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(shape)
+    u = rng.standard_normal((shape[n - 1] + 3, shape[n - 1]))
+    if np.iscomplexobj(np.zeros(1, dtype)):
+        x = x + 1j * rng.standard_normal(shape)
+        u = u - 0.5j * rng.standard_normal(u.shape)
+    x, u = x.astype(dtype), u.astype(dtype)
+    out = L.mode_n_product(x, u, n)
+    ref = O.mode_product(x.astype(np.complex128 if np.iscomplexobj(x) else np.float64), u, n)
+    assert out.shape == ref.shape and out.dtype == np.result_type(x.dtype, u.dtype)
+    tol = 1e-5 if dtype in (np.float32, np.complex64) else 1e-12
+    assert rel_err(out, ref) < tol if ref.size else out.size == 0
+
+
 @pytest.mark.parametrize("kind,dtype", [("fft", np.complex128), ("fft", np.complex64), ("dct", np.complex128)])
 def test_numeric_consistency_error_on_corrupted_spectrum(kind, dtype):
     """apply_l_inv(assume_real=True) raises when the transform-domain tensor is not the image
