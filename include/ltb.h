@@ -197,6 +197,14 @@ int ltb_spec_slice_svt(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t ba
  * (LTB_EUNSUPPORTED otherwise: use ltb_slice_svt). */
 int ltb_slice_svt_carry(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const float* d_a, double tau,
                         float* d_out, float* d_v, int warm);
+/* the same for complex64 slices too large for the shared-memory Jacobi tier (the
+ * block-cyclic tier; config 4's 1024 x 1024 slices): svt (linalg.py:168-181) warm-started
+ * from the previous call's right singular bases.  d_vt (batch x n x n complex64, n = I2)
+ * holds V^T (row j = the j-th right singular vector), caller-owned, read when warm != 0 and
+ * rewritten on return.  Needs I1 >= I2 >= 32 and I2 even (LTB_EUNSUPPORTED otherwise, also
+ * for slices that fit in shared memory: use ltb_slice_svt). */
+int ltb_slice_svt_carry_c64(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const void* d_a, double tau,
+                            void* d_out, void* d_vt, int warm);
 int ltb_slice_svd(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,
                   const void* d_a, void* d_u, void* d_s, void* d_v);
 int ltb_slice_singular_values(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n,

@@ -68,6 +68,7 @@ _SIGNATURES = {
                     _int),
     "ltb_slice_svt":([_vp, _int, _i64, _i64, _i64, _vp, C.c_double, _vp], _int),
     "ltb_slice_svt_carry": ([_vp, _i64, _i64, _i64, _vp, C.c_double, _vp, _vp, _int], _int),
+    "ltb_slice_svt_carry_c64": ([_vp, _i64, _i64, _i64, _vp, C.c_double, _vp, _vp, _int], _int),
     "ltb_reduce_sumsq_device": ([_vp, _int, _i64, _vp, _vp, _vp], _int),
     "ltb_spec_slice_svt": ([_vp, _vp, _int, _i64, _i64, _i64, _vp, C.c_double, _vp], _int),
     "ltb_slice_svd": ([_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp], _int),

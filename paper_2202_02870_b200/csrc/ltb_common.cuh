@@ -289,6 +289,10 @@ int ltb_svt_carry_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, cons
                        float* V, int warm, const int* skip);
 int ltb_svt_carry64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const double* G, double tau,
                          double* out, double* V, int warm, const int* skip);
+int ltb_svt_carry_c64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const void* d_g, double tau,
+                           void* d_out, void* d_vt, int warm, const int* skip);
+int ltb_svt_mirror_carry_c64_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t batch, int64_t I1, int64_t I2,
+                                  const void* d_a, double tau, void* d_out, void* d_vt, int warm, const int* d_skip);
 int ltb_svt_mirror_impl(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1, int64_t I2,
                         const void* d_a, double tau, void* d_out, const int* d_skip);
 int ltb_transform_pair_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t ntubes, int inverse, int dtype_in,
@@ -300,6 +304,11 @@ int ltb_gemm_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, 
                   const void* d_a, int64_t lda, int64_t sa, int op_b, const void* d_b, int64_t ldb,
                   int64_t sb, void* d_c, int64_t ldc, int64_t sc, const int* d_mlim, const int* d_nlim,
                   const int* d_klim, const void* d_row_scale, const void* d_col_scale, const int* d_skip = nullptr);
+// complex64 GEMM on the tcgen05 engine (ltb_gemm.cu): C = [conj] A * op(B), A m x k with K
+// contiguous, B stored k x n (b_kn) or n x k; LTB_EUNSUPPORTED when it does not fit
+int ltb_cgemm_tc(ltb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t k, bool conj_a, const void* d_a,
+                 int64_t lda, int64_t sa, bool b_kn, bool conj_b, const void* d_b, int64_t ldb, int64_t sb,
+                 void* d_c, int64_t ldc, int64_t sc, const float* rscale, const int* skip);
 int ltb_svt_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, const void* d_a,
                  double tau, const double* d_tau /* optional per-call device tau */, void* d_out,
                  const int* d_skip /* optional device flag: nonzero -> kernels return */);

@@ -649,6 +649,18 @@ int ltb_slice_svt_carry(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, con
   return st;
 }
 
+int ltb_slice_svt_carry_c64(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const void* d_a, double tau,
+                            void* d_out, void* d_vt, int warm) {
+  if (!(tau >= 0)) return ltb_set_error(ctx, LTB_EPARAM, "tau must be >= 0, got %g", tau);
+  if (batch < 0 || I1 < 0 || I2 < 0) return ltb_set_error(ctx, LTB_ESHAPE, "svt_carry_c64: negative extent");
+  if (batch == 0 || I1 == 0 || I2 == 0) return LTB_OK;
+  const int st = ltb_svt_carry_c64_impl(ctx, batch, I1, I2, d_a, tau, d_out, d_vt, warm, nullptr);
+  if (st == LTB_EUNSUPPORTED)
+    return ltb_set_error(ctx, LTB_EUNSUPPORTED,
+                         "svt_carry_c64: needs I1 >= I2 >= 32, I2 even, and slices beyond the shared-memory tier");
+  return st;
+}
+
 int ltb_reduce_sumsq_device(ltb_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y, double* d_out) {
   return ltb_reduce_sumsq_dev(ctx, dtype, n, d_x, d_y, d_out);
 }

@@ -130,7 +130,66 @@ __global__ void zero_c_kernel(int64_t batch, int64_t m, int64_t n, T* c, int64_t
   }
 }
 
+// complex64 on the tensor cores: the real 2 x 2 representation of the right operand.
+// With X (m x k complex, K contiguous) viewed as a real m x 2k matrix [re, im interleaved
+// along K], X Y = X' Y~ where Y~ (2k x 2n real) holds, for every y = Y[l][j], the block
+//   rows 2l, 2l+1 / columns 2j, 2j+1:  [ re  im ; -im  re ]      (row 2l meets Re x, row 2l+1 Im x)
+// and conj(X) Y uses [ re  im ; im  -re ].  The real product X' Y~ (m x 2n) is the complex
+// result in its usual interleaved layout, so one fp32 tensor-core GEMM (3xTF32) with the
+// same 8 m n k real multiply-adds as the 4M scheme computes it.  `in` is stored rows x cols
+// complex (ld elements): kn == true, rows = k and cols = n (the block is written as above, the
+// result is the MN-major B operand); kn == false, rows = n and cols = k (the block is written
+// transposed: the K-major B operand).
+__global__ void cexpand_kernel(int rows, int cols, int64_t ld, int64_t sin, const cplx<float>* __restrict__ in,
+                               float* __restrict__ out, int kn, int conj_in, int conj_left,
+                               const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const int64_t b = blockIdx.z;
+  const int r = blockIdx.y;
+  const cplx<float>* src = in + b * sin + (int64_t)r * ld;
+  float2* o0 = reinterpret_cast<float2*>(out + (b * 4 * rows + (int64_t)(2 * r) * 2) * cols);
+  float2* o1 = o0 + cols;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
+    const float2 v = __ldg(reinterpret_cast<const float2*>(src + c));
+    const float re = v.x, im = conj_in ? -v.y : v.y;
+    // E = [e00 e01; e10 e11]
+    const float e00 = re, e01 = im, e10 = conj_left ? im : -im, e11 = conj_left ? -re : re;
+    if (kn) {
+      o0[c] = make_float2(e00, e01);
+      o1[c] = make_float2(e10, e11);
+    } else {
+      o0[c] = make_float2(e00, e10);
+      o1[c] = make_float2(e01, e11);
+    }
+  }
+}
+
 }  // namespace
+
+// C = op(A) op(B) for complex64 on the tcgen05 engine through the real representation above.
+// A: m x k, K contiguous (conj_a: conj(A)); B: stored k x n (b_kn) or n x k, conj_b conjugates
+// its elements.  rscale: optional real scale per row of C (batch x m).  LTB_EUNSUPPORTED when
+// the shape / alignment does not fit (the caller falls back to the CUDA-core kernel).
+int ltb_cgemm_tc(ltb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t k, bool conj_a, const void* d_a,
+                 int64_t lda, int64_t sa, bool b_kn, bool conj_b, const void* d_b, int64_t ldb, int64_t sb,
+                 void* d_c, int64_t ldc, int64_t sc, const float* rscale, const int* skip) {
+  if (batch < 1 || batch > 65535 || m < 32 || n < 16 || k < 4) return LTB_EUNSUPPORTED;
+  const int64_t rows = b_kn ? k : n, cols = b_kn ? n : k;
+  if (rows > 65535 || cols > (1 << 28)) return LTB_EUNSUPPORTED;
+  const int64_t nb = (sb == 0) ? 1 : batch;  // a B shared by the batch is expanded once
+  WsScope ws(ctx);
+  float* be = nullptr;
+  LTB_TRY(ws.alloc(sizeof(float) * (size_t)nb * 4 * rows * cols, &be));
+  {
+    const dim3 grid((unsigned)std::min<int64_t>((cols + 255) / 256, 64), (unsigned)rows, (unsigned)nb);
+    cexpand_kernel<<<grid, 256, 0, ctx->stream>>>((int)rows, (int)cols, ldb, sb, (const cplx<float>*)d_b, be,
+                                                  b_kn ? 1 : 0, conj_b ? 1 : 0, conj_a ? 1 : 0, skip);
+    LTB_LAUNCH_CHECK(ctx);
+  }
+  return ltb_tc_gemm_f32(ctx, batch, m, 2 * n, 2 * k, false, (const float*)d_a, 2 * lda, 2 * sa, b_kn, be, 2 * cols,
+                         sb == 0 ? 0 : 4 * rows * cols, (float*)d_c, 2 * ldc, 2 * sc, 3, false, nullptr, nullptr,
+                         rscale, nullptr, skip);
+}
 
 int ltb_gemm_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, int64_t k, int op_a, const void* d_a,
                   int64_t lda, int64_t sa, int op_b, const void* d_b, int64_t ldb, int64_t sb, void* d_c, int64_t ldc,
@@ -160,6 +219,18 @@ int ltb_gemm_impl(ltb_ctx* ctx, int dtype, int64_t batch, int64_t m, int64_t n, 
         const int st = ltb_tc_gemm_f32(ctx, batch, m, n, k, a_mn, a, lda, sa, b_mn, b, ldb, sb, c, ldc, sc, 3,
                                        false, nullptr, d_klim, (const float*)d_row_scale,
                                        (const float*)d_col_scale, d_skip);
+        if (st != LTB_EUNSUPPORTED) return st;
+      }
+    }
+    // complex64 without limits / column scaling and with A's K contiguous: one 3xTF32
+    // tensor-core GEMM on the real 2 x 2 representation of B (ltb_cgemm_tc)
+    if constexpr (std::is_same<T, cplx<float>>::value) {
+      if (!d_mlim && !d_nlim && !d_klim && !d_col_scale && (op_a == LTB_OP_N || op_a == LTB_OP_C) && m >= 64 &&
+          n >= 32 && k >= 16) {
+        const bool b_kn = (op_b == LTB_OP_N || op_b == LTB_OP_C);
+        const bool conj_b = (op_b == LTB_OP_C || op_b == LTB_OP_H);
+        const int st = ltb_cgemm_tc(ctx, batch, m, n, k, op_a == LTB_OP_C, a, lda, sa, b_kn, conj_b, b, ldb, sb, c,
+                                    ldc, sc, (const float*)d_row_scale, d_skip);
         if (st != LTB_EUNSUPPORTED) return st;
       }
     }

@@ -47,6 +47,7 @@ struct ltb_pga {
   // (ltb_svt_carry_impl); allocated on first use, warm after the first SVT
   float* vcarry = nullptr;
   double* vcarry64 = nullptr;  // the same for an fp64 real transform domain
+  void* vcarry_c = nullptr;    // complex64 domain, blocked tier: VT of the unique slices (ltb_svt_carry_c64_impl)
   int warm = 0;
   bool carry_off = false;
   bool tc_off = false;        // the tensor-core transform path declined this shape
@@ -405,6 +406,18 @@ int pga_svt(ltb_pga* g, double mu, const int* skip) {
     else if (carry == LTB_EUNSUPPORTED) g->carry_off = true;
     else return carry;
   }
+  // complex64 transform domain with slices beyond shared memory: carried bases for the
+  // blocked Jacobi tier (one slice of every conjugate pair)
+  if (g->hat_dtype == LTB_C64 && !g->carry_off && g_pga_carry) {
+    const int64_t n = std::min(g->I1, g->I2);
+    const int64_t nu = (g->spec->d_uniq && g->spec->P == g->P) ? g->spec->n_unique : g->P;
+    if (!g->vcarry_c) LTB_TRY(ltb_ws_alloc(ctx, 2 * sizeof(float) * nu * n * n, &g->vcarry_c));
+    carry = ltb_svt_mirror_carry_c64_impl(ctx, g->spec, g->P, g->I1, g->I2, g->hat_a, mu, g->hat_b, g->vcarry_c,
+                                          g->warm, skip);
+    if (carry == LTB_OK) g->warm = 1;
+    else if (carry == LTB_EUNSUPPORTED) g->carry_off = true;
+    else return carry;
+  }
   // otherwise (conjugate slice pairs of the real iterate are solved once)
   if (carry != LTB_OK)
     LTB_TRY(ltb_svt_mirror_impl(ctx, g->spec, g->hat_dtype, g->P, g->I1, g->I2, g->hat_a, mu, g->hat_b, skip));
@@ -662,6 +675,7 @@ void ltb_pga_destroy(ltb_pga* g) {
   ltb_ws_free(ctx, g->d_scalars);
   ltb_ws_free(ctx, g->vcarry);
   ltb_ws_free(ctx, g->vcarry64);
+  ltb_ws_free(ctx, g->vcarry_c);
   cudaStreamSynchronize(ctx->stream);
   delete g;
 }

@@ -92,6 +92,13 @@ struct JacobiOut {
   // QR/Cholesky path: stop after a sweep whose rotations all had |<w_p, w_q>| / (|w_p| |w_q|)
   // below this (0: stop only after a sweep without rotations)
   float early_stop = 0.f;
+  // blocked tier: optional device flags (batch), 0 = the slice is known to have no singular
+  // value above tau (||A||_F <= tau): it is not solved and reports kept = 0, sigma = 0
+  const int* pre_active = nullptr;
+  // blocked tier without WANT_V: optional batch x n x n array holding V^T (row j = the right
+  // vector that belongs to working column j, in the Jacobi's own column order); every round
+  // multiplies the rows of its block pair by the pair's accumulated rotations (V <- V J)
+  void* v_acc = nullptr;
 };
 
 template <typename T, bool WANT_V, bool GLOBAL, int TS, int MPL, int MINB>
@@ -681,12 +688,21 @@ __global__ void block_load_kernel(int64_t I1, int64_t I2, const T* __restrict__ 
   }
 }
 
+// rotation accumulation (JacobiOut::v_acc): at most kAccB / 2 columns per block
+constexpr int kAccB = 24;
+template <typename T> __host__ __device__ inline size_t block_acc_offset(int b, int mp) {
+  using R = typename scalar_traits<T>::real;
+  const size_t base = (size_t)2 * b * mp * sizeof(T) + (size_t)2 * b * sizeof(R) + 2 * sizeof(int);
+  return (base + 15) / 16 * 16;
+}
+
 // MPL > 0: each lane holds rows lane + 32 e (e < MPL) of the pair in registers
 // between the dot product and the rotation (mp == 32 MPL); MPL == 0 loops.
-template <typename T, bool WANT_V, int MPL, int NTMAX>
+template <typename T, bool WANT_V, int MPL, int NTMAX, bool ACC = false>
 __global__ void __launch_bounds__(NTMAX, 1)
     jacobi_block_kernel(BlockGeom g, int round, int full, T* __restrict__ W, int* __restrict__ rot,
-                        const int* __restrict__ active, const int* __restrict__ skip, unsigned* __restrict__ relmax) {
+                        const int* __restrict__ active, const int* __restrict__ skip, unsigned* __restrict__ relmax,
+                        T* __restrict__ Vacc) {
   using R = typename scalar_traits<T>::real;
   constexpr bool CPLX = scalar_traits<T>::is_complex;
   if (skip && *skip) return;
@@ -715,6 +731,8 @@ __global__ void __launch_bounds__(NTMAX, 1)
   R* nrm = reinterpret_cast<R*>(C + (size_t)2 * b * mp);
   int* flag = reinterpret_cast<int*>(nrm + 2 * b);
   unsigned* fmax_sh = reinterpret_cast<unsigned*>(flag + 1);  // largest relative rotated |gamma| (float bits)
+  // Vacc: the rotations of this block pair accumulated as a kAccB x kAccB matrix (2b <= kAccB)
+  T* Jb = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(C) + block_acc_offset<T>(b, mp));
   T* Ws = W + s * (int64_t)g.n * mp;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
   auto gcol = [&](int l) { return l < b ? cp0 + l : cq0 + (l - b); };
@@ -730,6 +748,8 @@ __global__ void __launch_bounds__(NTMAX, 1)
     *flag = 0;
     *fmax_sh = 0u;
   }
+  if constexpr (ACC)
+    for (int l = tid; l < kAccB * kAccB; l += nth) Jb[l] = cvt<T>((R)((l / kAccB == l % kAccB) ? 1 : 0));
   __syncthreads();
   for (int l = warp; l < 2 * b; l += nwarps) {
     R s2 = 0;
@@ -744,7 +764,95 @@ __global__ void __launch_bounds__(NTMAX, 1)
   const R tol = eps_of<R>::value * sqrt((R)max(m, 1));
   const int rows = WANT_V ? m + g.n : m;  // rotated rows (padding rows stay zero)
   const int nrounds = full ? 2 * b - 1 : b;
-  for (int r = 0; r < nrounds; ++r) {
+  bool rounds_done = false;
+  if constexpr (MPL > 0) {
+    // cross rounds with one warp per column of block P: the warp's own column stays in
+    // registers over all b inner rounds (only the columns of Q travel through shared memory,
+    // half the shared-memory traffic per rotation)
+    if (!full && nwarps == b) {
+      const int p = warp;
+      const bool pvld = valid(p);
+      T* x = C + (size_t)p * mp;
+      T xr[MPL];
+      if (pvld) {
+#pragma unroll
+        for (int e = 0; e < MPL; e += 2) {
+          const vec2<T> vx = *reinterpret_cast<const vec2<T>*>(x + 2 * lane + 32 * e);
+          xr[e] = vx.a;
+          xr[e + 1] = vx.b;
+        }
+      }
+      bool xdirty = false;
+      for (int r = 0; r < b; ++r) {
+        const int q = b + (p + r) % b;
+        if (pvld && valid(q)) {
+          T* y = C + (size_t)q * mp;
+          T yr[MPL];
+          T ga = zero_v<T>();
+#pragma unroll
+          for (int e = 0; e < MPL; e += 2) {
+            const vec2<T> vy = *reinterpret_cast<const vec2<T>*>(y + 2 * lane + 32 * e);
+            yr[e] = vy.a;
+            yr[e + 1] = vy.b;
+            fma_acc(ga, conj_v(xr[e]), yr[e]);
+            fma_acc(ga, conj_v(xr[e + 1]), yr[e + 1]);
+          }
+          const R gre = warp_sum_r(re_v(ga));
+          const R gim = CPLX ? warp_sum_r(im_v(ga)) : (R)0;
+          const R al = nrm[p], be = nrm[q];
+          const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
+          if (gabs > tol * sqrt(al) * sqrt(be) && al != (R)0 && be != (R)0) {
+            const R zeta = (be - al) / (2 * gabs);
+            const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
+            const R c = (R)1 / sqrt((R)1 + t * t);
+            const R sn = c * t;
+            T ph;
+            if constexpr (CPLX) {
+              ph = T{gre / gabs, -gim / gabs};
+            } else {
+              ph = (gre >= 0) ? (R)1 : (R)-1;
+            }
+#pragma unroll
+            for (int e = 0; e < MPL; e += 2) {
+              const T y0 = ph * yr[e], y1 = ph * yr[e + 1];
+              vec2<T> vy;
+              vy.a = sn * xr[e] + c * y0;
+              vy.b = sn * xr[e + 1] + c * y1;
+              xr[e] = c * xr[e] - sn * y0;
+              xr[e + 1] = c * xr[e + 1] - sn * y1;
+              *reinterpret_cast<vec2<T>*>(y + 2 * lane + 32 * e) = vy;
+            }
+            xdirty = true;
+            if (ACC && lane < kAccB) {
+              const T jp = Jb[lane * kAccB + p];
+              const T jq = ph * Jb[lane * kAccB + q];
+              Jb[lane * kAccB + p] = c * jp - sn * jq;
+              Jb[lane * kAccB + q] = sn * jp + c * jq;
+            }
+            if (lane == 0) {
+              nrm[p] = fmax(al - t * gabs, (R)0);
+              nrm[q] = be + t * gabs;
+              *flag = 1;
+              if (relmax) atomicMax(fmax_sh, __float_as_uint((float)(gabs / (sqrt(al) * sqrt(be)))));
+            }
+          }
+        }
+        __syncthreads();
+      }
+      if (xdirty) {
+#pragma unroll
+        for (int e = 0; e < MPL; e += 2) {
+          vec2<T> vx;
+          vx.a = xr[e];
+          vx.b = xr[e + 1];
+          *reinterpret_cast<vec2<T>*>(x + 2 * lane + 32 * e) = vx;
+        }
+      }
+      __syncthreads();
+      rounds_done = true;
+    }
+  }
+  for (int r = 0; r < nrounds && !rounds_done; ++r) {
     for (int pi = warp; pi < b; pi += nwarps) {
       int p, q;
       if (full) {  // every pair of the 2b columns: circle method over 2b slots
@@ -817,6 +925,12 @@ __global__ void __launch_bounds__(NTMAX, 1)
           y[i] = sn * xv + c * yv;
         }
       }
+      if (ACC && lane < kAccB) {  // the same rotation on columns p, q of the accumulated J (row `lane`)
+        const T jp = Jb[lane * kAccB + p];
+        const T jq = ph * Jb[lane * kAccB + q];
+        Jb[lane * kAccB + p] = c * jp - sn * jq;
+        Jb[lane * kAccB + q] = sn * jp + c * jq;
+      }
       if (lane == 0) {
         nrm[p] = fmax(al - t * gabs, (R)0);
         nrm[q] = be + t * gabs;
@@ -831,6 +945,24 @@ __global__ void __launch_bounds__(NTMAX, 1)
     const int4* src = reinterpret_cast<const int4*>(C + (size_t)l * mp);
     int4* dst = reinterpret_cast<int4*>(Ws + (int64_t)gcol(l) * mp);
     for (int v = lane; v < vpc; v += 32) dst[v] = src[v];
+  }
+  if constexpr (ACC) if (*flag) {
+    // V^T rows of the pair's columns times J: one thread per element index, the 2b values in
+    // registers, J broadcast from shared memory (rows past 2b are identity rows meeting zeros)
+    T* Vs = Vacc + s * (int64_t)g.n * g.n;
+    const int n = g.n;
+    for (int i = tid; i < n; i += nth) {
+      T v[kAccB];
+#pragma unroll
+      for (int l = 0; l < kAccB; ++l) v[l] = (l < 2 * b && valid(l)) ? Vs[(int64_t)gcol(l) * n + i] : zero_v<T>();
+      for (int l2 = 0; l2 < 2 * b; ++l2) {
+        if (!valid(l2)) continue;
+        T acc = zero_v<T>();
+#pragma unroll
+        for (int l = 0; l < kAccB; ++l) fma_acc(acc, v[l], Jb[l * kAccB + l2]);
+        Vs[(int64_t)gcol(l2) * n + i] = acc;
+      }
+    }
   }
   if (tid == 0 && *flag) {
     rot[s] = 1;
@@ -879,9 +1011,11 @@ __global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, Jaco
   const T* Ws = W + s * (int64_t)n * mp;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
   if (tid == 0) *kept_sh = 0;
+  const bool dead = o.pre_active && !o.pre_active[s];
   for (int j = warp; j < n; j += nwarps) {
     R s2 = 0;
-    for (int i = lane; i < m; i += 32) s2 += abs2_v(Ws[(int64_t)j * mp + i]);
+    if (!dead)
+      for (int i = lane; i < m; i += 32) s2 += abs2_v(Ws[(int64_t)j * mp + i]);
     s2 = warp_sum_r(s2);
     if (lane == 0) sig[j] = sqrt(s2);
   }
@@ -906,7 +1040,7 @@ __global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, Jaco
   __syncthreads();
   if (o.kept_out && tid == 0) o.kept_out[s] = *kept_sh;
   if (o.stats && tid == 0) atomicAdd(&o.stats[0], 1ull);
-  if (o.w_out) {
+  if (o.w_out && !dead) {
     T* dst = reinterpret_cast<T*>(o.w_out) + s * (int64_t)n * m;
     for (int j = warp; j < n; j += nwarps) {
       T* dj = dst + (int64_t)rank_sh[j] * m;
@@ -925,13 +1059,15 @@ __global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, Jaco
 }
 
 // the sweep loop of the blocked tier for one kernel variant
-template <typename T, bool WANT_V, int MPL, int NTMAX>
+template <typename T, bool WANT_V, int MPL, int NTMAX, bool ACC = false>
 int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int* rot, int* active, int* count,
                      const JacobiOut& o, int max_sweeps, unsigned* relmax, float early) {
   using R = typename scalar_traits<T>::real;
   const int nbp = g.nb + (g.nb & 1);
-  const size_t smem = 2 * (size_t)g.mp * sizeof(T) * g.b + 2 * g.b * sizeof(R) + 16;
-  auto kern = jacobi_block_kernel<T, WANT_V, MPL, NTMAX>;
+  T* vacc = ACC ? reinterpret_cast<T*>(o.v_acc) : nullptr;
+  const size_t smem = ACC ? block_acc_offset<T>(g.b, g.mp) + (size_t)kAccB * kAccB * sizeof(T)
+                           : 2 * (size_t)g.mp * sizeof(T) * g.b + 2 * g.b * sizeof(R) + 16;
+  auto kern = jacobi_block_kernel<T, WANT_V, MPL, NTMAX, ACC>;
   LTB_TRY(ensure_smem(ctx, kern, smem));
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(ctx->stream, &cap);
@@ -939,7 +1075,7 @@ int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int*
   const int threads = 32 * std::min(g.b, NTMAX / 32);
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int r = 0; r < nbp - 1; ++r) {
-      kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip, relmax);
+      kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip, relmax, vacc);
       LTB_LAUNCH_CHECK(ctx);
     }
     block_sweep_update_kernel<<<1, 256, 0, ctx->stream>>>(batch, rot, active, count, o.stats, relmax, early);
@@ -984,6 +1120,7 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   const size_t fit = (kBlockSmem - 256) / (2 * colb);
   if (fit < 1) return ltb_set_error(ctx, LTB_EUNSUPPORTED, "svd: slice columns too long for the blocked tier");
   g.b = (int)std::min<size_t>(std::min<size_t>((size_t)ntmax / 32, (size_t)std::max(1, (g.n + 1) / 2)), fit);
+  if (!WANT_V && c32 && o.v_acc) g.b = std::min(g.b, kAccB / 2);
   g.nb = (g.n + g.b - 1) / g.b;
   T* W = nullptr;
   int* flags = nullptr;
@@ -1003,8 +1140,12 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   int* count = flags + 3 * batch;
   LTB_CUDA_TRY(ctx, cudaMemsetAsync(rot, 0, sizeof(int) * batch, ctx->stream));
   LTB_CUDA_TRY(ctx, cudaMemsetAsync(flags + 2 * batch, 0, sizeof(int) * batch, ctx->stream));
-  fill_int_kernel<<<grid_for(batch, 256, 1024), 256, 0, ctx->stream>>>(batch, active, 1);
-  LTB_LAUNCH_CHECK(ctx);
+  if (o.pre_active) {
+    LTB_CUDA_TRY(ctx, cudaMemcpyAsync(active, o.pre_active, sizeof(int) * batch, cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    fill_int_kernel<<<grid_for(batch, 256, 1024), 256, 0, ctx->stream>>>(batch, active, 1);
+    LTB_LAUNCH_CHECK(ctx);
+  }
   {
     dim3 grid((unsigned)std::min<int64_t>(((int64_t)g.n * g.mp + 255) / 256, 256), (unsigned)batch);
     block_load_kernel<T, WANT_V><<<grid, 256, 0, ctx->stream>>>(I1, I2, A, W, g);
@@ -1012,7 +1153,19 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   }
   if (g.n > 1) {
     int st = LTB_OK;
-    if constexpr (!WANT_V && (f32 || c32)) {
+    if constexpr (!WANT_V && c32) {
+      if (o.v_acc) {  // rotation accumulation: blocks of at most kAccB / 2 columns, 384 threads
+        if (mpl == 8) st = run_block_sweeps<T, WANT_V, 8, 384, true>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+        else if (mpl == 16) st = run_block_sweeps<T, WANT_V, 16, 384, true>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+        else if (mpl == 32) st = run_block_sweeps<T, WANT_V, 32, 384, true>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+        else st = run_block_sweeps<T, WANT_V, 0, 384, true>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+        LTB_TRY(st);
+        st = -1;
+      }
+    }
+    if (st == -1) {
+      st = LTB_OK;
+    } else if constexpr (!WANT_V && (f32 || c32)) {
       if (mpl == 8) st = run_block_sweeps<T, WANT_V, 8, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
       else if (mpl == 16 && f32) st = run_block_sweeps<T, WANT_V, 16, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
       else if (mpl == 16) st = run_block_sweeps<T, WANT_V, 16, 512>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
@@ -2387,6 +2540,201 @@ int ltb_svt_mirror_impl(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t b
       return LTB_OK;
     }
   });
+}
+
+// ---------------------------------------------------------------- carried complex64 SVT (blocked tier)
+// The PGA iterates of a complex transform domain whose slices do not fit in shared memory
+// (config 4: 99 unique 1024 x 1024 complex slices) cost ~14 cold sweeps of the block-cyclic
+// Jacobi per iteration.  As in the real carried paths the slices' right singular bases are
+// kept between calls: the Jacobi runs on A0 = G V_prev (one tensor-core GEMM), whose columns
+// are nearly orthogonal (a few sweeps with the sqrt(tol) early stop); its columns
+// w_j = sigma_j u_j are G's own (V_prev J is unitary), so the V-free recomposition with G
+// applies unchanged.  Every round of the blocked tier accumulates the rotations of its block
+// pair in shared memory and multiplies the pair's rows of V^T by them (JacobiOut::v_acc), so
+// V <- V_prev J without V riding along as extra rows of the working columns.  (The one-GEMM
+// alternative v_j = G^H w_j / sigma_j^2 amplifies the rounding error of w_j by
+// (sigma_max / sigma_j)^2: useless for the small singular values of a square noisy slice.)
+// One Newton-Schulz step V <- V (3 I - V^H V) / 2 per call keeps the basis unitary to
+// rounding; a slice whose basis leaves the step's convergence region (|V^H V - I| >= 1/4 or
+// NaN) restarts from the identity.  The carried array is VT = V^T (row j = v_j, no
+// conjugation): contiguous right vectors for the accumulation, and K contiguous on the left
+// operand of every GEMM here.  Slices with ||G||_F <= tau have no singular value above tau:
+// they are not solved at all (exact zero output), and when that holds for every slice the
+// GEMMs are skipped too.
+namespace {
+constexpr int kFroChunks = 32;
+
+__global__ void slice_fro_partial_kernel(int64_t S, const cplx<float>* __restrict__ G, double* __restrict__ partial) {
+  const int64_t s = blockIdx.y;
+  const float2* g = reinterpret_cast<const float2*>(G + s * S);
+  double acc = 0.0;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < S; l += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = __ldg(g + l);
+    acc += (double)v.x * v.x + (double)v.y * v.y;
+  }
+  __shared__ double sh[8];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+    partial[s * kFroChunks + blockIdx.x] = t;
+  }
+}
+
+// active[s] = ||G_s||_F > tau (NaN counts as active); skip2[0] = stop flag or no active slice
+__global__ void carry_preactive_kernel(int64_t batch, const double* __restrict__ partial, double tau,
+                                       int* __restrict__ active, const int* __restrict__ skip, int* __restrict__ skip2) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int local = 0;
+  for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
+    double t = 0.0;
+    for (int c = 0; c < kFroChunks; ++c) t += partial[s * kFroChunks + c];
+    const int a = !(t <= tau * tau);
+    active[s] = a;
+    local += a;
+  }
+  if (local) atomicAdd(&cnt, local);
+  __syncthreads();
+  if (threadIdx.x == 0) skip2[0] = ((skip && *skip) || cnt == 0) ? 1 : 0;
+}
+
+__global__ void set_identity_c_kernel(int n, cplx<float>* __restrict__ VT) {
+  const int nn = n * n;
+  const int64_t off = (int64_t)blockIdx.y * nn;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
+    const int i = l / n;
+    VT[off + l] = cplx<float>{(l - i * n == i) ? 1.f : 0.f, 0.f};
+  }
+}
+
+// MT = 1.5 I - 0.5 conj(S)  (the transpose of the Newton-Schulz factor: S is Hermitian);
+// dev[s] = max |S - I| (float bits: non-negative floats order like unsigned integers, NaN above)
+__global__ void ns_combine_c_kernel(int n, const cplx<float>* __restrict__ S, cplx<float>* __restrict__ MT,
+                                    unsigned* __restrict__ dev, const int* skip) {
+  if (skip && *skip) return;
+  const int nn = n * n;
+  const int64_t off = (int64_t)blockIdx.y * nn;
+  float worst = 0.f;
+  bool bad = false;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
+    const int i = l / n;
+    const bool diag = (l - i * n == i);
+    const cplx<float> v = S[off + l];
+    const float dr = v.re - (diag ? 1.f : 0.f);
+    const float e = fmaxf(fabsf(dr), fabsf(v.im));
+    bad |= !(dr == dr) || !(v.im == v.im);
+    worst = fmaxf(worst, e);
+    MT[off + l] = cplx<float>{(diag ? 1.5f : 0.f) - 0.5f * v.re, 0.5f * v.im};
+  }
+  if (bad) worst = __int_as_float(0x7fc00000);
+  atomicMax(&dev[blockIdx.y], __float_as_uint(worst));
+}
+
+// VT <- VTn, or the identity for a basis outside the Newton-Schulz convergence region
+__global__ void carry_commit_kernel(int n, cplx<float>* __restrict__ VT, const cplx<float>* __restrict__ VTn,
+                                    const unsigned* __restrict__ dev, const int* skip) {
+  if (skip && *skip) return;
+  const float d = __uint_as_float(dev[blockIdx.y]);
+  const bool ok = d < 0.25f;
+  const int nn = n * n;
+  const int64_t off = (int64_t)blockIdx.y * nn;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
+    const int i = l / n;
+    VT[off + l] = ok ? VTn[off + l] : cplx<float>{(l - i * n == i) ? 1.f : 0.f, 0.f};
+  }
+}
+}  // namespace
+
+int ltb_svt_carry_c64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const void* d_g, double tau,
+                           void* d_out, void* d_vt, int warm, const int* skip) {
+  using T = cplx<float>;
+  const int64_t m = I1, n = I2, nn = n * n, S = I1 * I2;
+  if (batch <= 0 || batch > 65535 || I1 < I2 || n < 32 || (n & 1)) return LTB_EUNSUPPORTED;
+  // slices that fit in shared memory keep the (much faster) resident kernel
+  if (!ctx->opt_force_blocked && jacobi_smem_bytes<T>((int)m, (int)n, false, (int)(m | 1)) <= kSmemLimit)
+    return LTB_EUNSUPPORTED;
+  const int C = LTB_C64;
+  const T* G = (const T*)d_g;
+  T* out = (T*)d_out;
+  T* VT = (T*)d_vt;
+  WsScope ws(ctx);
+  T *A0 = nullptr, *w = nullptr, *z = nullptr, *Sg = nullptr, *MT = nullptr, *VTn = nullptr;
+  float* d = nullptr;
+  double* partial = nullptr;
+  int *kept = nullptr, *pre = nullptr, *skip2 = nullptr;
+  unsigned* dev = nullptr;
+  if (warm) LTB_TRY(ws.alloc(sizeof(T) * batch * S, &A0));
+  LTB_TRY(ws.alloc(sizeof(T) * batch * n * m, &w));
+  LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &z));
+  LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &Sg));
+  LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &MT));
+  LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &VTn));
+  LTB_TRY(ws.alloc(sizeof(float) * batch * n, &d));
+  LTB_TRY(ws.alloc(sizeof(double) * batch * kFroChunks, &partial));
+  LTB_TRY(ws.alloc(sizeof(int) * batch, &kept));
+  LTB_TRY(ws.alloc(sizeof(int) * batch, &pre));
+  LTB_TRY(ws.alloc(sizeof(int) * 2, &skip2));
+  LTB_TRY(ws.alloc(sizeof(unsigned) * batch, &dev));
+  const dim3 egrid((unsigned)std::min<int64_t>((nn + 1023) / 1024, 64), (unsigned)batch);
+  // slices without a singular value above tau
+  slice_fro_partial_kernel<<<dim3(kFroChunks, (unsigned)batch), 256, 0, ctx->stream>>>(S, G, partial);
+  LTB_LAUNCH_CHECK(ctx);
+  carry_preactive_kernel<<<1, 256, 0, ctx->stream>>>(batch, partial, tau, pre, skip, skip2);
+  LTB_LAUNCH_CHECK(ctx);
+  if (warm) {  // A0 = G V  (B = V stored as VT: n x k)
+    LTB_TRY(ltb_gemm_impl(ctx, C, batch, m, n, n, LTB_OP_N, G, n, S, LTB_OP_T, VT, n, nn, A0, n, S, nullptr, nullptr,
+                          nullptr, nullptr, nullptr, skip2));
+  } else {
+    set_identity_c_kernel<<<egrid, 256, 0, ctx->stream>>>((int)n, VT);
+    LTB_LAUNCH_CHECK(ctx);
+  }
+  JacobiOut o{w, nullptr, nullptr, kept, d, tau, skip2};
+  o.stats = ctx->d_stats;
+  o.pre_active = pre;
+  o.v_acc = VT;
+  LTB_TRY((launch_jacobi_blocked<T, false>(ctx, batch, I1, I2, warm ? A0 : G, o, 40)));
+  // Z = D W^H G (rows limited to the kept count), out = W Z (zeros for a slice that keeps nothing)
+  LTB_TRY(ltb_gemm_impl(ctx, C, batch, n, I2, m, LTB_OP_C, w, m, n * m, LTB_OP_N, G, I2, S, z, I2, nn, kept, nullptr,
+                        nullptr, d, nullptr, skip));
+  LTB_TRY(ltb_gemm_impl(ctx, C, batch, I1, I2, n, LTB_OP_T, w, m, n * m, LTB_OP_N, z, I2, nn, out, I2, S, nullptr,
+                        nullptr, kept, nullptr, nullptr, skip));
+  // Newton-Schulz: S = V^H V = conj(VT) VT^T, VT <- (1.5 I - 0.5 S)^T VT
+  LTB_TRY(ltb_gemm_impl(ctx, C, batch, n, n, n, LTB_OP_C, VT, n, nn, LTB_OP_T, VT, n, nn, Sg, n, nn, nullptr, nullptr,
+                        nullptr, nullptr, nullptr, skip2));
+  LTB_CUDA_TRY(ctx, cudaMemsetAsync(dev, 0, sizeof(unsigned) * batch, ctx->stream));
+  ns_combine_c_kernel<<<egrid, 256, 0, ctx->stream>>>((int)n, Sg, MT, dev, skip2);
+  LTB_LAUNCH_CHECK(ctx);
+  LTB_TRY(ltb_gemm_impl(ctx, C, batch, n, n, n, LTB_OP_N, MT, n, nn, LTB_OP_N, VT, n, nn, VTn, n, nn, nullptr, nullptr,
+                        nullptr, nullptr, nullptr, skip2));
+  carry_commit_kernel<<<egrid, 256, 0, ctx->stream>>>((int)n, VT, VTn, dev, skip2);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
+}
+
+// the carried complex64 SVT on the transform-domain stack of a REAL tensor: one slice of
+// every conjugate pair is solved (VT holds n_unique bases) and its conjugate mirrored
+int ltb_svt_mirror_carry_c64_impl(ltb_ctx* ctx, const ltb_spec* spec, int64_t batch, int64_t I1, int64_t I2,
+                                  const void* d_a, double tau, void* d_out, void* d_vt, int warm, const int* d_skip) {
+  using T = cplx<float>;
+  if (!spec || !spec->d_uniq || spec->P != batch)
+    return ltb_svt_carry_c64_impl(ctx, batch, I1, I2, d_a, tau, d_out, d_vt, warm, d_skip);
+  const int64_t nu = spec->n_unique, S = I1 * I2;
+  WsScope ws(ctx);
+  T *cin = nullptr, *cout = nullptr;
+  LTB_TRY(ws.alloc(sizeof(T) * nu * S, &cin));
+  LTB_TRY(ws.alloc(sizeof(T) * nu * S, &cout));
+  const unsigned grid = grid_for(nu * S, 256, ctx->num_sms * 8);
+  slice_gather_kernel<T><<<grid, 256, 0, ctx->stream>>>(nu, S, spec->d_uniq, (const T*)d_a, cin, d_skip);
+  LTB_LAUNCH_CHECK(ctx);
+  LTB_TRY(ltb_svt_carry_c64_impl(ctx, nu, I1, I2, cin, tau, cout, d_vt, warm, d_skip));
+  slice_mirror_scatter_kernel<T><<<grid, 256, 0, ctx->stream>>>(nu, S, spec->d_uniq, spec->d_partner, cout, (T*)d_out,
+                                                                d_skip);
+  LTB_LAUNCH_CHECK(ctx);
+  return LTB_OK;
 }
 
 extern "C" int ltb_spec_slice_svt(ltb_ctx* ctx, const ltb_spec* spec, int dtype, int64_t batch, int64_t I1,
