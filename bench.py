@@ -713,7 +713,7 @@ def _run_pga(L, nat, torch, m, mask, spec, precision, iters, **cfg_kw):
 
 def bench_extras(L, nat, torch, args, cpu):
     """The other BASELINE configs (parity is in tests/test_gpu_configs.py): config 1 PGA (fp64),
-    config 5 svt / t_svd at n = 128, 256, 512, config 4 PGA at full size (2 iterations)."""
+    config 5 svt / t_svd at n = 128, 256, 512, config 4 PGA at full size (all 50 iterations)."""
     import torch as _t
 
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -746,12 +746,15 @@ def bench_extras(L, nat, torch, args, cpu):
         sv = L.linalg._singular_values(a5, spec5)
         tau = 0.1 * float(np.median(sv))
         _t.cuda.synchronize()
-        t0 = time.perf_counter()
-        L.svt(a5, tau, spec5)
-        t_svt = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        L.t_svd(a5, spec5)
-        t_tsvd = time.perf_counter() - t0
+        t_svt = t_tsvd = float("inf")
+        for _ in range(2):  # best of two: the first call of a shape grows the workspace pool
+            t0 = time.perf_counter()
+            L.svt(a5, tau, spec5)
+            t_svt = min(t_svt, time.perf_counter() - t0)
+        for _ in range(2 if n < 512 else 1):
+            t0 = time.perf_counter()
+            L.t_svd(a5, spec5)
+            t_tsvd = min(t_tsvd, time.perf_counter() - t0)
         # K3 alone on the device-resident transform-domain stack (no host copies, no transforms)
         hat = L.linalg._hat_stack(a5, spec5)
         hout = nat.DeviceArray(hat.shape, hat.dtype)
@@ -785,11 +788,16 @@ def bench_extras(L, nat, torch, args, cpu):
         spec4 = L.make_spec("explicit", (1024, 1024, 3, 64), matrices={3: q, 4: L.build_fourier_matrix(64)})
         m4 = L.l_product(a4.astype(np.float64), b4.astype(np.float64), spec4)
         mask4 = rng.random(m4.shape) < 0.3
-        out["config4_pga"] = {"metric": "PGA completion iters/sec",
-                              "value": _run_pga(L, nat, torch, m4.astype(np.float32), mask4, spec4, "fp32", 2),
-                              "unit": "it/s", "dtype": "c64",
-                              "config": "config4 1024x1024x3x64 Q(x)DFT64, rank 20, Bernoulli(0.3); 2 of 50 iterations",
-                              "note": "1024^2 complex slices run the blocked (block-cyclic) Jacobi tier"}
+        nat.jacobi_stats(reset=True)
+        v4 = _run_pga(L, nat, torch, m4.astype(np.float32), mask4, spec4, "fp32", 50)
+        sl4, sw4 = nat.jacobi_stats(reset=True)
+        out["config4_pga"] = {"metric": "PGA completion iters/sec", "value": v4,
+                              "unit": "it/s", "dtype": "c64", "iterations": 50,
+                              "config": "config4 1024x1024x3x64 Q(x)DFT64, rank 20, Bernoulli(0.3); all 50 iterations",
+                              "jacobi_sweeps_per_slice": sw4 / max(sl4, 1),
+                              "note": "99 unique 1024^2 complex slices on the blocked (block-cyclic) Jacobi tier, "
+                                      "right bases carried between iterations (ltb_svt_carry_c64_impl); "
+                                      "0.72 it/s cold (round-2 start, 2 iterations)"}
     return out
 
 

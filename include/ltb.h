@@ -266,7 +266,8 @@ int ltb_l_product_device(ltb_ctx* ctx, const ltb_spec* spec, int64_t I1, int64_t
  *   forward   : rows shard (ntubes tubes, tube-major) -> gradient step fused into the load
  *               (y = x + beta (x - x_prev), g = y - (P_Omega(y) - p_obs)) -> L -> slice-major
  *   svt       : the slice block; d_v (batch x n x n) carries right bases between calls for
- *               real fp32 / fp64 slices (warm = 0 on the first call), NULL for plain svt
+ *               real fp32 / fp64 slices and (as V^T, complex64) for complex64 slices beyond the
+ *               shared-memory Jacobi tier (warm = 0 on the first call), NULL for plain svt
  *   inverse   : slice-major rows shard -> L^-1, real part -> x_next, fused norms into
  *               d_sums[0..4] = {sum (y-x+)^2, sum x+^2, sum (x+-gt)^2, sum Im^2} (all-reduce
  *               SUM) and d_sums[4] = max x+ (all-reduce MAX); d_gt may be NULL

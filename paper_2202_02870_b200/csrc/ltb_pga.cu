@@ -727,6 +727,10 @@ int ltb_pga_shard_svt(ltb_ctx* ctx, int dtype, int64_t batch, int64_t I1, int64_
                                         (double*)d_v, warm, d_state);
     if (st != LTB_EUNSUPPORTED) return st;
   }
+  if (d_v && dtype == LTB_C64) {  // slices beyond the shared-memory tier: carried blocked Jacobi (d_v holds V^T)
+    const int st = ltb_svt_carry_c64_impl(ctx, batch, I1, I2, d_hat, tau, d_out, d_v, warm, d_state);
+    if (st != LTB_EUNSUPPORTED) return st;
+  }
   return ltb_svt_impl(ctx, dtype, batch, I1, I2, d_hat, tau, nullptr, d_out, d_state);
 }
 

@@ -688,8 +688,12 @@ __global__ void block_load_kernel(int64_t I1, int64_t I2, const T* __restrict__ 
   }
 }
 
-// rotation accumulation (JacobiOut::v_acc): at most kAccB / 2 columns per block
-constexpr int kAccB = 24;
+// rotation accumulation (JacobiOut::v_acc): blocks of at most ACCB / 2 columns (the 2b values of a
+// V^T element index live in one thread's registers): 24 for complex64 / fp64, 32 for fp32
+template <typename T> struct acc_dim { static constexpr int value = 0; };
+template <> struct acc_dim<cplx<float>> { static constexpr int value = 24; };
+template <> struct acc_dim<float> { static constexpr int value = 32; };
+template <> struct acc_dim<double> { static constexpr int value = 24; };
 template <typename T> __host__ __device__ inline size_t block_acc_offset(int b, int mp) {
   using R = typename scalar_traits<T>::real;
   const size_t base = (size_t)2 * b * mp * sizeof(T) + (size_t)2 * b * sizeof(R) + 2 * sizeof(int);
@@ -698,7 +702,7 @@ template <typename T> __host__ __device__ inline size_t block_acc_offset(int b, 
 
 // MPL > 0: each lane holds rows lane + 32 e (e < MPL) of the pair in registers
 // between the dot product and the rotation (mp == 32 MPL); MPL == 0 loops.
-template <typename T, bool WANT_V, int MPL, int NTMAX, bool ACC = false>
+template <typename T, bool WANT_V, int MPL, int NTMAX, int ACCB = 0>
 __global__ void __launch_bounds__(NTMAX, 1)
     jacobi_block_kernel(BlockGeom g, int round, int full, T* __restrict__ W, int* __restrict__ rot,
                         const int* __restrict__ active, const int* __restrict__ skip, unsigned* __restrict__ relmax,
@@ -731,7 +735,9 @@ __global__ void __launch_bounds__(NTMAX, 1)
   R* nrm = reinterpret_cast<R*>(C + (size_t)2 * b * mp);
   int* flag = reinterpret_cast<int*>(nrm + 2 * b);
   unsigned* fmax_sh = reinterpret_cast<unsigned*>(flag + 1);  // largest relative rotated |gamma| (float bits)
-  // Vacc: the rotations of this block pair accumulated as a kAccB x kAccB matrix (2b <= kAccB)
+  // Vacc: the rotations of this block pair accumulated as an ACCB x ACCB matrix (2b <= ACCB)
+  constexpr bool ACC = ACCB > 0;
+  constexpr int kAccB = ACCB > 0 ? ACCB : 1;
   T* Jb = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(C) + block_acc_offset<T>(b, mp));
   T* Ws = W + s * (int64_t)g.n * mp;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
@@ -1048,6 +1054,15 @@ __global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, Jaco
       for (int i = lane; i < m; i += 32) dj[i] = sj[i];
     }
   }
+  if (!WANT_V && o.v_out && o.v_acc) {  // accumulated rotations: row j of V^T goes to its sorted place
+    T* dst = reinterpret_cast<T*>(o.v_out) + s * (int64_t)n * n;
+    const T* src = reinterpret_cast<const T*>(o.v_acc) + s * (int64_t)n * n;
+    for (int j = warp; j < n; j += nwarps) {
+      T* dj = dst + (int64_t)rank_sh[j] * n;
+      const T* sj = src + (int64_t)j * n;
+      for (int i = lane; i < n; i += 32) dj[i] = sj[i];
+    }
+  }
   if (WANT_V && o.v_out) {
     T* dst = reinterpret_cast<T*>(o.v_out) + s * (int64_t)n * n;
     for (int j = warp; j < n; j += nwarps) {
@@ -1059,15 +1074,16 @@ __global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, Jaco
 }
 
 // the sweep loop of the blocked tier for one kernel variant
-template <typename T, bool WANT_V, int MPL, int NTMAX, bool ACC = false>
+template <typename T, bool WANT_V, int MPL, int NTMAX, int ACCB = 0>
 int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int* rot, int* active, int* count,
                      const JacobiOut& o, int max_sweeps, unsigned* relmax, float early) {
   using R = typename scalar_traits<T>::real;
   const int nbp = g.nb + (g.nb & 1);
+  constexpr bool ACC = ACCB > 0;
   T* vacc = ACC ? reinterpret_cast<T*>(o.v_acc) : nullptr;
-  const size_t smem = ACC ? block_acc_offset<T>(g.b, g.mp) + (size_t)kAccB * kAccB * sizeof(T)
+  const size_t smem = ACC ? block_acc_offset<T>(g.b, g.mp) + (size_t)ACCB * ACCB * sizeof(T)
                            : 2 * (size_t)g.mp * sizeof(T) * g.b + 2 * g.b * sizeof(R) + 16;
-  auto kern = jacobi_block_kernel<T, WANT_V, MPL, NTMAX, ACC>;
+  auto kern = jacobi_block_kernel<T, WANT_V, MPL, NTMAX, ACCB>;
   LTB_TRY(ensure_smem(ctx, kern, smem));
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(ctx->stream, &cap);
@@ -1100,7 +1116,12 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   // register-tile variants (fp32 / complex64 SVT): rows padded to 32 * MPL, block size capped
   // by the variant's thread count (registers per thread)
   constexpr bool f32 = std::is_same<T, float>::value, c32 = std::is_same<T, cplx<float>>::value;
+  constexpr bool f64 = std::is_same<T, double>::value;
   int mpl = 0, ntmax = 1024;
+  if constexpr (!WANT_V && f64) {  // fp64 register tiles only with rotation accumulation (t_svd)
+    const int need = (rows + 31) / 32;
+    if (o.v_acc && need <= 16) mpl = need <= 8 ? 8 : 16;
+  }
   if constexpr (!WANT_V && (f32 || c32)) {
     const int need = (rows + 31) / 32;
     if (need <= 8) {
@@ -1120,7 +1141,7 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   const size_t fit = (kBlockSmem - 256) / (2 * colb);
   if (fit < 1) return ltb_set_error(ctx, LTB_EUNSUPPORTED, "svd: slice columns too long for the blocked tier");
   g.b = (int)std::min<size_t>(std::min<size_t>((size_t)ntmax / 32, (size_t)std::max(1, (g.n + 1) / 2)), fit);
-  if (!WANT_V && c32 && o.v_acc) g.b = std::min(g.b, kAccB / 2);
+  if (!WANT_V && (c32 || f32 || f64) && o.v_acc) g.b = std::min(g.b, acc_dim<T>::value / 2);
   g.nb = (g.n + g.b - 1) / g.b;
   T* W = nullptr;
   int* flags = nullptr;
@@ -1130,7 +1151,7 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   int* active = flags + batch;
   unsigned* relmax = nullptr;
   float early = 0.f;
-  if ((f32 || c32) && !WANT_V && g_qr_early > 0.f) {  // svt / values in single precision
+  if ((f32 || c32) && !WANT_V && !o.v_out && g_qr_early > 0.f) {  // svt / values in single precision
     relmax = reinterpret_cast<unsigned*>(flags + 2 * batch);
     early = g_qr_early * sqrtf(FLT_EPSILON * sqrtf((float)std::max(g.m, 1)));
   } else if (o.early_stop > 0.f) {  // the caller's early stop (warm carried fp64 SVT: sqrt(tol))
@@ -1153,12 +1174,13 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   }
   if (g.n > 1) {
     int st = LTB_OK;
-    if constexpr (!WANT_V && c32) {
-      if (o.v_acc) {  // rotation accumulation: blocks of at most kAccB / 2 columns, 384 threads
-        if (mpl == 8) st = run_block_sweeps<T, WANT_V, 8, 384, true>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
-        else if (mpl == 16) st = run_block_sweeps<T, WANT_V, 16, 384, true>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
-        else if (mpl == 32) st = run_block_sweeps<T, WANT_V, 32, 384, true>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
-        else st = run_block_sweeps<T, WANT_V, 0, 384, true>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+    if constexpr (!WANT_V && (c32 || f32 || f64)) {
+      if (o.v_acc) {  // rotation accumulation: blocks of at most ACCB / 2 columns, one warp per column
+        constexpr int AB = acc_dim<T>::value, NT = 16 * AB;
+        if (mpl == 8) st = run_block_sweeps<T, WANT_V, 8, NT, AB>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+        else if (mpl == 16) st = run_block_sweeps<T, WANT_V, 16, NT, AB>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+        else if (mpl == 32 && !f64) st = run_block_sweeps<T, WANT_V, f64 ? 0 : 32, NT, AB>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
+        else st = run_block_sweeps<T, WANT_V, 0, NT, AB>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
         LTB_TRY(st);
         st = -1;
       }
@@ -1187,6 +1209,51 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
   return LTB_OK;
 }
 
+// t_svd on the blocked tier for fp32 / complex64: the V-free kernel variants (register tiles,
+// working columns of m rows instead of m + n) with the rotations accumulated per block pair
+// and applied to V^T (JacobiOut::v_acc), instead of V riding along as extra rows
+template <typename T>
+__global__ void set_identity_kernel(int n, T* __restrict__ VT) {
+  using R = typename scalar_traits<T>::real;
+  const int nn = n * n;
+  const int64_t off = (int64_t)blockIdx.y * nn;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
+    const int i = l / n;
+    VT[off + l] = cvt<T>((R)((l - i * n == i) ? 1 : 0));
+  }
+}
+
+template <typename T>
+int launch_jacobi_blocked_acc(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, JacobiOut o,
+                              int max_sweeps) {
+  const int64_t n = std::min(I1, I2);
+  WsScope ws(ctx);
+  T* vt = nullptr;
+  LTB_TRY(ws.alloc(sizeof(T) * batch * n * n, &vt));
+  const dim3 grid((unsigned)std::min<int64_t>((n * n + 1023) / 1024, 64), (unsigned)batch);
+  set_identity_kernel<T><<<grid, 256, 0, ctx->stream>>>((int)n, vt);
+  LTB_LAUNCH_CHECK(ctx);
+  o.v_acc = vt;
+  return launch_jacobi_blocked<T, false>(ctx, batch, I1, I2, A, o, max_sweeps);
+}
+
+template <typename T, bool WANT_V>
+int launch_jacobi_blocked_any(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, const JacobiOut& o,
+                              int max_sweeps) {
+  if constexpr (WANT_V && (std::is_same<T, float>::value || std::is_same<T, cplx<float>>::value ||
+                           std::is_same<T, double>::value)) {
+    // only when V riding along as n extra rows would not allow larger blocks than the accumulation
+    // does (acc_dim / 2 columns): smaller blocks mean more rounds per sweep (fp64: n = 512 gains,
+    // n = 128 / 256 would lose)
+    const int64_t n = std::min(I1, I2), rows_v = (std::max(I1, I2) + n + 31) / 32 * 32;
+    const int64_t fit_v = (int64_t)((kBlockSmem - 256) / (2 * rows_v * sizeof(T)));
+    const int64_t b_v = std::min<int64_t>(std::min<int64_t>(32, (n + 1) / 2), fit_v);
+    if (batch <= 65535 && n > 1 && b_v <= acc_dim<T>::value / 2)
+      return launch_jacobi_blocked_acc<T>(ctx, batch, I1, I2, A, o, max_sweeps);
+  }
+  return launch_jacobi_blocked<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
+}
+
 template <typename T, bool WANT_V>
 int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, JacobiOut o) {
   using R = typename scalar_traits<T>::real;
@@ -1195,7 +1262,7 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
   if (batch > 0x7fffffff) return ltb_set_error(ctx, LTB_ESHAPE, "svd: batch too large");
   o.stats = ctx->d_stats;
   constexpr bool big = std::is_same<T, cplx<double>>::value;
-  if (ctx->opt_force_blocked) return launch_jacobi_blocked<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
+  if (ctx->opt_force_blocked) return launch_jacobi_blocked_any<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
   auto fits = [&](int mp) { return jacobi_smem_bytes<T>(m, n, WANT_V, mp) <= kSmemLimit; };
   if (m <= 8 && fits(8)) return launch_smem<T, WANT_V, 4, 2>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   if (m <= 32 && fits(32)) return launch_smem<T, WANT_V, 8, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
@@ -1208,7 +1275,7 @@ int launch_jacobi(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* 
     if (m <= 128 && fits(128)) return launch_smem<T, WANT_V, 32, 4>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
   }
   if (fits(m | 1)) return launch_smem<T, WANT_V, 32, 0>(ctx, batch, I1, I2, A, o, max_sweeps, m, n);
-  return launch_jacobi_blocked<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
+  return launch_jacobi_blocked_any<T, WANT_V>(ctx, batch, I1, I2, A, o, max_sweeps);
 }
 
 // ---------------------------------------------------------------- QR-preconditioned fp32 SVT

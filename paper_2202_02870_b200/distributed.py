@@ -485,7 +485,11 @@ def _dist_pga_device(m_rows, mask_rows, cfg, I1, engine, group, gt_rows, mu0, ch
     xs = [torch.zeros_like(m_rows), torch.zeros_like(m_rows), torch.empty_like(m_rows)]
     hat_rows = torch.empty((P, r, I2), dtype=hat_t, device=dev)
     sl_out = torch.empty((nq, I1, I2), dtype=hat_t, device=dev)
-    vcarry = torch.empty((nq, n, n), dtype=dt, device=dev) if not hat_t.is_complex and nq else None
+    # carried right bases of this rank's slices: real domains, and complex64 slices too large for
+    # the shared-memory Jacobi tier (I1 >= I2: ltb_svt_carry_c64_impl; smaller ones ignore it)
+    carry_c = hat_t == torch.complex64 and I1 >= I2 and I1 * I2 * 8 > 200 * 1024
+    vcarry = torch.empty((nq, n, n), dtype=hat_t if carry_c else dt, device=dev) \
+        if nq and (not hat_t.is_complex or carry_c) else None
     state = torch.zeros(2, dtype=torch.int32, device=dev)
     sums = torch.zeros(5, dtype=torch.float64, device=dev)
     recs = torch.zeros((chunk, 5), dtype=torch.float64, device=dev)
