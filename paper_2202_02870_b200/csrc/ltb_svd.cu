@@ -99,6 +99,7 @@ struct JacobiOut {
   // vector that belongs to working column j, in the Jacobi's own column order); every round
   // multiplies the rows of its block pair by the pair's accumulated rotations (V <- V J)
   void* v_acc = nullptr;
+  int* rank_out = nullptr;  // blocked tier: optional batch x n, the sorted position of working column j
 };
 
 template <typename T, bool WANT_V, bool GLOBAL, int TS, int MPL, int MINB>
@@ -1037,6 +1038,7 @@ __global__ void block_finalize_kernel(BlockGeom g, const T* __restrict__ W, Jaco
       rank += (si > sj) || (si == sj && i < j);
     }
     rank_sh[j] = rank;
+    if (o.rank_out) o.rank_out[s * n + j] = rank;
     if (sv_out) sv_out[s * n + rank] = sj;
     const bool keep = sj > (R)o.tau && sj > (R)0;
     kept_local += keep;
@@ -2701,17 +2703,25 @@ __global__ void ns_combine_c_kernel(int n, const cplx<float>* __restrict__ S, cp
   atomicMax(&dev[blockIdx.y], __float_as_uint(worst));
 }
 
-// VT <- VTn, or the identity for a basis outside the Newton-Schulz convergence region
+// VT <- VTn with its rows (the right vectors) moved to their sigma-sorted places, so that the next
+// call's working columns A0 = G V come in descending order of norm (de Rijk's ordering: the large
+// columns share the first blocks and meet each other first), or the identity for a basis outside
+// the Newton-Schulz convergence region
 __global__ void carry_commit_kernel(int n, cplx<float>* __restrict__ VT, const cplx<float>* __restrict__ VTn,
-                                    const unsigned* __restrict__ dev, const int* skip) {
+                                    const unsigned* __restrict__ dev, const int* __restrict__ rank,
+                                    const int* skip) {
   if (skip && *skip) return;
   const float d = __uint_as_float(dev[blockIdx.y]);
   const bool ok = d < 0.25f;
   const int nn = n * n;
   const int64_t off = (int64_t)blockIdx.y * nn;
+  const int* rk = rank + (int64_t)blockIdx.y * n;
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
-    const int i = l / n;
-    VT[off + l] = ok ? VTn[off + l] : cplx<float>{(l - i * n == i) ? 1.f : 0.f, 0.f};
+    const int j = l / n, i = l - j * n;
+    if (ok)
+      VT[off + (int64_t)rk[j] * n + i] = VTn[off + l];
+    else
+      VT[off + l] = cplx<float>{(i == j) ? 1.f : 0.f, 0.f};
   }
 }
 }  // namespace
@@ -2732,8 +2742,9 @@ int ltb_svt_carry_c64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, 
   T *A0 = nullptr, *w = nullptr, *z = nullptr, *Sg = nullptr, *MT = nullptr, *VTn = nullptr;
   float* d = nullptr;
   double* partial = nullptr;
-  int *kept = nullptr, *pre = nullptr, *skip2 = nullptr;
+  int *kept = nullptr, *pre = nullptr, *skip2 = nullptr, *rank = nullptr;
   unsigned* dev = nullptr;
+  LTB_TRY(ws.alloc(sizeof(int) * batch * n, &rank));
   if (warm) LTB_TRY(ws.alloc(sizeof(T) * batch * S, &A0));
   LTB_TRY(ws.alloc(sizeof(T) * batch * n * m, &w));
   LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &z));
@@ -2763,6 +2774,7 @@ int ltb_svt_carry_c64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, 
   o.stats = ctx->d_stats;
   o.pre_active = pre;
   o.v_acc = VT;
+  o.rank_out = rank;
   LTB_TRY((launch_jacobi_blocked<T, false>(ctx, batch, I1, I2, warm ? A0 : G, o, 40)));
   // Z = D W^H G (rows limited to the kept count), out = W Z (zeros for a slice that keeps nothing)
   LTB_TRY(ltb_gemm_impl(ctx, C, batch, n, I2, m, LTB_OP_C, w, m, n * m, LTB_OP_N, G, I2, S, z, I2, nn, kept, nullptr,
@@ -2777,7 +2789,7 @@ int ltb_svt_carry_c64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, 
   LTB_LAUNCH_CHECK(ctx);
   LTB_TRY(ltb_gemm_impl(ctx, C, batch, n, n, n, LTB_OP_N, MT, n, nn, LTB_OP_N, VT, n, nn, VTn, n, nn, nullptr, nullptr,
                         nullptr, nullptr, nullptr, skip2));
-  carry_commit_kernel<<<egrid, 256, 0, ctx->stream>>>((int)n, VT, VTn, dev, skip2);
+  carry_commit_kernel<<<egrid, 256, 0, ctx->stream>>>((int)n, VT, VTn, dev, rank, skip2);
   LTB_LAUNCH_CHECK(ctx);
   return LTB_OK;
 }

@@ -1,6 +1,7 @@
 """Config-4 PGA (1024x1024x3x64, Q (x) DFT64, complex64 transform domain): wall time and blocked-Jacobi
 sweeps of each of the 50 iterations (carried complex SVT), then the per-kernel device time (CUPTI)
-of the last `W` iterations re-run as a profile."""
+of the `W` iterations that follow (argv[3] == "ncu": those iterations between cudaProfilerStart / Stop
+instead, for `ncu --profile-from-start off`)."""
 import sys
 import time
 from collections import defaultdict
@@ -38,6 +39,14 @@ for k in range(1, N + 1):
     print(f"iteration {k:3d}: {dt * 1e3:8.1f} ms  slices {sl} sweeps {sw} ({sw / max(sl, 1):.2f} per slice)  mu {mus[k - 1]:.4g}",
           flush=True)
 print(f"{N} iterations: {total:.2f} s = {N / total:.3f} it/s", flush=True)
+if len(sys.argv) > 3 and sys.argv[3] == "ncu":
+    # under `ncu --profile-from-start off`: only the last W iterations are visible to the profiler
+    torch.cuda.profiler.start()
+    s.run(N + 1, betas[N:N + W], mus[N:N + W], cfg.tol)
+    nat.sync()
+    torch.cuda.profiler.stop()
+    s.close()
+    sys.exit(0)
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
     s.run(N + 1, betas[N:N + W], mus[N:N + W], cfg.tol)
     nat.sync()
