@@ -701,6 +701,39 @@ template <typename T> __host__ __device__ inline size_t block_acc_offset(int b, 
   return (base + 15) / 16 * 16;
 }
 
+__device__ __forceinline__ bool jacobi_pair_params(float g, float al, float be, float tol, float& c, float& sn,
+                                                   float& sg, float& tt, float& gabs, float& rel);
+
+// Register-tile variants of complex64 keep the working columns PAIR-PLANAR in shared memory: every
+// 16-byte group (two consecutive rows) holds (re0, re1, im0, im1) instead of (re0, im0, re1, im1),
+// so that a lane's 16-byte access yields the packed operands (re0, re1) and (im0, im1) of
+// FFMA2 / FMUL2 directly (the copies from and to global memory swap the two middle words).
+template <typename T, int MPL> struct block_pair_planar {
+  static constexpr bool value = MPL > 0 && std::is_same<T, cplx<float>>::value;
+};
+// two consecutive rows of a column as two elements, whatever the layout
+template <bool PLANAR, typename T> __device__ __forceinline__ void ld_rows2(const T* p, T& a, T& b) {
+  if constexpr (PLANAR) {
+    const float4 q = *reinterpret_cast<const float4*>(p);
+    a = T{q.x, q.z};
+    b = T{q.y, q.w};
+  } else {
+    const vec2<T> v = *reinterpret_cast<const vec2<T>*>(p);
+    a = v.a;
+    b = v.b;
+  }
+}
+template <bool PLANAR, typename T> __device__ __forceinline__ void st_rows2(T* p, T a, T b) {
+  if constexpr (PLANAR) {
+    *reinterpret_cast<float4*>(p) = make_float4(a.re, b.re, a.im, b.im);
+  } else {
+    vec2<T> v;
+    v.a = a;
+    v.b = b;
+    *reinterpret_cast<vec2<T>*>(p) = v;
+  }
+}
+
 // MPL > 0: each lane holds rows lane + 32 e (e < MPL) of the pair in registers
 // between the dot product and the rotation (mp == 32 MPL); MPL == 0 loops.
 template <typename T, bool WANT_V, int MPL, int NTMAX, int ACCB = 0>
@@ -745,11 +778,15 @@ __global__ void __launch_bounds__(NTMAX, 1)
   auto gcol = [&](int l) { return l < b ? cp0 + l : cq0 + (l - b); };
   auto valid = [&](int l) { return l < b ? l < np_ : (l - b) < nq_; };
   const int vpc = (int)(mp * sizeof(T) / 16);  // 16-byte vectors per column
+  constexpr bool PLANAR = block_pair_planar<T, MPL>::value;
   for (int l = warp; l < 2 * b; l += nwarps) {
     if (!valid(l)) continue;
     const int4* src = reinterpret_cast<const int4*>(Ws + (int64_t)gcol(l) * mp);
     int4* dst = reinterpret_cast<int4*>(C + (size_t)l * mp);
-    for (int v = lane; v < vpc; v += 32) dst[v] = src[v];
+    for (int v = lane; v < vpc; v += 32) {
+      const int4 t = src[v];
+      dst[v] = PLANAR ? make_int4(t.x, t.z, t.y, t.w) : t;
+    }
   }
   if (tid == 0) {
     *flag = 0;
@@ -758,11 +795,12 @@ __global__ void __launch_bounds__(NTMAX, 1)
   if constexpr (ACC)
     for (int l = tid; l < kAccB * kAccB; l += nth) Jb[l] = cvt<T>((R)((l / kAccB == l % kAccB) ? 1 : 0));
   __syncthreads();
+  const int m_even = min(mp, (m + 1) & ~1);  // (the pair-planar groups pair row m - 1 with a zero padding row)
   for (int l = warp; l < 2 * b; l += nwarps) {
     R s2 = 0;
     if (valid(l)) {
       const T* c = C + (size_t)l * mp;
-      for (int i = lane; i < m; i += 32) s2 += abs2_v(c[i]);
+      for (int i = lane; i < (PLANAR ? m_even : m); i += 32) s2 += abs2_v(c[i]);
     }
     s2 = warp_sum_r(s2);
     if (lane == 0) nrm[l] = s2;
@@ -780,79 +818,187 @@ __global__ void __launch_bounds__(NTMAX, 1)
       const int p = warp;
       const bool pvld = valid(p);
       T* x = C + (size_t)p * mp;
-      T xr[MPL];
-      if (pvld) {
-#pragma unroll
-        for (int e = 0; e < MPL; e += 2) {
-          const vec2<T> vx = *reinterpret_cast<const vec2<T>*>(x + 2 * lane + 32 * e);
-          xr[e] = vx.a;
-          xr[e + 1] = vx.b;
-        }
-      }
       bool xdirty = false;
-      for (int r = 0; r < b; ++r) {
-        const int q = b + (p + r) % b;
-        if (pvld && valid(q)) {
-          T* y = C + (size_t)q * mp;
-          T yr[MPL];
-          T ga = zero_v<T>();
+      if constexpr (std::is_same<R, float>::value) {
+        // fp32 / complex64: packed FFMA2 / FMUL2 on two rows at a time (complex64: the pair-planar
+        // layout gives (re0, re1) and (im0, im1) per 16-byte access), MUFU rotation parameters
+        constexpr int H = MPL / 2;
+        float2 XA[H], XB[CPLX ? H : 1];  // real: XA = rows; complex: XA = re pairs, XB = im pairs
+        if (pvld) {
 #pragma unroll
-          for (int e = 0; e < MPL; e += 2) {
-            const vec2<T> vy = *reinterpret_cast<const vec2<T>*>(y + 2 * lane + 32 * e);
-            yr[e] = vy.a;
-            yr[e + 1] = vy.b;
-            fma_acc(ga, conj_v(xr[e]), yr[e]);
-            fma_acc(ga, conj_v(xr[e + 1]), yr[e + 1]);
-          }
-          const R gre = warp_sum_r(re_v(ga));
-          const R gim = CPLX ? warp_sum_r(im_v(ga)) : (R)0;
-          const R al = nrm[p], be = nrm[q];
-          const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
-          if (gabs > tol * sqrt(al) * sqrt(be) && al != (R)0 && be != (R)0) {
-            const R zeta = (be - al) / (2 * gabs);
-            const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
-            const R c = (R)1 / sqrt((R)1 + t * t);
-            const R sn = c * t;
-            T ph;
+          for (int h = 0; h < H; ++h) {
             if constexpr (CPLX) {
-              ph = T{gre / gabs, -gim / gabs};
+              const float4 q = *reinterpret_cast<const float4*>(x + 2 * lane + 64 * h);
+              XA[h] = make_float2(q.x, q.y);
+              XB[h] = make_float2(q.z, q.w);
             } else {
-              ph = (gre >= 0) ? (R)1 : (R)-1;
+              XA[h] = *reinterpret_cast<const float2*>(x + 2 * lane + 64 * h);
             }
+          }
+        }
+        for (int r = 0; r < b; ++r) {
+          const int q = b + (p + r) % b;
+          if (pvld && valid(q)) {
+            T* y = C + (size_t)q * mp;
+            float2 YA[H], YB[CPLX ? H : 1];
+            float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+              if constexpr (CPLX) {
+                const float4 v = *reinterpret_cast<const float4*>(y + 2 * lane + 64 * h);
+                YA[h] = make_float2(v.x, v.y);
+                YB[h] = make_float2(v.z, v.w);
+                a0 = __ffma2_rn(XA[h], YA[h], a0);  // xr yr
+                a1 = __ffma2_rn(XB[h], YB[h], a1);  // xi yi
+                a2 = __ffma2_rn(XA[h], YB[h], a2);  // xr yi
+                a3 = __ffma2_rn(XB[h], YA[h], a3);  // xi yr
+              } else {
+                YA[h] = *reinterpret_cast<const float2*>(y + 2 * lane + 64 * h);
+                if (h & 1) a1 = __ffma2_rn(XA[h], YA[h], a1);
+                else a0 = __ffma2_rn(XA[h], YA[h], a0);
+              }
+            }
+            float gre, gim = 0.f;
+            if constexpr (CPLX) {
+              gre = warp_sum_r((a0.x + a0.y) + (a1.x + a1.y));
+              gim = warp_sum_r((a2.x + a2.y) - (a3.x + a3.y));
+            } else {
+              gre = warp_sum_r((a0.x + a0.y) + (a1.x + a1.y));
+            }
+            const float al = nrm[p], be = nrm[q];
+            float gsig = gre, pr = 1.f, pi = 0.f;
+            if constexpr (CPLX) {
+              // |g| and the unit phase conj(g) / |g|: scaled by the larger component first (g^2 of a
+              // tiny inner product underflows: a flushed rsqrt input gave an infinite |g| and a
+              // rotation by NaN), one Newton step on the MUFU rsqrt so that |ph| = 1 to rounding
+              const float smax = fmaxf(fabsf(gre), fabsf(gim));
+              const bool tiny = !(smax >= FLT_MIN);
+              const float k = rcp_apx(tiny ? 1.f : smax);
+              const float gr = gre * k, gi = gim * k;
+              const float g2 = fmaf(gr, gr, gi * gi);  // in [1, 2]
+              float rinv = rsqrt_apx(g2);
+              rinv = rinv * fmaf(-0.5f * g2 * rinv, rinv, 1.5f);
+              gsig = tiny ? 0.f : smax * (g2 * rinv);
+              pr = gr * rinv;
+              pi = -gi * rinv;
+            }
+            float c, sn, sg, tt, gabs, rel;
+            if (jacobi_pair_params(gsig, al, be, tol, c, sn, sg, tt, gabs, rel)) {
+              if constexpr (CPLX) {
+                // x' = c x + a y, y' = sn x + bb y with a = -sn ph, bb = c ph
+                const float ar = -sn * pr, ai = -sn * pi, br = c * pr, bi = c * pi;
+                const float2 C2 = make_float2(c, c), S2 = make_float2(sn, sn);
+                const float2 AR = make_float2(ar, ar), AI = make_float2(ai, ai), NAI = make_float2(-ai, -ai);
+                const float2 BR = make_float2(br, br), BI = make_float2(bi, bi), NBI = make_float2(-bi, -bi);
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                  const float2 yr2 = __ffma2_rn(NBI, YB[h], __ffma2_rn(BR, YA[h], __fmul2_rn(S2, XA[h])));
+                  const float2 yi2 = __ffma2_rn(BI, YA[h], __ffma2_rn(BR, YB[h], __fmul2_rn(S2, XB[h])));
+                  const float2 xr2 = __ffma2_rn(NAI, YB[h], __ffma2_rn(AR, YA[h], __fmul2_rn(C2, XA[h])));
+                  const float2 xi2 = __ffma2_rn(AI, YA[h], __ffma2_rn(AR, YB[h], __fmul2_rn(C2, XB[h])));
+                  XA[h] = xr2;
+                  XB[h] = xi2;
+                  *reinterpret_cast<float4*>(y + 2 * lane + 64 * h) = make_float4(yr2.x, yr2.y, yi2.x, yi2.y);
+                }
+              } else {
+                const float2 C2 = make_float2(c, c), S2 = make_float2(sn, sn);
+                const float2 NSQ = make_float2(-sn * sg, -sn * sg), CQ = make_float2(c * sg, c * sg);
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                  const float2 yn = __ffma2_rn(S2, XA[h], __fmul2_rn(CQ, YA[h]));
+                  XA[h] = __ffma2_rn(C2, XA[h], __fmul2_rn(NSQ, YA[h]));
+                  *reinterpret_cast<float2*>(y + 2 * lane + 64 * h) = yn;
+                }
+              }
+              xdirty = true;
+              if (ACC && lane < kAccB) {
+                T ph;
+                if constexpr (CPLX) ph = T{pr, pi};
+                else ph = sg;
+                const T jp = Jb[lane * kAccB + p];
+                const T jq = ph * Jb[lane * kAccB + q];
+                Jb[lane * kAccB + p] = c * jp - sn * jq;
+                Jb[lane * kAccB + q] = sn * jp + c * jq;
+              }
+              if (lane == 0) {
+                nrm[p] = fmaxf(al - tt * gabs, 0.f);
+                nrm[q] = be + tt * gabs;
+                *flag = 1;
+                if (relmax) atomicMax(fmax_sh, __float_as_uint(rel));
+              }
+            }
+          }
+          __syncthreads();
+        }
+        if (xdirty) {
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            if constexpr (CPLX)
+              *reinterpret_cast<float4*>(x + 2 * lane + 64 * h) = make_float4(XA[h].x, XA[h].y, XB[h].x, XB[h].y);
+            else
+              *reinterpret_cast<float2*>(x + 2 * lane + 64 * h) = XA[h];
+          }
+        }
+      } else {
+        T xr[MPL];
+        if (pvld) {
+#pragma unroll
+          for (int e = 0; e < MPL; e += 2) ld_rows2<PLANAR>(x + 2 * lane + 32 * e, xr[e], xr[e + 1]);
+        }
+        for (int r = 0; r < b; ++r) {
+          const int q = b + (p + r) % b;
+          if (pvld && valid(q)) {
+            T* y = C + (size_t)q * mp;
+            T yr[MPL];
+            T ga = zero_v<T>();
 #pragma unroll
             for (int e = 0; e < MPL; e += 2) {
-              const T y0 = ph * yr[e], y1 = ph * yr[e + 1];
-              vec2<T> vy;
-              vy.a = sn * xr[e] + c * y0;
-              vy.b = sn * xr[e + 1] + c * y1;
-              xr[e] = c * xr[e] - sn * y0;
-              xr[e + 1] = c * xr[e + 1] - sn * y1;
-              *reinterpret_cast<vec2<T>*>(y + 2 * lane + 32 * e) = vy;
+              ld_rows2<PLANAR>(y + 2 * lane + 32 * e, yr[e], yr[e + 1]);
+              fma_acc(ga, conj_v(xr[e]), yr[e]);
+              fma_acc(ga, conj_v(xr[e + 1]), yr[e + 1]);
             }
-            xdirty = true;
-            if (ACC && lane < kAccB) {
-              const T jp = Jb[lane * kAccB + p];
-              const T jq = ph * Jb[lane * kAccB + q];
-              Jb[lane * kAccB + p] = c * jp - sn * jq;
-              Jb[lane * kAccB + q] = sn * jp + c * jq;
-            }
-            if (lane == 0) {
-              nrm[p] = fmax(al - t * gabs, (R)0);
-              nrm[q] = be + t * gabs;
-              *flag = 1;
-              if (relmax) atomicMax(fmax_sh, __float_as_uint((float)(gabs / (sqrt(al) * sqrt(be)))));
+            const R gre = warp_sum_r(re_v(ga));
+            const R gim = CPLX ? warp_sum_r(im_v(ga)) : (R)0;
+            const R al = nrm[p], be = nrm[q];
+            const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
+            if (gabs > tol * sqrt(al) * sqrt(be) && al != (R)0 && be != (R)0) {
+              const R zeta = (be - al) / (2 * gabs);
+              const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
+              const R c = (R)1 / sqrt((R)1 + t * t);
+              const R sn = c * t;
+              T ph;
+              if constexpr (CPLX) {
+                ph = T{gre / gabs, -gim / gabs};
+              } else {
+                ph = (gre >= 0) ? (R)1 : (R)-1;
+              }
+#pragma unroll
+              for (int e = 0; e < MPL; e += 2) {
+                const T y0 = ph * yr[e], y1 = ph * yr[e + 1];
+                st_rows2<PLANAR>(y + 2 * lane + 32 * e, sn * xr[e] + c * y0, sn * xr[e + 1] + c * y1);
+                xr[e] = c * xr[e] - sn * y0;
+                xr[e + 1] = c * xr[e + 1] - sn * y1;
+              }
+              xdirty = true;
+              if (ACC && lane < kAccB) {
+                const T jp = Jb[lane * kAccB + p];
+                const T jq = ph * Jb[lane * kAccB + q];
+                Jb[lane * kAccB + p] = c * jp - sn * jq;
+                Jb[lane * kAccB + q] = sn * jp + c * jq;
+              }
+              if (lane == 0) {
+                nrm[p] = fmax(al - t * gabs, (R)0);
+                nrm[q] = be + t * gabs;
+                *flag = 1;
+                if (relmax) atomicMax(fmax_sh, __float_as_uint((float)(gabs / (sqrt(al) * sqrt(be)))));
+              }
             }
           }
+          __syncthreads();
         }
-        __syncthreads();
-      }
-      if (xdirty) {
+        if (xdirty) {
 #pragma unroll
-        for (int e = 0; e < MPL; e += 2) {
-          vec2<T> vx;
-          vx.a = xr[e];
-          vx.b = xr[e + 1];
-          *reinterpret_cast<vec2<T>*>(x + 2 * lane + 32 * e) = vx;
+          for (int e = 0; e < MPL; e += 2) st_rows2<PLANAR>(x + 2 * lane + 32 * e, xr[e], xr[e + 1]);
         }
       }
       __syncthreads();
@@ -884,12 +1030,8 @@ __global__ void __launch_bounds__(NTMAX, 1)
 #pragma unroll
         for (int e = 0; e < MPL; e += 2) {
           const int i = 2 * lane + 32 * e;
-          const vec2<T> vx = *reinterpret_cast<const vec2<T>*>(x + i);
-          const vec2<T> vy = *reinterpret_cast<const vec2<T>*>(y + i);
-          xr[e] = vx.a;
-          xr[e + 1] = vx.b;
-          yr[e] = vy.a;
-          yr[e + 1] = vy.b;
+          ld_rows2<PLANAR>(x + i, xr[e], xr[e + 1]);
+          ld_rows2<PLANAR>(y + i, yr[e], yr[e + 1]);
           fma_acc(ga, conj_v(xr[e]), yr[e]);
           fma_acc(ga, conj_v(xr[e + 1]), yr[e + 1]);
         }
@@ -916,13 +1058,8 @@ __global__ void __launch_bounds__(NTMAX, 1)
         for (int e = 0; e < MPL; e += 2) {
           const int i = 2 * lane + 32 * e;
           const T y0 = ph * yr[e], y1 = ph * yr[e + 1];
-          vec2<T> vx, vy;
-          vx.a = c * xr[e] - sn * y0;
-          vx.b = c * xr[e + 1] - sn * y1;
-          vy.a = sn * xr[e] + c * y0;
-          vy.b = sn * xr[e + 1] + c * y1;
-          *reinterpret_cast<vec2<T>*>(x + i) = vx;
-          *reinterpret_cast<vec2<T>*>(y + i) = vy;
+          st_rows2<PLANAR>(x + i, c * xr[e] - sn * y0, c * xr[e + 1] - sn * y1);
+          st_rows2<PLANAR>(y + i, sn * xr[e] + c * y0, sn * xr[e + 1] + c * y1);
         }
       } else {
         for (int i = lane; i < rows; i += 32) {
@@ -951,14 +1088,58 @@ __global__ void __launch_bounds__(NTMAX, 1)
     if (!valid(l)) continue;
     const int4* src = reinterpret_cast<const int4*>(C + (size_t)l * mp);
     int4* dst = reinterpret_cast<int4*>(Ws + (int64_t)gcol(l) * mp);
-    for (int v = lane; v < vpc; v += 32) dst[v] = src[v];
+    for (int v = lane; v < vpc; v += 32) {
+      const int4 t = src[v];
+      dst[v] = PLANAR ? make_int4(t.x, t.z, t.y, t.w) : t;
+    }
   }
   if constexpr (ACC) if (*flag) {
     // V^T rows of the pair's columns times J: one thread per element index, the 2b values in
     // registers, J broadcast from shared memory (rows past 2b are identity rows meeting zeros)
     T* Vs = Vacc + s * (int64_t)g.n * g.n;
     const int n = g.n;
-    for (int i = tid; i < n; i += nth) {
+    bool packed_done = false;
+    if constexpr (std::is_same<T, cplx<float>>::value) {
+      // complex64, n even: two element indices per thread, packed across the two (FFMA2):
+      // (v0, v1) (x) (j, j) with J staged as (re, re, im, im) in the (now free) column buffer;
+      // half the FMA instructions and half the shared-memory reads per element
+      if (!(n & 1) && mp * 2 * b * sizeof(T) >= (size_t)kAccB * kAccB * sizeof(float4)) {
+        __syncthreads();  // the copy-out above has read the columns
+        float4* JP = reinterpret_cast<float4*>(C);
+        for (int l = tid; l < kAccB * kAccB; l += nth) {
+          const T j = Jb[l];
+          JP[l] = make_float4(j.re, j.re, j.im, j.im);
+        }
+        __syncthreads();
+        for (int ip = tid; ip < n / 2; ip += nth) {
+          float2 Vr[kAccB], Vi[kAccB];
+#pragma unroll
+          for (int l = 0; l < kAccB; ++l) {
+            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (l < 2 * b && valid(l)) q = *reinterpret_cast<const float4*>(Vs + (int64_t)gcol(l) * n + 2 * ip);
+            Vr[l] = make_float2(q.x, q.z);
+            Vi[l] = make_float2(q.y, q.w);
+          }
+          for (int l2 = 0; l2 < 2 * b; ++l2) {
+            if (!valid(l2)) continue;
+            float2 r1 = make_float2(0.f, 0.f), r2 = r1, i1 = r1, i2 = r1;
+#pragma unroll
+            for (int l = 0; l < kAccB; ++l) {
+              const float4 j4 = JP[l * kAccB + l2];
+              const float2 JR = make_float2(j4.x, j4.y), JI = make_float2(j4.z, j4.w);
+              r1 = __ffma2_rn(Vr[l], JR, r1);
+              r2 = __ffma2_rn(Vi[l], JI, r2);
+              i1 = __ffma2_rn(Vr[l], JI, i1);
+              i2 = __ffma2_rn(Vi[l], JR, i2);
+            }
+            *reinterpret_cast<float4*>(Vs + (int64_t)gcol(l2) * n + 2 * ip) =
+                make_float4(r1.x - r2.x, i1.x + i2.x, r1.y - r2.y, i1.y + i2.y);
+          }
+        }
+        packed_done = true;
+      }
+    }
+    for (int i = tid; i < n && !packed_done; i += nth) {
       T v[kAccB];
 #pragma unroll
       for (int l = 0; l < kAccB; ++l) v[l] = (l < 2 * b && valid(l)) ? Vs[(int64_t)gcol(l) * n + i] : zero_v<T>();

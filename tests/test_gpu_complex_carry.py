@@ -104,9 +104,10 @@ def test_carried_complex_svt_blocked(shape, force_blocked):
     assert max(sweeps[1:]) < sweeps[0], sweeps
 
 
-def test_carried_complex_svt_rank_deficient_restarts(force_blocked):
-    """Vanishing singular values: v_j = G^H w_j / sigma_j^2 is undefined, the guard restarts the
-    slice's basis from the identity and the results stay correct call after call."""
+def test_carried_complex_svt_rank_deficient(force_blocked):
+    """Vanishing singular values: the tiny columns' inner products are so small that their squares
+    underflow (the packed rotation computes the phase scaled by the larger component); every
+    call stays correct, the carried basis finite and unitary."""
     rng = np.random.default_rng(8)
     batch, i1, i2 = 2, 80, 40
     g = (crand(rng, (batch, i1, 5)) @ crand(rng, (batch, 5, i2))).astype(np.complex64)  # rank 5 of 40
@@ -117,7 +118,8 @@ def test_carried_complex_svt_rank_deficient_restarts(force_blocked):
         assert rel_err(got, ref) < 1e-4
         v = vt.numpy()
         assert np.all(np.isfinite(v))
-        assert np.abs(v[0].conj() @ v[0].T - np.eye(i2)).max() < 1e-3
+        for b in range(batch):
+            assert np.abs(v[b].conj() @ v[b].T - np.eye(i2)).max() < 1e-4
 
 
 def test_carried_complex_svt_unsupported_shapes():
