@@ -1098,48 +1098,7 @@ __global__ void __launch_bounds__(NTMAX, 1)
     // registers, J broadcast from shared memory (rows past 2b are identity rows meeting zeros)
     T* Vs = Vacc + s * (int64_t)g.n * g.n;
     const int n = g.n;
-    bool packed_done = false;
-    if constexpr (std::is_same<T, cplx<float>>::value) {
-      // complex64, n even: two element indices per thread, packed across the two (FFMA2):
-      // (v0, v1) (x) (j, j) with J staged as (re, re, im, im) in the (now free) column buffer;
-      // half the FMA instructions and half the shared-memory reads per element
-      if (!(n & 1) && mp * 2 * b * sizeof(T) >= (size_t)kAccB * kAccB * sizeof(float4)) {
-        __syncthreads();  // the copy-out above has read the columns
-        float4* JP = reinterpret_cast<float4*>(C);
-        for (int l = tid; l < kAccB * kAccB; l += nth) {
-          const T j = Jb[l];
-          JP[l] = make_float4(j.re, j.re, j.im, j.im);
-        }
-        __syncthreads();
-        for (int ip = tid; ip < n / 2; ip += nth) {
-          float2 Vr[kAccB], Vi[kAccB];
-#pragma unroll
-          for (int l = 0; l < kAccB; ++l) {
-            float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (l < 2 * b && valid(l)) q = *reinterpret_cast<const float4*>(Vs + (int64_t)gcol(l) * n + 2 * ip);
-            Vr[l] = make_float2(q.x, q.z);
-            Vi[l] = make_float2(q.y, q.w);
-          }
-          for (int l2 = 0; l2 < 2 * b; ++l2) {
-            if (!valid(l2)) continue;
-            float2 r1 = make_float2(0.f, 0.f), r2 = r1, i1 = r1, i2 = r1;
-#pragma unroll
-            for (int l = 0; l < kAccB; ++l) {
-              const float4 j4 = JP[l * kAccB + l2];
-              const float2 JR = make_float2(j4.x, j4.y), JI = make_float2(j4.z, j4.w);
-              r1 = __ffma2_rn(Vr[l], JR, r1);
-              r2 = __ffma2_rn(Vi[l], JI, r2);
-              i1 = __ffma2_rn(Vr[l], JI, i1);
-              i2 = __ffma2_rn(Vi[l], JR, i2);
-            }
-            *reinterpret_cast<float4*>(Vs + (int64_t)gcol(l2) * n + 2 * ip) =
-                make_float4(r1.x - r2.x, i1.x + i2.x, r1.y - r2.y, i1.y + i2.y);
-          }
-        }
-        packed_done = true;
-      }
-    }
-    for (int i = tid; i < n && !packed_done; i += nth) {
+    for (int i = tid; i < n; i += nth) {
       T v[kAccB];
 #pragma unroll
       for (int l = 0; l < kAccB; ++l) v[l] = (l < 2 * b && valid(l)) ? Vs[(int64_t)gcol(l) * n + i] : zero_v<T>();
