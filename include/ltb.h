@@ -77,7 +77,8 @@ enum ltb_option {
   LTB_OPT_FORCE_BLOCKED_SVD = 1, /* route every SVD / SVT through the blocked Jacobi tier */
   LTB_OPT_TC_TIMELINE = 2,       /* tcgen05 GEMM / transform: per-tile stamps of CTA 0 */
   LTB_OPT_QR_TIMELINE = 3,       /* QR-preconditioned Jacobi: stage stamps of CTA 0 */
-  LTB_OPT_JACOBI_PAIRS = 4       /* warm Cholesky-path Jacobi: 0 blocks of 4 columns, 1 one pair per team, 2 blocks of 2 */
+  LTB_OPT_JACOBI_PAIRS = 4,      /* warm Cholesky-path Jacobi: 0 blocks of 4 columns, 1 one pair per team, 2 blocks of 2 */
+  LTB_OPT_FULL_SWEEPS = 5        /* carried complex SVT: full sweeps instead of the truncated ones (cross-checks) */
 };
 int ltb_ctx_set_option(ltb_ctx* ctx, int option, int64_t value);
 /* make ctx's device the calling host thread's current CUDA device (contexts of several

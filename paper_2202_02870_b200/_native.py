@@ -18,7 +18,7 @@ from .errors import STATUS_TO_ERROR, DeviceError
 LIB_PATH = Path(__file__).resolve().with_name("libltb.so")
 
 F32, F64, C64, C128 = 0, 1, 2, 3
-OPT_FORCE_BLOCKED_SVD, OPT_TC_TIMELINE, OPT_QR_TIMELINE, OPT_JACOBI_PAIRS = 1, 2, 3, 4
+OPT_FORCE_BLOCKED_SVD, OPT_TC_TIMELINE, OPT_QR_TIMELINE, OPT_JACOBI_PAIRS, OPT_FULL_SWEEPS = 1, 2, 3, 4, 5
 TUBE_MAJOR, SLICE_MAJOR = 0, 1
 OP_N, OP_T, OP_C, OP_H = 0, 1, 2, 3
 

@@ -146,6 +146,7 @@ struct ltb_ctx {
   int opt_force_blocked = 0;                       // route every SVD through the blocked Jacobi tier
   unsigned long long* opt_tc_timeline = nullptr;   // tcgen05 kernels: per-tile clock stamps (CTA 0)
   unsigned long long* opt_qr_timeline = nullptr;   // QR-preconditioned Jacobi: stage stamps (CTA 0)
+  int opt_full_sweeps = 0;   // carried complex SVT: no truncated sweeps
   int opt_jacobi_pairs = 0;  // warm Cholesky Jacobi: 0 / 2 two-column blocks, 1 one pair per team, 3 four-column blocks
 };
 

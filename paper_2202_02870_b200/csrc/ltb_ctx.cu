@@ -156,6 +156,7 @@ int ltb_ctx_set_option(ltb_ctx* ctx, int option, int64_t value) {
     case LTB_OPT_TC_TIMELINE: ctx->opt_tc_timeline = (unsigned long long*)(uintptr_t)value; return LTB_OK;
     case LTB_OPT_QR_TIMELINE: ctx->opt_qr_timeline = (unsigned long long*)(uintptr_t)value; return LTB_OK;
     case LTB_OPT_JACOBI_PAIRS: ctx->opt_jacobi_pairs = (int)value; return LTB_OK;
+    case LTB_OPT_FULL_SWEEPS: ctx->opt_full_sweeps = value != 0; return LTB_OK;
   }
   return ltb_set_error(ctx, LTB_EPARAM, "unknown context option %d", option);
 }

@@ -100,6 +100,13 @@ struct JacobiOut {
   // multiplies the rows of its block pair by the pair's accumulated rotations (V <- V J)
   void* v_acc = nullptr;
   int* rank_out = nullptr;  // blocked tier: optional batch x n, the sorted position of working column j
+  // blocked tier, SVT of complex64 slices with sigma-sorted working columns (the carried path): only
+  // block pairs that involve one of the slice's leading blocks are rotated; the untouched columns are
+  // certified to have no singular value above tau (see block_certify), else the slice is finished
+  // with full sweeps
+  bool truncate = false;
+  const int* lead = nullptr;  // (internal) batch: leading blocks of each slice
+  float small2 = 0.f;         // (internal) pairs of two columns with squared norms <= small2 are left alone
 };
 
 template <typename T, bool WANT_V, bool GLOBAL, int TS, int MPL, int MINB>
@@ -740,7 +747,7 @@ template <typename T, bool WANT_V, int MPL, int NTMAX, int ACCB = 0>
 __global__ void __launch_bounds__(NTMAX, 1)
     jacobi_block_kernel(BlockGeom g, int round, int full, T* __restrict__ W, int* __restrict__ rot,
                         const int* __restrict__ active, const int* __restrict__ skip, unsigned* __restrict__ relmax,
-                        T* __restrict__ Vacc) {
+                        T* __restrict__ Vacc, const int* __restrict__ lead, float small2) {
   using R = typename scalar_traits<T>::real;
   constexpr bool CPLX = scalar_traits<T>::is_complex;
   if (skip && *skip) return;
@@ -761,6 +768,10 @@ __global__ void __launch_bounds__(NTMAX, 1)
   // needs its internal pairs on the first round of the sweep
   const bool pv = P < g.nb, qv = Q < g.nb;
   if (!(pv && qv) && !(full && (pv || qv))) return;
+  if (lead) {  // truncated sweeps: pairs of two trailing blocks are left alone
+    const int kl = lead[s];
+    if ((!pv || P >= kl) && (!qv || Q >= kl)) return;
+  }
   const int b = g.b, mp = g.mp, m = g.m;
   const int cp0 = P * b, cq0 = Q * b;
   const int np_ = pv ? min(b, g.n - cp0) : 0, nq_ = qv ? min(b, g.n - cq0) : 0;
@@ -883,7 +894,7 @@ __global__ void __launch_bounds__(NTMAX, 1)
               pi = -gi * rinv;
             }
             float c, sn, sg, tt, gabs, rel;
-            if (jacobi_pair_params(gsig, al, be, tol, c, sn, sg, tt, gabs, rel)) {
+            if (!(al <= small2 && be <= small2) && jacobi_pair_params(gsig, al, be, tol, c, sn, sg, tt, gabs, rel)) {
               if constexpr (CPLX) {
                 // x' = c x + a y, y' = sn x + bb y with a = -sn ph, bb = c ph
                 const float ar = -sn * pr, ai = -sn * pi, br = c * pr, bi = c * pi;
@@ -961,7 +972,8 @@ __global__ void __launch_bounds__(NTMAX, 1)
             const R gim = CPLX ? warp_sum_r(im_v(ga)) : (R)0;
             const R al = nrm[p], be = nrm[q];
             const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
-            if (gabs > tol * sqrt(al) * sqrt(be) && al != (R)0 && be != (R)0) {
+            if (gabs > tol * sqrt(al) * sqrt(be) && al != (R)0 && be != (R)0 &&
+                !((float)al <= small2 && (float)be <= small2)) {
               const R zeta = (be - al) / (2 * gabs);
               const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
               const R c = (R)1 / sqrt((R)1 + t * t);
@@ -1043,6 +1055,7 @@ __global__ void __launch_bounds__(NTMAX, 1)
       const R al = nrm[p], be = nrm[q];
       const R gabs = CPLX ? hypot(gre, gim) : fabs(gre);
       if (!(gabs > tol * sqrt(al) * sqrt(be)) || al == (R)0 || be == (R)0) continue;
+      if ((float)al <= small2 && (float)be <= small2) continue;  // truncated sweeps: two small columns
       const R zeta = (be - al) / (2 * gabs);
       const R t = (zeta >= 0 ? (R)1 : (R)-1) / (fabs(zeta) + hypot((R)1, zeta));
       const R c = (R)1 / sqrt((R)1 + t * t);
@@ -1233,7 +1246,8 @@ int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int*
   const int threads = 32 * std::min(g.b, NTMAX / 32);
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int r = 0; r < nbp - 1; ++r) {
-      kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip, relmax, vacc);
+      kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip, relmax, vacc,
+                                                  o.lead, o.lead ? o.small2 : 0.f);
       LTB_LAUNCH_CHECK(ctx);
     }
     block_sweep_update_kernel<<<1, 256, 0, ctx->stream>>>(batch, rot, active, count, o.stats, relmax, early);
@@ -1246,9 +1260,124 @@ int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int*
   return LTB_OK;
 }
 
+// ---- truncated sweeps (JacobiOut::truncate)
+// With the working columns in descending order of norm (the carried, sigma-sorted bases) the
+// singular values above tau live in the first few blocks.  A sweep that rotates only the pairs
+// involving one of these `lead` blocks still converges (every rotation lowers off(W^H W)), to
+// W = [W_L | W_S] with the columns of W_L mutually orthogonal and orthogonal to every column of
+// W_S: the singular values of the slice are then the norms of W_L's columns together with the
+// singular values of W_S, whatever the angles inside W_S.  The SVT only needs to know that no
+// singular value of W_S exceeds tau: with S = W_S^H W_S / tau^2, lambda_max(S)^64 <= tr(S^64),
+// so tr(S^64) <= 0.9 certifies it (six squarings of the Gram matrix on the tensor cores; the
+// bound is within n^(1/128) = 5.6% of sigma_max(W_S)).  A slice that fails is finished with full
+// sweeps.  lead = the blocks holding the columns with norm above 0.7 tau, plus two blocks.
+constexpr float kLeadTheta = 0.7f;
+constexpr double kCertifyBound = 0.9;
+constexpr int kCertifySquarings = 6;
+constexpr int kTruncSweeps = 16;  // truncated sweeps before a slice is handed to the full ones
+
+template <typename T>
+__global__ void block_lead_kernel(BlockGeom g, const T* __restrict__ W, double tau, int* __restrict__ lead) {
+  using R = typename scalar_traits<T>::real;
+  const int64_t s = blockIdx.x;
+  const T* Ws = W + s * (int64_t)g.n * g.mp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  __shared__ int last;
+  if (threadIdx.x == 0) last = -1;
+  __syncthreads();
+  const double thr = (double)kLeadTheta * tau * (double)kLeadTheta * tau;
+  for (int j = warp; j < g.n; j += nwarps) {
+    R s2 = 0;
+    for (int i = lane; i < g.m; i += 32) s2 += abs2_v(Ws[(int64_t)j * g.mp + i]);
+    s2 = warp_sum_r(s2);
+    if (lane == 0 && (double)s2 > thr) atomicMax(&last, j);  // the last large column decides
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) lead[s] = min(g.nb, (last + 1 + g.b - 1) / g.b + 1);
+}
+
+// S <- mask(S) / tau^2: rows / columns of the large columns (squared norm = diagonal entry > small2)
+// are zeroed: what remains is the Gram matrix of the small columns W_S
+__global__ void certify_diag_kernel(int n, const cplx<float>* __restrict__ S, float* __restrict__ diag) {
+  const int64_t off = (int64_t)blockIdx.y * n * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    diag[(int64_t)blockIdx.y * n + i] = S[off + (int64_t)i * n + i].re;
+}
+__global__ void certify_mask_kernel(int n, double tau, float small2, const float* __restrict__ diag,
+                                    cplx<float>* __restrict__ S, const int* skip) {
+  if (skip && *skip) return;
+  const int nn = n * n;
+  const int64_t off = (int64_t)blockIdx.y * nn;
+  const float* dg = diag + (int64_t)blockIdx.y * n;
+  const float sc = (float)(1.0 / (tau * tau));
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
+    const int i = l / n, j = l - i * n;
+    cplx<float> v = S[off + l];
+    const bool keep = dg[i] <= small2 && dg[j] <= small2;
+    S[off + l] = cplx<float>{keep ? v.re * sc : 0.f, keep ? v.im * sc : 0.f};
+  }
+}
+
+// a slice whose trace bound fails (or is not finite) becomes active again with every block leading
+__global__ void certify_decide_kernel(int64_t batch, int n, int nb, const cplx<float>* __restrict__ S,
+                                      const int* __restrict__ was_active, int* __restrict__ active,
+                                      int* __restrict__ lead, int* __restrict__ count) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
+    int fail = 0;
+    if (was_active[s] && lead[s] < nb) {
+      double tr = 0.0;
+      for (int i = 0; i < n; ++i) tr += (double)S[s * (int64_t)n * n + (int64_t)i * n + i].re;
+      fail = active[s] || !(tr <= kCertifyBound);  // (still active: the truncated sweeps did not converge)
+    }
+    active[s] = fail;
+    if (fail) {
+      lead[s] = nb;
+      atomicAdd(&cnt, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *count = cnt;
+}
+
+// after the truncated sweeps: certify the trailing columns; *h_failed = slices to finish with full sweeps
+inline int block_certify(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, const cplx<float>* W, double tau,
+                         float small2, const int* was_active, int* active, int* lead, int* count, const int* skip, int* h_failed) {
+  using T = cplx<float>;
+  const int64_t n = g.n, nn = n * n;
+  WsScope ws(ctx);
+  T *S1 = nullptr, *S2 = nullptr;
+  LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &S1));
+  LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &S2));
+  // Gram matrix of the working columns (row j of the n x mp array W is column j; padding rows are zero)
+  LTB_TRY(ltb_gemm_impl(ctx, LTB_C64, batch, n, n, g.mp, LTB_OP_C, W, g.mp, n * g.mp, LTB_OP_T, W, g.mp, n * g.mp, S1,
+                        n, nn, nullptr, nullptr, nullptr, nullptr, nullptr, skip));
+  const dim3 egrid((unsigned)std::min<int64_t>((nn + 1023) / 1024, 64), (unsigned)batch);
+  float* diag = nullptr;
+  LTB_TRY(ws.alloc(sizeof(float) * batch * n, &diag));
+  certify_diag_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)batch), 256, 0, ctx->stream>>>((int)n, S1, diag);
+  LTB_LAUNCH_CHECK(ctx);
+  certify_mask_kernel<<<egrid, 256, 0, ctx->stream>>>((int)n, tau, small2, diag, S1, skip);
+  LTB_LAUNCH_CHECK(ctx);
+  for (int q = 0; q < kCertifySquarings; ++q) {
+    LTB_TRY(ltb_gemm_impl(ctx, LTB_C64, batch, n, n, n, LTB_OP_N, S1, n, nn, LTB_OP_N, S1, n, nn, S2, n, nn, nullptr,
+                          nullptr, nullptr, nullptr, nullptr, skip));
+    std::swap(S1, S2);
+  }
+  certify_decide_kernel<<<1, 256, 0, ctx->stream>>>(batch, (int)n, g.nb, S1, was_active, active, lead, count);
+  LTB_LAUNCH_CHECK(ctx);
+  LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  *h_failed = *reinterpret_cast<int*>(ctx->h_scratch);
+  return LTB_OK;
+}
+
 template <typename T, bool WANT_V>
-int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, const JacobiOut& o,
+int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, const T* A, const JacobiOut& o_in,
                           int max_sweeps) {
+  JacobiOut o = o_in;
   using R = typename scalar_traits<T>::real;
   if (batch > 65535) return ltb_set_error(ctx, LTB_ESHAPE, "svd: batch too large for the blocked tier");
   BlockGeom g;
@@ -1314,7 +1443,7 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
     block_load_kernel<T, WANT_V><<<grid, 256, 0, ctx->stream>>>(I1, I2, A, W, g);
     LTB_LAUNCH_CHECK(ctx);
   }
-  if (g.n > 1) {
+  auto sweeps = [&](int max_sweeps) -> int {
     int st = LTB_OK;
     if constexpr (!WANT_V && (c32 || f32 || f64)) {
       if (o.v_acc) {  // rotation accumulation: blocks of at most ACCB / 2 columns, one warp per column
@@ -1339,6 +1468,39 @@ int launch_jacobi_blocked(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, c
     } else {
       st = run_block_sweeps<T, WANT_V, 0, 1024>(ctx, batch, g, W, rot, active, count, o, max_sweeps, relmax, early);
     }
+    return st;
+  };
+  if (g.n > 1) {
+    bool truncated = false;
+    int* lead = nullptr;
+    int* was_active = nullptr;
+    if constexpr (c32 && !WANT_V) {
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(ctx->stream, &cap);
+      if (o.truncate && o.tau > 0.0 && o.v_acc && cap == cudaStreamCaptureStatusNone && g.nb > 3) {
+        LTB_TRY(ltb_ws_alloc(ctx, sizeof(int) * (size_t)(2 * batch), (void**)&lead));
+        was_active = lead + batch;
+        block_lead_kernel<T><<<(unsigned)batch, 256, 0, ctx->stream>>>(g, W, o.tau, lead);
+        LTB_LAUNCH_CHECK(ctx);
+        LTB_CUDA_TRY(ctx, cudaMemcpyAsync(was_active, active, sizeof(int) * batch, cudaMemcpyDeviceToDevice, ctx->stream));
+        o.lead = lead;
+        o.small2 = (float)((double)kLeadTheta * o.tau * (double)kLeadTheta * o.tau);
+        truncated = true;
+      }
+    }
+    int st = sweeps(truncated ? std::min(max_sweeps, kTruncSweeps) : max_sweeps);
+    if constexpr (c32 && !WANT_V) {
+      if (truncated && st == LTB_OK) {
+        int failed = 0;
+        st = block_certify(ctx, batch, g, W, o.tau, o.small2, was_active, active, lead, count, o.skip, &failed);
+        // full sweeps for the slices without a certificate (lead = every block: no pair is skipped)
+        if (st == LTB_OK && failed > 0) {
+          o.small2 = 0.f;
+          st = sweeps(max_sweeps);
+        }
+      }
+    }
+    if (lead) ltb_ws_free(ctx, lead);
     LTB_TRY(st);
   }
   const size_t fsmem = (size_t)g.n * (sizeof(R) + sizeof(int)) + 16;
@@ -3032,6 +3194,7 @@ int ltb_svt_carry_c64_impl(ltb_ctx* ctx, int64_t batch, int64_t I1, int64_t I2, 
   o.pre_active = pre;
   o.v_acc = VT;
   o.rank_out = rank;
+  o.truncate = warm != 0 && !ctx->opt_full_sweeps;  // (the carried bases are sigma-sorted: the large columns lead)
   LTB_TRY((launch_jacobi_blocked<T, false>(ctx, batch, I1, I2, warm ? A0 : G, o, 40)));
   // Z = D W^H G (rows limited to the kept count), out = W Z (zeros for a slice that keeps nothing)
   LTB_TRY(ltb_gemm_impl(ctx, C, batch, n, I2, m, LTB_OP_C, w, m, n * m, LTB_OP_N, G, I2, S, z, I2, nn, kept, nullptr,

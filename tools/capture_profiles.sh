@@ -12,7 +12,7 @@ python tools/experiments/lprod_fused_time.py > gpurun_out/prof/${R}_lprod_fused_
 ncu --set full --clock-control none --import-source on -k regex:lprod_fused_kernel -s 3 -c 1 -o gpurun_out/prof/${R}_lprod_fused \
     python tools/experiments/lprod_fused_time.py > /dev/null 2>&1
 python tools/experiments/prof_pga_late.py 120 2 > /dev/null 2>&1 && \
-ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:jacobi_qr_kernel -c 1 \
+ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:jacobi_qr_kernel -s 1 -c 1 \
     -o gpurun_out/prof/${R}_jacobi_qr python tools/experiments/prof_pga_late.py 120 2 > /dev/null 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:xform_tile_kernel -c 2 \
     -o gpurun_out/prof/${R}_xform_pga python tools/experiments/prof_pga_late.py 120 2 > /dev/null 2>&1
@@ -25,13 +25,14 @@ ncu --profile-from-start off --set full --clock-control none -k regex:tc3_kernel
     python tools/experiments/cfg4_pga_iters.py 12 1 ncu > /dev/null 2>&1
 python tools/experiments/tsvd_time.py > gpurun_out/prof/${R}_config5_times.txt 2>&1
 python tools/experiments/pga_kernel_breakdown.py 120 5 > gpurun_out/prof/${R}_pga_breakdown.txt 2>&1
+python tools/experiments/pga_kernel_breakdown.py 120 5 fp64 > gpurun_out/prof/${R}_pga_breakdown_fp64.txt 2>&1
 ls -la gpurun_out/prof
 # summaries on the box (the .ncu-rep files together exceed what gpurun copies back): markdown,
 # raw CSV per report, then drop the reports themselves
 P=gpurun_out/prof
 python tools/experiments/ncu_summary.py $P/${R}_ncu_summary.md \
     $P/${R}_lprod_fused.ncu-rep:"config-2 l_product, the one-launch persistent tcgen05 kernel (F, G, I tiles)" \
-    $P/${R}_jacobi_qr.ncu-rep:"config-3 PGA K3 (Cholesky-preconditioned Jacobi, warm iteration 121)" \
+    $P/${R}_jacobi_qr.ncu-rep:"config-3 PGA K3 (Cholesky-preconditioned Jacobi, warm iteration 121; the 296-slice launch of the split batch)" \
     $P/${R}_xform_pga.ncu-rep:"config-3 PGA fused transforms (K1 + K4 prologue, K1' + norms epilogue)" \
     $P/${R}_jacobi_block.ncu-rep:"config-4 PGA, one warm round of the blocked Jacobi with rotation accumulation (complex64 1024x1024, 99 slices x 43 block pairs)" \
     $P/${R}_cgemm_tc.ncu-rep:"config-4 PGA, complex64 GEMM A0 = G V on tcgen05 (real 1024 x 2048 x 2048 per slice, 3xTF32)" \
