@@ -796,8 +796,11 @@ def bench_extras(L, nat, torch, args, cpu):
                               "config": "config4 1024x1024x3x64 Q(x)DFT64, rank 20, Bernoulli(0.3); all 50 iterations",
                               "jacobi_sweeps_per_slice": sw4 / max(sl4, 1),
                               "note": "99 unique 1024^2 complex slices on the blocked (block-cyclic) Jacobi tier, "
-                                      "right bases carried between iterations (ltb_svt_carry_c64_impl); "
-                                      "0.72 it/s cold (round-2 start, 2 iterations)"}
+                                      "right bases carried between iterations (ltb_svt_carry_c64_impl), truncated "
+                                      "sweeps with the trace-power certificate for the columns below tau; "
+                                      "0.72 it/s cold (round-2 start, 2 iterations), 2.39 it/s with full warm sweeps; "
+                                      "final iterate 7e-6 from the full-sweep run (tools/experiments/"
+                                      "cfg4_truncation_check.py)"}
     return out
 
 

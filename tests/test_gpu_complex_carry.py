@@ -185,3 +185,34 @@ def test_config4_recipe_pga_blocked_carry(force_blocked):
     fin = np.isfinite(rr)
     np.testing.assert_array_equal(np.isfinite(rc), fin)
     assert np.max(np.abs(rc[fin] - rr[fin]) / np.maximum(rr[fin], 1e-12)) < 1e-2
+
+
+def test_config4_recipe_256_truncated_vs_oracle_and_full_sweeps():
+    """Config 4's recipe at 256 x 256 x 3 x 8 (complex64 slices beyond shared memory: the carried blocked
+    path with truncated sweeps is what runs by default), 45 iterations: against the fp64 oracle (1e-4) and
+    against the same run with full sweeps (LTB_OPT_FULL_SWEEPS)."""
+    rng = np.random.default_rng(0)
+    shape = (256, 256, 3, 8)
+    q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    f = L.build_fourier_matrix(8)
+    a = rng.standard_normal((256, 8, 3, 8), dtype=np.float32)
+    b = rng.standard_normal((8, 256, 3, 8), dtype=np.float32)
+    spec = L.make_spec("explicit", shape, matrices={3: q, 4: f})
+    ospec = O.ospec("explicit", shape, matrices={3: q, 4: f})
+    m = O.l_product(a.astype(np.float64), b.astype(np.float64), ospec).astype(np.float32)
+    mask = rng.random(m.shape) < 0.3
+    cfg = L.CompletionConfig(spec=spec, tol=1e-300, max_iters=45)
+    nat.jacobi_stats(reset=True)
+    x, trace = L.pga_complete(m, mask, cfg)
+    sl_t, sw_t = nat.jacobi_stats(reset=True)
+    nat.check(nat.lib().ltb_ctx_set_option(nat.context(), nat.OPT_FULL_SWEEPS, 1))
+    try:
+        xf, _ = L.pga_complete(m, mask, cfg)
+    finally:
+        nat.check(nat.lib().ltb_ctx_set_option(nat.context(), nat.OPT_FULL_SWEEPS, 0))
+    ref, recs, _ = O.pga_complete(m.astype(np.float64), mask, ospec, tol=1e-300, max_iters=45)
+    assert trace.iterations == 45
+    assert rel_err(x, ref) < 1e-4
+    assert rel_err(xf, ref) < 1e-4
+    assert rel_err(x, xf) < 1e-4
+    assert np.count_nonzero(x) > 0  # the run got past the all-zero iterations
