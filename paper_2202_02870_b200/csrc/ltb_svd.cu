@@ -1268,8 +1268,9 @@ int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int*
 // W_S: the singular values of the slice are then the norms of W_L's columns together with the
 // singular values of W_S, whatever the angles inside W_S.  The SVT only needs to know that no
 // singular value of W_S exceeds tau: with S = W_S^H W_S / tau^2, lambda_max(S)^64 <= tr(S^64),
-// so tr(S^64) <= 0.9 certifies it (six squarings of the Gram matrix on the tensor cores; the
-// bound is within n^(1/128) = 5.6% of sigma_max(W_S)).  A slice that fails is finished with full
+// so tr(S^64) <= 0.9 certifies it, and so does tr(S^(2^k)) <= 0.9 at any earlier squaring (up to
+// six squarings of the Gram matrix on the tensor cores, stopped once every slice has passed; the
+// last bound is within n^(1/128) = 5.6% of sigma_max(W_S)).  A slice that fails is finished with full
 // sweeps.  lead = the blocks holding the columns with norm above 0.7 tau, plus two blocks.
 constexpr float kLeadTheta = 0.7f;
 constexpr double kCertifyBound = 0.9;
@@ -1318,20 +1319,42 @@ __global__ void certify_mask_kernel(int n, double tau, float small2, const float
   }
 }
 
-// a slice whose trace bound fails (or is not finite) becomes active again with every block leading
-__global__ void certify_decide_kernel(int64_t batch, int n, int nb, const cplx<float>* __restrict__ S,
+// after each squaring: slices whose trace bound already holds pass; once every slice has passed the
+// remaining squarings are skipped (cflags[0], the skip slot of their GEMMs); cflags[1 + s] = passed
+__global__ void certify_init_kernel(int64_t batch, int* __restrict__ cflags, const int* __restrict__ skip) {
+  for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) cflags[1 + s] = 0;
+  if (threadIdx.x == 0) cflags[0] = (skip && *skip) ? 1 : 0;
+}
+__global__ void certify_level_kernel(int64_t batch, int n, int nb, const cplx<float>* __restrict__ S,
+                                     const int* __restrict__ was_active, const int* __restrict__ lead,
+                                     int* __restrict__ cflags) {
+  if (cflags[0]) return;  // (done: S was not updated by the skipped squaring)
+  __shared__ int open_cnt;
+  if (threadIdx.x == 0) open_cnt = 0;
+  __syncthreads();
+  for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
+    if (!was_active[s] || lead[s] >= nb || cflags[1 + s]) continue;
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += (double)S[s * (int64_t)n * n + (int64_t)i * n + i].re;
+    if (tr <= kCertifyBound) cflags[1 + s] = 1;
+    else atomicAdd(&open_cnt, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && open_cnt == 0) cflags[0] = 1;
+}
+
+// a slice without a certificate (or whose truncated sweeps did not converge) becomes active again
+// with every block leading
+__global__ void certify_decide_kernel(int64_t batch, int nb, const int* __restrict__ cflags,
                                       const int* __restrict__ was_active, int* __restrict__ active,
-                                      int* __restrict__ lead, int* __restrict__ count) {
+                                      int* __restrict__ lead, int* __restrict__ count, const int* __restrict__ skip) {
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
+  const bool stop = skip && *skip;
   for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
     int fail = 0;
-    if (was_active[s] && lead[s] < nb) {
-      double tr = 0.0;
-      for (int i = 0; i < n; ++i) tr += (double)S[s * (int64_t)n * n + (int64_t)i * n + i].re;
-      fail = active[s] || !(tr <= kCertifyBound);  // (still active: the truncated sweeps did not converge)
-    }
+    if (!stop && was_active[s] && lead[s] < nb) fail = active[s] || !cflags[1 + s];
     active[s] = fail;
     if (fail) {
       lead[s] = nb;
@@ -1342,31 +1365,38 @@ __global__ void certify_decide_kernel(int64_t batch, int n, int nb, const cplx<f
   if (threadIdx.x == 0) *count = cnt;
 }
 
-// after the truncated sweeps: certify the trailing columns; *h_failed = slices to finish with full sweeps
+// after the truncated sweeps: certify the small columns; *h_failed = slices to finish with full sweeps
 inline int block_certify(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, const cplx<float>* W, double tau,
-                         float small2, const int* was_active, int* active, int* lead, int* count, const int* skip, int* h_failed) {
+                         float small2, const int* was_active, int* active, int* lead, int* count, const int* skip,
+                         int* h_failed) {
   using T = cplx<float>;
   const int64_t n = g.n, nn = n * n;
   WsScope ws(ctx);
   T *S1 = nullptr, *S2 = nullptr;
+  float* diag = nullptr;
+  int* cflags = nullptr;
   LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &S1));
   LTB_TRY(ws.alloc(sizeof(T) * batch * nn, &S2));
+  LTB_TRY(ws.alloc(sizeof(float) * batch * n, &diag));
+  LTB_TRY(ws.alloc(sizeof(int) * (batch + 1), &cflags));
+  certify_init_kernel<<<1, 256, 0, ctx->stream>>>(batch, cflags, skip);
+  LTB_LAUNCH_CHECK(ctx);
   // Gram matrix of the working columns (row j of the n x mp array W is column j; padding rows are zero)
   LTB_TRY(ltb_gemm_impl(ctx, LTB_C64, batch, n, n, g.mp, LTB_OP_C, W, g.mp, n * g.mp, LTB_OP_T, W, g.mp, n * g.mp, S1,
-                        n, nn, nullptr, nullptr, nullptr, nullptr, nullptr, skip));
+                        n, nn, nullptr, nullptr, nullptr, nullptr, nullptr, cflags));
   const dim3 egrid((unsigned)std::min<int64_t>((nn + 1023) / 1024, 64), (unsigned)batch);
-  float* diag = nullptr;
-  LTB_TRY(ws.alloc(sizeof(float) * batch * n, &diag));
   certify_diag_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)batch), 256, 0, ctx->stream>>>((int)n, S1, diag);
   LTB_LAUNCH_CHECK(ctx);
-  certify_mask_kernel<<<egrid, 256, 0, ctx->stream>>>((int)n, tau, small2, diag, S1, skip);
+  certify_mask_kernel<<<egrid, 256, 0, ctx->stream>>>((int)n, tau, small2, diag, S1, cflags);
   LTB_LAUNCH_CHECK(ctx);
   for (int q = 0; q < kCertifySquarings; ++q) {
     LTB_TRY(ltb_gemm_impl(ctx, LTB_C64, batch, n, n, n, LTB_OP_N, S1, n, nn, LTB_OP_N, S1, n, nn, S2, n, nn, nullptr,
-                          nullptr, nullptr, nullptr, nullptr, skip));
+                          nullptr, nullptr, nullptr, nullptr, cflags));
     std::swap(S1, S2);
+    certify_level_kernel<<<1, 256, 0, ctx->stream>>>(batch, (int)n, g.nb, S1, was_active, lead, cflags);
+    LTB_LAUNCH_CHECK(ctx);
   }
-  certify_decide_kernel<<<1, 256, 0, ctx->stream>>>(batch, (int)n, g.nb, S1, was_active, active, lead, count);
+  certify_decide_kernel<<<1, 256, 0, ctx->stream>>>(batch, g.nb, cflags, was_active, active, lead, count, skip);
   LTB_LAUNCH_CHECK(ctx);
   LTB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->h_scratch, count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   LTB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
