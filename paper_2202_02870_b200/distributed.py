@@ -477,7 +477,11 @@ def _dist_pga_device(m_rows, mask_rows, cfg, I1, engine, group, gt_rows, mu0, ch
     gt_sumsq = None
     if gt is not None and cfg.rse_denominator == "original":
         gt_sumsq = float(allsum([float((gt.double() ** 2).sum())])[0])
-    hat_np = np.dtype(forward_dtype(np.dtype(np.float32 if code == nat.F32 else np.float64), engine.spec))
+    # the transform-domain dtype of the COMPUTE precision (as ltb_pga_run: complex of the real compute
+    # dtype for complex specs), not apply_l's return dtype: the reference promotes an explicit-matrix
+    # transform of float32 data to complex128, the fused PGA steps write complex64
+    real_np = np.dtype(np.float32 if code == nat.F32 else np.float64)
+    hat_np = np.dtype(nat.complex_of(real_np)) if engine.spec.is_complex else real_np
     hat_t = _TORCH_DT[hat_np]
     world, rank = _world(group)
     q0, q1 = blocks(P, world)[rank]
