@@ -1314,7 +1314,10 @@ __global__ void certify_mask_kernel(int n, double tau, float small2, const float
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nn; l += gridDim.x * blockDim.x) {
     const int i = l / n, j = l - i * n;
     cplx<float> v = S[off + l];
-    const bool keep = dg[i] <= small2 && dg[j] <= small2;
+    // (a band above the sweeps' threshold: a column whose norm sits within rounding of it may have
+    // been treated as small by a round, so it must be covered by the certificate)
+    const float lim = small2 * 1.001f;
+    const bool keep = dg[i] <= lim && dg[j] <= lim;
     S[off + l] = cplx<float>{keep ? v.re * sc : 0.f, keep ? v.im * sc : 0.f};
   }
 }
