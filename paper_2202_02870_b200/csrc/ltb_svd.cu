@@ -698,6 +698,7 @@ __global__ void block_load_kernel(int64_t I1, int64_t I2, const T* __restrict__ 
 
 // rotation accumulation (JacobiOut::v_acc): blocks of at most ACCB / 2 columns (the 2b values of a
 // V^T element index live in one thread's registers): 24 for complex64 / fp64, 32 for fp32
+constexpr int kLeadMax = 8;  // truncated sweeps: most leading blocks of a slice (more: full sweeps)
 template <typename T> struct acc_dim { static constexpr int value = 0; };
 template <> struct acc_dim<cplx<float>> { static constexpr int value = 24; };
 template <> struct acc_dim<float> { static constexpr int value = 32; };
@@ -747,7 +748,7 @@ template <typename T, bool WANT_V, int MPL, int NTMAX, int ACCB = 0>
 __global__ void __launch_bounds__(NTMAX, 1)
     jacobi_block_kernel(BlockGeom g, int round, int full, T* __restrict__ W, int* __restrict__ rot,
                         const int* __restrict__ active, const int* __restrict__ skip, unsigned* __restrict__ relmax,
-                        T* __restrict__ Vacc, const int* __restrict__ lead, float small2) {
+                        T* __restrict__ Vacc, const int* __restrict__ lead, float small2, int compact) {
   using R = typename scalar_traits<T>::real;
   constexpr bool CPLX = scalar_traits<T>::is_complex;
   if (skip && *skip) return;
@@ -757,7 +758,18 @@ __global__ void __launch_bounds__(NTMAX, 1)
   const int nbp = g.nb + (g.nb & 1), m1 = nbp - 1;
   const int k = blockIdx.x;
   int P, Q;
-  if (k == 0) {
+  if (compact) {
+    // truncated sweeps, compacted grid: CTA i takes leading block i and its partner of this round
+    // (the circle method pairs block m1 with `round` and blocks whose indices sum to 2 round mod m1);
+    // a pair of two leading blocks is taken by the lower one; slices whose every block leads wait
+    // for the full sweeps
+    const int kl = lead[s];
+    if (kl >= g.nb || k >= kl) return;
+    P = k;
+    Q = (k == round) ? m1 : (2 * round - k + 2 * m1) % m1;
+    if (Q == P) Q = m1;  // (2 round = 2 k mod m1 with k != round cannot happen for odd m1; guard anyway)
+    if (Q < kl && Q < P) return;
+  } else if (k == 0) {
     P = m1;
     Q = round;
   } else {
@@ -1242,12 +1254,14 @@ int run_block_sweeps(ltb_ctx* ctx, int64_t batch, const BlockGeom& g, T* W, int*
   LTB_TRY(ensure_smem(ctx, kern, smem));
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(ctx->stream, &cap);
-  const dim3 bgrid((unsigned)(nbp / 2), (unsigned)batch);
+  // truncated sweeps (o.lead with o.small2 > 0): one CTA per leading block, at most kLeadMax per slice
+  const bool compact = o.lead && o.small2 > 0.f;
+  const dim3 bgrid((unsigned)(compact ? std::min(kLeadMax, nbp / 2) : nbp / 2), (unsigned)batch);
   const int threads = 32 * std::min(g.b, NTMAX / 32);
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int r = 0; r < nbp - 1; ++r) {
       kern<<<bgrid, threads, smem, ctx->stream>>>(g, r, r == 0 ? 1 : 0, W, rot, active, o.skip, relmax, vacc,
-                                                  o.lead, o.lead ? o.small2 : 0.f);
+                                                  o.lead, o.lead ? o.small2 : 0.f, compact ? 1 : 0);
       LTB_LAUNCH_CHECK(ctx);
     }
     block_sweep_update_kernel<<<1, 256, 0, ctx->stream>>>(batch, rot, active, count, o.stats, relmax, early);
@@ -1294,7 +1308,10 @@ __global__ void block_lead_kernel(BlockGeom g, const T* __restrict__ W, double t
     if (lane == 0 && (double)s2 > thr) atomicMax(&last, j);  // the last large column decides
   }
   __syncthreads();
-  if (threadIdx.x == 0) lead[s] = min(g.nb, (last + 1 + g.b - 1) / g.b + 1);
+  if (threadIdx.x == 0) {
+    const int kl = (last + 1 + g.b - 1) / g.b + 1;
+    lead[s] = (kl > kLeadMax || kl >= g.nb) ? g.nb : kl;  // (g.nb: not truncated, left to the full sweeps)
+  }
 }
 
 // S <- mask(S) / tau^2: rows / columns of the large columns (squared norm = diagonal entry > small2)
@@ -1357,7 +1374,7 @@ __global__ void certify_decide_kernel(int64_t batch, int nb, const int* __restri
   const bool stop = skip && *skip;
   for (int64_t s = threadIdx.x; s < batch; s += blockDim.x) {
     int fail = 0;
-    if (!stop && was_active[s] && lead[s] < nb) fail = active[s] || !cflags[1 + s];
+    if (!stop && was_active[s]) fail = lead[s] >= nb ? 1 : (active[s] || !cflags[1 + s]);
     active[s] = fail;
     if (fail) {
       lead[s] = nb;
