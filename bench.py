@@ -799,7 +799,7 @@ def bench_extras(L, nat, torch, args, cpu):
                                       "right bases carried between iterations (ltb_svt_carry_c64_impl), truncated "
                                       "sweeps with the trace-power certificate for the columns below tau; "
                                       "0.72 it/s cold (round-2 start, 2 iterations), 2.39 it/s with full warm sweeps; "
-                                      "final iterate 7e-6 from the full-sweep run (tools/experiments/"
+                                      "final iterate 2e-5 from the full-sweep run (tools/experiments/"
                                       "cfg4_truncation_check.py)"}
     return out
 
