@@ -614,12 +614,16 @@ def run_ours(args):
 
 
 def _ncu_traffic(kernel):
-    """dram bytes read + written per launch of `kernel` from the committed ncu capture
-    (profiles/r01_traffic.json, see profiles/r01_ncu_summary.md), or None."""
-    try:
-        return json.load(open(ROOT / "profiles" / "r01_traffic.json")).get(kernel)
-    except (OSError, ValueError):
-        return None
+    """dram bytes read + written per launch of `kernel` from the committed ncu captures
+    (profiles/r02_traffic.json, then r01_traffic.json; see profiles/rNN_ncu_summary.md), or None."""
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            v = json.load(open(ROOT / "profiles" / name)).get(kernel)
+        except (OSError, ValueError):
+            v = None
+        if v is not None:
+            return v
+    return None
 
 
 def bench_pga(L, nat, torch, args):
